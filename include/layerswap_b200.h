@@ -1,0 +1,187 @@
+/*
+ * layerswap_b200.h -- C ABI of the B200-native Pipelined Demand Layering library
+ * (liblayerswap_b200.so).
+ *
+ * Three groups of entry points, one per north_star subsystem:
+ *
+ *   1. Residency policy + performance predictor + schedule model (host code,
+ *      bit-exact with the reference `layerswap` package under CPython 3.12
+ *      float semantics).  Each function replaces one reference function; the
+ *      reference file:line is cited beside the declaration.
+ *   2. The Double-Flat-Buffer (DFB) transfer engine and the model executor
+ *      (CUDA, sm_100a): pinned host arena -> N-slot HBM ring on a dedicated
+ *      copy stream, event hand-off to the compute stream, emulated VRAM cap.
+ *      The reference models this engine in `dfbsim.simulate`
+ *      (pkg/src/layerswap/dfbsim.py:179-247) and has no executable version.
+ *   3. Kernel launchers (raw device pointers + shapes + cudaStream_t) used by
+ *      the executor and by the parity tests.
+ *
+ * Conventions: every function returns int status (LS_OK == 0); on failure
+ * ls_last_error() returns a thread-local message whose wording follows the
+ * reference's exception messages (tests regex-match them).  No torch types
+ * cross this boundary: plain pointers, sizes and POD structs only.
+ */
+#ifndef LAYERSWAP_B200_H
+#define LAYERSWAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------- */
+#define LS_OK 0
+#define LS_ERR_VALUE 1        /* Python ValueError                               */
+#define LS_ERR_INFEASIBLE 2   /* planner.InfeasibleBudgetError (planner.py:34)   */
+#define LS_ERR_CUDA 3         /* CUDA runtime failure -> RuntimeError            */
+#define LS_ERR_CAP 4          /* emulated VRAM cap exceeded -> MemoryError       */
+#define LS_ERR_NCCL 5         /* NCCL failure -> RuntimeError                    */
+
+const char* ls_last_error(void);
+const char* ls_version(void);
+
+/* ---- profile data model (mirror of profile.py:54-166) ---------------------- */
+typedef struct ls_phase {
+  const char* name;
+  int64_t repetitions;     /* PhaseProfile.repetitions  (profile.py:89)  */
+  double dma_ms;           /* PhaseProfile.dma_ms                        */
+  double exe_ms;           /* PhaseProfile.exe_ms                        */
+} ls_phase;
+
+typedef struct ls_module {
+  const char* name;
+  int64_t layers;          /* ModuleProfile.layers (profile.py:107)      */
+  double layer_mem_mb;     /* ModuleProfile.layer_mem_mb                 */
+  int32_t n_phases;
+  const ls_phase* phases;
+} ls_module;
+
+typedef struct ls_profile {
+  double vram_mb;            /* HardwareProfile.vram_mb (profile.py:64)   */
+  double h2d_gbps;
+  double overhead_mb;
+  double always_resident_mb; /* ModelProfile.always_resident_mb (:136)    */
+  int32_t n_modules;
+  const ls_module* modules;
+} ls_profile;
+
+/* SimConfig (dfbsim.py:106-114) */
+#define LS_MODE_SEQUENTIAL 0
+#define LS_MODE_PIPELINED 1
+typedef struct ls_simconfig {
+  int32_t mode;
+  int32_t cross_invocation_prefetch;
+  int32_t slot_count;
+} ls_simconfig;
+
+/* SimEvent (dfbsim.py:117-125).  engine: 0 = copy, 1 = execute. */
+typedef struct ls_event {
+  int32_t engine;
+  int32_t module;
+  int32_t phase;
+  int32_t _pad;
+  int64_t invocation;
+  int64_t layer;
+  double start_ms;
+  double end_ms;
+} ls_event;
+
+/* Placement (dfbsim.py:70-103): a resident mask of sum(layers) bytes laid out
+ * module after module in profile order; mask[off(m) + i] != 0 <=> layer i of
+ * module m is GPU-resident. */
+
+/* Per-layer cost overrides (dfbsim.py:57, _phase_costs :161-176).
+ * costs: for (module m, phase j) with has_override[flat(m,j)] != 0, the
+ * 2*layers doubles (dma0, exe0, dma1, exe1, ...) start at
+ * costs[cost_offset[flat(m,j)]].  flat(m,j) = sum_{m'<m} n_phases(m') + j. */
+typedef struct ls_layer_costs {
+  const uint8_t* has_override;
+  const int64_t* cost_offset;
+  const int64_t* n_entries;   /* entries supplied per (m,j); checked == layers */
+  const double* costs;
+} ls_layer_costs;
+
+/* ---- analytic.py -------------------------------------------------------- */
+/* classify (profile.py:177-187): *kind = 0 exe-intensive, 1 dma-intensive */
+int ls_classify(const ls_phase* ph, int32_t* kind, double* ratio);
+/* phase_time_full_offload (analytic.py:71-77) */
+int ls_phase_time_full_offload(const ls_phase* ph, int64_t layers, double* out);
+/* module_time_full_offload (analytic.py:80-82) */
+int ls_module_time_full_offload(const ls_module* m, double* out);
+/* lower_bound (analytic.py:85-90): per_module[n_modules], total */
+int ls_lower_bound(const ls_profile* p, double* per_module, double* total);
+/* residency_benefit (analytic.py:103-117); position 0 first, 1 middle, 2 last */
+int ls_residency_benefit(const ls_module* m, int32_t position, double* delta_ms,
+                         double* benefit_ms_per_mb);
+/* consecutive_limit (analytic.py:120-132) */
+int ls_consecutive_limit(const ls_phase* ph, int64_t* out);
+/* crossover_tokens (analytic.py:161-171); *out = -1 encodes None */
+int ls_crossover_tokens(const ls_module* target, const ls_module* other, int64_t cap,
+                        int64_t* out);
+
+/* ---- dfbsim.py ---------------------------------------------------------- */
+/* simulate (dfbsim.py:179-247).  events may be NULL (total only, the
+ * simulated_total fast path dfbsim.py:250-256); otherwise capacity must be
+ * >= ls_event_capacity(p). costs may be NULL. */
+int64_t ls_event_capacity(const ls_profile* p);
+int ls_simulate(const ls_profile* p, const uint8_t* resident_mask, const ls_simconfig* cfg,
+                const ls_layer_costs* costs, ls_event* events, int64_t capacity,
+                int64_t* n_events, double* total_ms);
+/* vram_report (dfbsim.py:259-276): out = {buffer, resident, always, overhead, total} */
+int ls_vram_report(const ls_profile* p, const uint8_t* resident_mask, int32_t slot_count,
+                   double out[5], int32_t* fits);
+
+/* ---- planner.py --------------------------------------------------------- */
+/* interleaved_indices (planner.py:67-83): writes k sorted indices */
+int ls_interleaved_indices(int64_t k, int64_t layers, int64_t* out);
+
+typedef struct ls_candidate {  /* Candidate (planner.py:38-47) */
+  int32_t module;
+  int32_t position;            /* 0 first, 1 middle, 2 last */
+  double benefit_ms_per_mb;
+  double delta_ms_per_layer;
+  double layer_mem_mb;
+  int64_t capacity;
+} ls_candidate;
+/* rank_candidates (planner.py:86-116); out must hold 3*n_modules entries */
+int ls_rank_candidates(const ls_profile* p, ls_candidate* out, int32_t* n_out);
+/* fixed_costs_mb (planner.py:119-126) */
+int ls_fixed_costs_mb(const ls_profile* p, int32_t slot_count, double* out);
+/* plan_for_budget (planner.py:145-185). mask_out: sum(layers) bytes.
+ * sim_total is written only when include_simulated != 0. */
+int ls_plan_for_budget(const ls_profile* p, double vram_budget_mb, const ls_simconfig* cfg,
+                       int32_t include_simulated, uint8_t* mask_out, double* saving_ms,
+                       double vram_out[5], int32_t* fits, double* sim_total_ms);
+/* sweep (planner.py:188-206) over interleaved placements of one module */
+int ls_sweep(const ls_profile* p, int32_t module, const int64_t* k_values, int32_t n_k,
+             const ls_simconfig* cfg, double* sim_total_ms, double* vram_total_mb);
+
+/* ---- predictor.py ------------------------------------------------------- */
+/* slope_from_profile (predictor.py:53-59) */
+int ls_slope_from_profile(const ls_module* m, double* out);
+/* predict (predictor.py:62-72) */
+int ls_predict(double intercept_s, double slope_ms_per_layer, const int64_t* k_values,
+               int32_t n, double* predicted_s);
+/* validate (predictor.py:75-104).  Rows come back sorted by k (n_rows = n_pred);
+ * *has_fit = 0 when fewer than two rows (fitted_slope_s is None). */
+int ls_validate(const int64_t* pred_k, const double* pred_s, int32_t n_pred,
+                const int64_t* meas_k, const double* meas_s, int32_t n_meas,
+                int64_t* row_k, double* row_pred, double* row_meas, double* row_err,
+                double* max_abs_err, int32_t* has_fit, double* fitted_slope_s);
+/* resolve_intercept (predictor.py:107-112); *source = 0 measured, 1 simulated.
+ * calibration_total_s < 0 encodes None. */
+int ls_resolve_intercept(const ls_profile* p, double calibration_total_s,
+                         const ls_simconfig* cfg, double* intercept_s, int32_t* source);
+
+/* ---- CPython float helpers (exported for the parity tests) ---------------- */
+double ls_py_sum(const double* x, int64_t n);      /* builtins.sum, CPython 3.12 */
+double ls_py_floordiv(double a, double b);         /* float.__floordiv__          */
+double ls_py_fsum(const double* x, int64_t n);     /* math.fsum                   */
+double ls_py_sumprod(const double* a, const double* b, int64_t n); /* math.sumprod */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAYERSWAP_B200_H */
