@@ -1,0 +1,360 @@
+// attention.cu -- GQA attention kernels.
+//
+// decode_attention: one query token per head against the bf16 KV cache
+//   (flash-decoding split over the context; per-split partials combined by
+//   the last-arriving CTA in split order -> deterministic).  HBM-bound on the
+//   KV bytes: hkv * n_ctx * hd * 2 (K,V) * 2 B per launch.
+// flash_attention: many queries (LM prefill, ViT, action expert) with
+//   bf16 mma.sync m16n8k16 tiles, online softmax in fp32, causal /
+//   block-diagonal (per image) / two-segment KV (expert: VLM cache + own).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsb {
+
+// ------------------------------- decode ---------------------------------------
+
+template <int HD, int G>
+__global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a) {
+  constexpr int E = HD / 32;  // elements per lane
+  const int kh = blockIdx.x, split = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = (a.n_ctx + a.n_split - 1) / a.n_split;
+  const int p0 = split * chunk, p1 = min(a.n_ctx, p0 + chunk);
+  const float sl2 = a.scale * 1.4426950408889634f;
+
+  float qv[G][E];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < E; ++e) qv[g][e] = a.q[(kh * G + g) * HD + lane * E + e] * sl2;
+
+  float m[G], l[G], acc[G][E];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[g][e] = 0.f;
+  }
+  const bf16* kb = a.k_cache + static_cast<long>(kh) * a.cache_head_stride;
+  const bf16* vb = a.v_cache + static_cast<long>(kh) * a.cache_head_stride;
+  for (int p = p0 + warp; p < p1; p += 4) {
+    float kv[E], vv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      kv[e] = bf2f(kb[static_cast<long>(p) * HD + lane * E + e]);
+      vv[e] = bf2f(vb[static_cast<long>(p) * HD + lane * E + e]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float s = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) s = fmaf(qv[g][e], kv[e], s);
+      s = warp_sum(s);
+      const float mn = fmaxf(m[g], s);
+      const float corr = exp2f(m[g] - mn), pe = exp2f(s - mn);
+      l[g] = l[g] * corr + pe;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[g][e] = acc[g][e] * corr + pe * vv[e];
+      m[g] = mn;
+    }
+  }
+  // combine the 4 warps of this CTA
+  __shared__ float sm_m[4][G], sm_l[4][G];
+  __shared__ float sm_o[4][G][HD];
+  __shared__ int s_last;
+  if (lane == 0)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      sm_m[warp][g] = m[g];
+      sm_l[warp][g] = l[g];
+    }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm_o[warp][g][lane * E + e] = acc[g][e];
+  __syncthreads();
+  // thread layout for the combine: idx over G*HD
+  const int W = HD + 2;  // workspace record: M, L, O[HD]
+  for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
+    const int g = idx / HD, d = idx % HD;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][g]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY)
+      for (int w = 0; w < 4; ++w) {
+        const float f = exp2f(sm_m[w][g] - M);
+        L += sm_l[w][g] * f;
+        O += sm_o[w][g][d] * f;
+      }
+    const int h = kh * G + g;
+    if (a.n_split == 1) {
+      a.out[h * HD + d] = O / L;
+    } else {
+      float* rec = a.ws + (static_cast<long>(h) * a.n_split + split) * W;
+      rec[2 + d] = O;
+      if (d == 0) {
+        rec[0] = M;
+        rec[1] = L;
+      }
+    }
+  }
+  if (a.n_split == 1) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[kh], 1) == a.n_split - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
+    const int g = idx / HD, d = idx % HD, h = kh * G + g;
+    const float* rec = a.ws + static_cast<long>(h) * a.n_split * W;
+    float M = -INFINITY;
+    for (int s = 0; s < a.n_split; ++s) M = fmaxf(M, __ldcg(rec + s * W));
+    float L = 0.f, O = 0.f;
+    for (int s = 0; s < a.n_split; ++s) {
+      const float ms = __ldcg(rec + s * W);
+      if (ms == -INFINITY) continue;
+      const float f = exp2f(ms - M);
+      L += __ldcg(rec + s * W + 1) * f;
+      O += __ldcg(rec + s * W + 2 + d) * f;
+    }
+    a.out[h * HD + d] = O / L;
+  }
+  if (threadIdx.x == 0) a.counters[kh] = 0;
+}
+
+template <int HD>
+static cudaError_t decode_hd(const DecodeAttnArgs& a, cudaStream_t st) {
+  dim3 grid(a.hkv, a.n_split);
+  switch (a.hq / a.hkv) {
+    case 1: decode_attn_kernel<HD, 1><<<grid, 128, 0, st>>>(a); break;
+    case 2: decode_attn_kernel<HD, 2><<<grid, 128, 0, st>>>(a); break;
+    case 4: decode_attn_kernel<HD, 4><<<grid, 128, 0, st>>>(a); break;
+    case 8: decode_attn_kernel<HD, 8><<<grid, 128, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
+  switch (a.hd) {
+    case 32: return decode_hd<32>(a, st);
+    case 64: return decode_hd<64>(a, st);
+    case 128: return decode_hd<128>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------- flash ----------------------------------------
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t& r0, uint32_t& r1, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(p)));
+}
+
+template <int HD>
+struct FlashCfg {
+  static constexpr int kDK = (HD + 15) / 16 * 16;  // QK^T contraction, padded to k16
+  static constexpr int kLd = kDK + 8;              // smem row pitch (bank spread)
+  static constexpr int kND = HD / 8;               // PV n-tiles of 8
+  static constexpr int kBM = 64, kBN = 64;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
+  using Cfg = FlashCfg<HD>;
+  constexpr int DK = Cfg::kDK, LD = Cfg::kLd, ND = Cfg::kND, BM = Cfg::kBM, BN = Cfg::kBN;
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+  extern __shared__ __align__(16) uint8_t fsm[];
+  bf16* qs = reinterpret_cast<bf16*>(fsm);
+  bf16* ks = qs + BM * LD;
+  bf16* vs = ks + BN * LD;
+
+  const int h = blockIdx.y, kvh = h / (a.hq / a.hkv);
+  const int q0 = blockIdx.x * BM;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const float sl2 = a.scale * 1.4426950408889634f;
+
+  // ---- Q tile -> smem (zero padded) ----
+  for (int i = threadIdx.x; i < BM * (DK / 8); i += 128) {
+    const int r = i / (DK / 8), c = i % (DK / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (q0 + r < a.Tq && c < CH)
+      v = *reinterpret_cast<const uint4*>(a.q + static_cast<long>(q0 + r) * a.q_tok_stride +
+                                          static_cast<long>(h) * a.q_head_stride + c * 8);
+    *reinterpret_cast<uint4*>(qs + r * LD + c * 8) = v;
+  }
+  __syncthreads();
+  uint32_t qf[DK / 16][4];
+  {
+    const bf16* qr = qs + (warp * 16) * LD;
+#pragma unroll
+    for (int kk = 0; kk < DK / 16; ++kk) {
+      qf[kk][0] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 2 * t4);
+      qf[kk][1] = *reinterpret_cast<const uint32_t*>(qr + (g + 8) * LD + kk * 16 + 2 * t4);
+      qf[kk][2] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 8 + 2 * t4);
+      qf[kk][3] = *reinterpret_cast<const uint32_t*>(qr + (g + 8) * LD + kk * 16 + 8 + 2 * t4);
+    }
+  }
+  float o[ND][4];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int qi[2] = {q0 + warp * 16 + g, q0 + warp * 16 + g + 8};
+
+  const int n_keys = a.len1 + a.len2;
+  int k_begin = 0, k_end = n_keys;
+  if (a.seg_len > 0) {
+    const int img = q0 / a.seg_len;
+    k_begin = img * a.seg_len;
+    k_end = min(n_keys, k_begin + a.seg_len);
+  }
+  if (a.causal) k_end = min(k_end, q0 + BM + a.q_offset);
+
+  for (int j0 = k_begin; j0 < k_end; j0 += BN) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < BN * (DK / 8); i += 128) {
+      const int r = i / (DK / 8), c = i % (DK / 8);
+      const int j = j0 + r;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (j < k_end && c < CH) {
+        const bf16 *kp, *vp;
+        if (j < a.len1) {
+          const long off = static_cast<long>(j) * a.k1_tok_stride + static_cast<long>(kvh) * a.k1_head_stride + c * 8;
+          kp = a.k1 + off;
+          vp = a.v1 + off;
+        } else {
+          const long off = static_cast<long>(j - a.len1) * a.k2_tok_stride + static_cast<long>(kvh) * a.k2_head_stride + c * 8;
+          kp = a.k2 + off;
+          vp = a.v2 + off;
+        }
+        kv = *reinterpret_cast<const uint4*>(kp);
+        vv = *reinterpret_cast<const uint4*>(vp);
+      }
+      *reinterpret_cast<uint4*>(ks + r * LD + c * 8) = kv;
+      *reinterpret_cast<uint4*>(vs + r * LD + c * 8) = vv;
+    }
+    __syncthreads();
+    // S = Q K^T  (16 x 64 per warp)
+    float s[BN / 8][4];
+#pragma unroll
+    for (int nt = 0; nt < BN / 8; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+      const bf16* kr = ks + (nt * 8 + g) * LD;
+#pragma unroll
+      for (int kk = 0; kk < DK / 16; ++kk) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 2 * t4);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8 + 2 * t4);
+        mma_bf16_16816(s[nt], qf[kk], b0, b1);
+      }
+    }
+    // mask + online softmax (rows g and g+8 of this warp)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < BN / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = j0 + nt * 8 + 2 * t4 + e;
+          float v = s[nt][2 * r + e] * sl2;
+          bool ok = j < k_end && qi[r] < a.Tq;
+          if (a.causal) ok = ok && (j <= qi[r] + a.q_offset);
+          v = ok ? v : -INFINITY;
+          s[nt][2 * r + e] = v;
+          mx = fmaxf(mx, v);
+        }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mnew = fmaxf(mrow[r], mx);
+      const float base = mnew == -INFINITY ? 0.f : mnew;
+      const float corr = exp2f(mrow[r] - base);
+      float rs = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < BN / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float p = exp2f(s[nt][2 * r + e] - base);
+          s[nt][2 * r + e] = p;
+          rs += p;
+        }
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      lrow[r] = lrow[r] * corr + rs;
+      mrow[r] = mnew;
+#pragma unroll
+      for (int j = 0; j < ND; ++j) {
+        o[j][2 * r] *= corr;
+        o[j][2 * r + 1] *= corr;
+      }
+    }
+    // O += P V
+#pragma unroll
+    for (int kk = 0; kk < BN / 16; ++kk) {
+      uint32_t pa[4];
+      pa[0] = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
+      pa[1] = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
+      pa[2] = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+      pa[3] = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+      for (int dt = 0; dt < ND; ++dt) {
+        uint32_t b0, b1;
+        ldsm_x2_trans(b0, b1, vs + (kk * 16 + (lane & 15)) * LD + dt * 8);
+        mma_bf16_16816(o[dt], pa, b0, b1);
+      }
+    }
+  }
+  // normalise + store
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (qi[r] >= a.Tq) continue;
+    const float inv = lrow[r] > 0.f ? 1.0f / lrow[r] : 0.f;
+    bf16* op = a.out + static_cast<long>(qi[r]) * a.o_tok_stride + static_cast<long>(h) * a.o_head_stride;
+#pragma unroll
+    for (int dt = 0; dt < ND; ++dt)
+      *reinterpret_cast<uint32_t*>(op + dt * 8 + 2 * t4) =
+          pack_bf16x2(o[dt][2 * r] * inv, o[dt][2 * r + 1] * inv);
+  }
+}
+
+template <int HD>
+static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
+  using Cfg = FlashCfg<HD>;
+  const size_t smem = static_cast<size_t>(Cfg::kBM + 2 * Cfg::kBN) * Cfg::kLd * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq);
+  flash_kernel<HD><<<grid, 128, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {
+  if (a.Tq <= 0) return cudaSuccess;
+  switch (a.hd) {
+    case 32: return flash_hd<32>(a, st);
+    case 64: return flash_hd<64>(a, st);
+    case 72: return flash_hd<72>(a, st);
+    case 128: return flash_hd<128>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lsb

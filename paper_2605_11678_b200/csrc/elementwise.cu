@@ -1,0 +1,269 @@
+// elementwise.cu -- row norms, q/k-norm + RoPE + KV append for prefill,
+// embeddings, the action-expert input/output heads and small glue kernels.
+// All HBM-bound and tiny next to the weight streams; one CTA per row where a
+// row reduction is needed, vectorised 16-byte accesses where rows allow.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsb {
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (blockDim.x >> 5); ++i) t += sh[i];
+  return t;
+}
+
+// RMSNorm over rows of an fp32 [T x D] residual stream -> bf16 GEMM operand.
+__global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, int D, float eps) {
+  __shared__ float sh[32];
+  const float* xr = x + static_cast<long>(blockIdx.x) * D;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
+  const float rstd = rsqrtf(block_sum(ss, sh) / D + eps);
+  bf16* o = out + static_cast<long>(blockIdx.x) * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) o[i] = f2bf(xr[i] * rstd * bf2f(w[i]));
+}
+
+cudaError_t launch_rmsnorm_rows(const float* x, const bf16* w, bf16* out, int T, int D, float eps,
+                                cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  rmsnorm_rows_kernel<<<T, 256, 0, st>>>(x, w, out, D, eps);
+  return cudaGetLastError();
+}
+
+__global__ void layernorm_rows_kernel(const float* x, const bf16* w, const bf16* b, bf16* out,
+                                      int D, long ld_out, float eps) {
+  __shared__ float sh[32];
+  const float* xr = x + static_cast<long>(blockIdx.x) * D;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) s += xr[i];
+  const float mean = block_sum(s, sh) / D;
+  float v2 = 0.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float d = xr[i] - mean;
+    v2 = fmaf(d, d, v2);
+  }
+  const float rstd = rsqrtf(block_sum(v2, sh) / D + eps);
+  bf16* o = out + static_cast<long>(blockIdx.x) * ld_out;
+  for (int i = threadIdx.x; i < D; i += blockDim.x)
+    o[i] = f2bf((xr[i] - mean) * rstd * bf2f(w[i]) + bf2f(b[i]));
+}
+
+cudaError_t launch_layernorm_rows(const float* x, const bf16* w, const bf16* b, bf16* out, int T,
+                                  int D, long ld_out, float eps, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  layernorm_rows_kernel<<<T, 256, 0, st>>>(x, w, b, out, D, ld_out, eps);
+  return cudaGetLastError();
+}
+
+// Prefill q/k RMSNorm + RoPE; K,V appended to the cache at positions pos0+t.
+// One CTA per token, one warp per head.
+__global__ void qk_norm_rope_kernel(const bf16* qkv, int hq, int hkv, int hd, const bf16* qn_w,
+                                    const bf16* kn_w, float eps, const float2* rope, int pos0,
+                                    bf16* q_out, bf16* k_cache, bf16* v_cache,
+                                    int cache_head_stride) {
+  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nh = hq + 2 * hkv;
+  const int row_len = nh * hd;
+  const int pos = pos0 + t;
+  const int h2 = hd / 2;
+  for (int head = warp; head < nh; head += blockDim.x >> 5) {
+    const bf16* src = qkv + static_cast<long>(t) * row_len + head * hd;
+    const bool is_q = head < hq, is_k = !is_q && head < hq + hkv;
+    if (!is_q && !is_k) {
+      const int vh = head - hq - hkv;
+      bf16* dst = v_cache + static_cast<long>(vh) * cache_head_stride + static_cast<long>(pos) * hd;
+      for (int d = lane; d < hd; d += 32) dst[d] = src[d];
+      continue;
+    }
+    float ss = 0.f;
+    for (int d = lane; d < hd; d += 32) {
+      const float v = bf2f(src[d]);
+      ss = fmaf(v, v, ss);
+    }
+    const bf16* nw = is_q ? qn_w : kn_w;
+    const float rstd = nw ? rsqrtf(warp_sum(ss) / hd + eps) : 1.0f;
+    auto normed = [&](int d) {
+      const float v = bf2f(src[d]) * rstd;
+      return nw ? v * bf2f(nw[d]) : v;
+    };
+    bf16* dst = is_q ? q_out + (static_cast<long>(t) * hq + head) * hd
+                     : k_cache + static_cast<long>(head - hq) * cache_head_stride +
+                           static_cast<long>(pos) * hd;
+    for (int d = lane; d < hd; d += 32) {
+      const int f = d < h2 ? d : d - h2;
+      const float2 cs = rope[static_cast<long>(pos) * h2 + f];
+      const float v = normed(d);
+      const float o = d < h2 ? v * cs.x - normed(d + h2) * cs.y : v * cs.x + normed(d - h2) * cs.y;
+      dst[d] = f2bf(o);
+    }
+  }
+}
+
+cudaError_t launch_qk_norm_rope(const bf16* qkv, int T, int hq, int hkv, int hd, const bf16* qn_w,
+                                const bf16* kn_w, float eps, const float2* rope, int pos0,
+                                bf16* q_out, bf16* k_cache, bf16* v_cache, int cache_head_stride,
+                                cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  qk_norm_rope_kernel<<<T, 256, 0, st>>>(qkv, hq, hkv, hd, qn_w, kn_w, eps, rope, pos0, q_out,
+                                         k_cache, v_cache, cache_head_stride);
+  return cudaGetLastError();
+}
+
+__global__ void embed_rows_kernel(const bf16* table, const int* ids, int D, float* out, long ld) {
+  const int id = ids[blockIdx.x];
+  const bf16* src = table + static_cast<long>(id) * D;
+  float* dst = out + static_cast<long>(blockIdx.x) * ld;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) dst[i] = bf2f(src[i]);
+}
+
+cudaError_t launch_embed_rows(const bf16* table, const int* ids, int n, int D, float* out,
+                              long ld_out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  embed_rows_kernel<<<n, 256, 0, st>>>(table, ids, D, out, ld_out);
+  return cudaGetLastError();
+}
+
+// x[t, :] += add[t % period, :]   (learned ViT position embedding per image)
+__global__ void add_rows_kernel(float* x, const bf16* add, int D, int period) {
+  const int t = blockIdx.x;
+  const bf16* a = add + static_cast<long>(t % period) * D;
+  float* xr = x + static_cast<long>(t) * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) xr[i] += bf2f(a[i]);
+}
+
+cudaError_t launch_add_rows_bf16(float* x, const bf16* add, int T, int D, long period,
+                                 cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  add_rows_kernel<<<T, 256, 0, st>>>(x, add, D, static_cast<int>(period));
+  return cudaGetLastError();
+}
+
+__global__ void cast_kernel(const float* x, bf16* out, long n) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    out[i] = f2bf(x[i]);
+}
+
+cudaError_t launch_cast_f32_bf16(const float* x, bf16* out, long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  cast_kernel<<<296, 256, 0, st>>>(x, out, n);
+  return cudaGetLastError();
+}
+
+// Greedy decode bookkeeping: key -> token id (+ history), re-arm the key.
+__global__ void argmax_to_token_kernel(const unsigned long long* key, int* token_out, int* history,
+                                       int step, unsigned long long* key_reset) {
+  const unsigned long long k = *key;
+  const int idx = static_cast<int>(0xffffffffu - static_cast<uint32_t>(k & 0xffffffffull));
+  *token_out = idx;
+  if (history) history[step] = idx;
+  if (key_reset) *key_reset = 0ull;
+}
+
+cudaError_t launch_argmax_to_token(const unsigned long long* key, int* token_out, int* history,
+                                   int step, unsigned long long* key_reset, cudaStream_t st) {
+  argmax_to_token_kernel<<<1, 1, 0, st>>>(key, token_out, history, step, key_reset);
+  return cudaGetLastError();
+}
+
+__global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
+}
+
+cudaError_t launch_fill_u64(unsigned long long* p, unsigned long long v, int n, cudaStream_t st) {
+  fill_u64_kernel<<<1, 128, 0, st>>>(p, v, n);
+  return cudaGetLastError();
+}
+
+// Sinusoidal flow-time features: out[i] = sin(t * f_i) | cos(t * f_i), f_i = 1e4^(-i/(dim/2)).
+__global__ void time_embed_kernel(const float* t_table, int step, int dim, bf16* out) {
+  const float t = t_table[step];
+  const int half = dim / 2;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float f = expf(-9.210340371976184f * i / half);  // ln(1e4)
+    out[i] = f2bf(sinf(t * f));
+    out[half + i] = f2bf(cosf(t * f));
+  }
+}
+
+cudaError_t launch_time_embed(const float* t_table, int step, int dim, bf16* out, cudaStream_t st) {
+  time_embed_kernel<<<1, 128, 0, st>>>(t_table, step, dim, out);
+  return cudaGetLastError();
+}
+
+// Action-token input: h[i, :] = W_in . a_i + b_in + temb   (K = action dim, tiny).
+__global__ void action_in_kernel(const float* actions, const bf16* w_in, const bf16* b_in,
+                                 const float* temb, int a_dim, int D, float* out) {
+  const int i = blockIdx.x;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float s = bf2f(b_in[d]) + temb[d];
+    for (int k = 0; k < a_dim; ++k) s = fmaf(bf2f(w_in[d * a_dim + k]), actions[i * a_dim + k], s);
+    out[static_cast<long>(i) * D + d] = s;
+  }
+}
+
+cudaError_t launch_action_in(const float* actions, const bf16* w_in, const bf16* b_in,
+                             const float* temb, int n_tok, int a_dim, int D, float* out,
+                             cudaStream_t st) {
+  action_in_kernel<<<n_tok, 256, 0, st>>>(actions, w_in, b_in, temb, a_dim, D, out);
+  return cudaGetLastError();
+}
+
+// Final RMSNorm + velocity head (D -> a_dim) + explicit Euler step a += dt * v.
+__global__ void action_out_euler_kernel(const float* h, const bf16* norm_w, float eps,
+                                        const bf16* w_out, const bf16* b_out, int D, int a_dim,
+                                        float dt, float* actions, float* velocity) {
+  __shared__ float sh[32];
+  __shared__ float part[8][8];
+  const int i = blockIdx.x;
+  const float* hr = h + static_cast<long>(i) * D;
+  float ss = 0.f;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) ss = fmaf(hr[d], hr[d], ss);
+  const float rstd = rsqrtf(block_sum(ss, sh) / D + eps);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = 0; k < a_dim; ++k) {
+    float s = 0.f;
+    for (int d = threadIdx.x; d < D; d += blockDim.x)
+      s = fmaf(hr[d] * rstd * bf2f(norm_w[d]), bf2f(w_out[k * D + d]), s);
+    s = warp_sum(s);
+    if (lane == 0) part[k][warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < a_dim) {
+    const int k = threadIdx.x;
+    float v = bf2f(b_out[k]);
+    for (int w = 0; w < (blockDim.x >> 5); ++w) v += part[k][w];
+    if (velocity) velocity[i * a_dim + k] = v;
+    actions[i * a_dim + k] += dt * v;
+  }
+}
+
+cudaError_t launch_action_out_euler(const float* h, const bf16* norm_w, float eps,
+                                    const bf16* w_out, const bf16* b_out, int n_tok, int D,
+                                    int a_dim, float dt, float* actions, float* velocity,
+                                    cudaStream_t st) {
+  if (a_dim > 8) return cudaErrorInvalidValue;
+  action_out_euler_kernel<<<n_tok, 256, 0, st>>>(h, norm_w, eps, w_out, b_out, D, a_dim, dt,
+                                                 actions, velocity);
+  return cudaGetLastError();
+}
+
+// SiLU in place (time-MLP hidden).
+__global__ void silu_kernel(float* x, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = silu(x[i]);
+}
+
+cudaError_t launch_silu_inplace(float* x, int n, cudaStream_t st) {
+  silu_kernel<<<(n + 255) / 256, 256, 0, st>>>(x, n);
+  return cudaGetLastError();
+}
+
+}  // namespace lsb

@@ -1,0 +1,225 @@
+// gemm_sm100.cu -- tcgen05 tensor-core GEMM for the dense (prefill / ViT /
+// action-expert) contractions:  Y[T x N] = X[T x K] . W[N x K]^T.
+//
+// Roofline: tensor pipe (2*T*N*K FLOP per launch) for T >= ~256; weight-HBM
+// bound for the 64-token expert.  B200 mapping:
+//   * weights are the MMA "A" operand (M = 128 output features per CTA),
+//     tokens are "B" (N = BN tokens), so the 64-token expert still issues
+//     full-height M=128 MMAs;
+//   * A tiles are pre-swizzled in HBM (see common.cuh), one 16 KiB 1-D bulk
+//     copy per stage; B tiles come through a 2-D TMA tensor map with
+//     SWIZZLE_128B -- both land in the UMMA K-major SW128 layout;
+//   * warp 0: TMA producer, warp 1: TMEM allocator + single-thread MMA issuer
+//     (tcgen05.mma.cta_group::1.kind::f16, accumulator in TMEM), warps 2-5:
+//     epilogue (tcgen05.ld -> fused bias / GELU / SiLU*up / residual -> HBM);
+//   * mbarrier full/empty ring, tcgen05.commit releases smem stages.
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsb {
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kABytes = kTileBytes;
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes +
+                                  128 * 17 * 4 + (2 * kStages + 2) * 8 + 16;
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmArgs a) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + Cfg::kStages * Cfg::kABytes;
+  float* stage_f = reinterpret_cast<float*>(sb + Cfg::kStages * Cfg::kBBytes);  // [128][17]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_f + 128 * 17);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* accf = empty + Cfg::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.x, n0 = blockIdx.y * BN;
+  const int n_kb = a.n_kb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    fence_barrier_init();
+    prefetch_tmap(&xmap);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer ----
+      const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kTileBytes;
+      for (int kb = 0; kb < n_kb; ++kb) {
+        const int s = kb % Cfg::kStages;
+        if (kb >= Cfg::kStages) mbar_wait(&empty[s], ((kb / Cfg::kStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+        bulk_g2s(sa + s * Cfg::kABytes, wt + static_cast<long>(kb) * kTileBytes, kTileBytes, &full[s]);
+        tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- single-thread MMA issuer ----
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
+      for (int kb = 0; kb < n_kb; ++kb) {
+        const int s = kb % Cfg::kStages;
+        mbar_wait(&full[s], (kb / Cfg::kStages) & 1);
+        tc_fence_after();
+        const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
+        const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
+#pragma unroll
+        for (int k = 0; k < kTileCols / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+          umma_bf16(tmem, da + 2ull * k, db + 2ull * k, idesc, (kb | k) ? 1u : 0u);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(accf);
+    }
+    __syncwarp();
+  } else {  // ---- epilogue warps 2..5 ----
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int m = q * 32 + lane;
+    const int f = mt * kTileRows + m;
+    mbar_wait(accf, 0);
+    tc_fence_after();
+    float bias = 0.f;
+    if (f < a.n_valid) {
+      if (a.bias) bias = a.bias[f];
+      else if (a.bias_bf16) bias = bf2f(a.bias_bf16[f]);
+    }
+    const int etid = threadIdx.x - 64;  // 0..127
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+      if constexpr (EPI == GEMM_SILU_BF16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) stage_f[m * 17 + i] = v[i];
+        named_bar(2, 128);
+        if (m < 64) {
+          const int g = mt * 64 + m;
+          bf16* out = static_cast<bf16*>(a.out);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int t = n0 + c0 + i;
+            if (t < a.T && g < a.n_valid)
+              out[static_cast<long>(t) * a.ldo + g] = f2bf(silu(stage_f[m * 17 + i]) * stage_f[(m + 64) * 17 + i]);
+          }
+        }
+        named_bar(2, 128);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int t = n0 + c0 + i;
+          if (t >= a.T) break;
+          const long o = static_cast<long>(t) * a.ldo + f;
+          const float y = v[i] + bias;
+          if constexpr (EPI == GEMM_BF16) static_cast<bf16*>(a.out)[o] = f2bf(y);
+          else if constexpr (EPI == GEMM_BF16_GELU) static_cast<bf16*>(a.out)[o] = f2bf(gelu_tanh(y));
+          else if constexpr (EPI == GEMM_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] = y; }
+          else if constexpr (EPI == GEMM_RESID_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] += y; }
+        }
+      }
+    }
+    (void)etid;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, Cfg::kTmemCols);
+  }
+}
+
+int gemm_block_n(int T) { return T <= 64 ? 64 : 128; }
+
+template <int BN, int EPI>
+static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(a.n_mt, (a.T + BN - 1) / BN);
+  gemm_kernel<BN, EPI><<<grid, 192, Cfg::kSmem, st>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t launch_epi(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  switch (epi) {
+    case GEMM_BF16: return launch_bn<BN, GEMM_BF16>(a, map, st);
+    case GEMM_BF16_GELU: return launch_bn<BN, GEMM_BF16_GELU>(a, map, st);
+    case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32>(a, map, st);
+    case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16>(a, map, st);
+    case GEMM_F32: return launch_bn<BN, GEMM_F32>(a, map, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  if (a.T <= 0) return cudaSuccess;
+  switch (gemm_block_n(a.T)) {
+    case 64: return launch_epi<64>(epi, a, map, st);
+    default: return launch_epi<128>(epi, a, map, st);
+  }
+}
+
+// ---- tensor-map encoding through the driver entry point (no -lcuda) ----------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t ld_elems, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
+}
+
+}  // namespace lsb

@@ -1,0 +1,290 @@
+// gemv.cu -- decode-time (batch 1) matrix-vector product over tiled weights.
+//
+// Roofline: HBM.  Algorithmic bytes per launch = N*K*2 (weights, read once)
+// + K*4 (x) + N*4 (y).  Design for B200:
+//   * persistent grid (<= 148 CTAs, one per SM); the flattened (m-tile,
+//     k-block) tile sequence is split into equal contiguous ranges (stream-K),
+//     so every SM streams the same number of 16 KiB tiles regardless of shape;
+//   * one producer warp issues 1-D bulk copies (TMA engine, L2 evict-first)
+//     into an 8-stage shared-memory ring guarded by mbarriers -- 128 KiB in
+//     flight per SM, no registers spent on loads;
+//   * eight consumer warps dot the swizzled tile rows with x (fp32, resident
+//     in shared memory, RMSNorm fused in the prologue) and keep per-row
+//     partials in registers across a CTA's whole k-range;
+//   * m-tiles split across CTAs are fixed up deterministically: partials land
+//     in a workspace slot per contributor and the last arriving CTA sums them
+//     in contributor order (bit-reproducible), then runs the fused epilogue
+//     (residual add / SiLU*up / q,k-norm + RoPE + KV-cache append / argmax).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsb {
+
+constexpr int kGemvStages = 8;
+constexpr int kGemvConsumers = 256;  // 8 warps
+constexpr int kGemvThreads = kGemvConsumers + 32;
+
+__device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
+  return static_cast<int>(((t + 1) * G - 1) / T);
+}
+
+__device__ __forceinline__ float dot8(uint4 w, const float4& a, const float4& b) {
+  float s = bf16_lo(w.x) * a.x;
+  s = fmaf(bf16_hi(w.x), a.y, s);
+  s = fmaf(bf16_lo(w.y), a.z, s);
+  s = fmaf(bf16_hi(w.y), a.w, s);
+  s = fmaf(bf16_lo(w.z), b.x, s);
+  s = fmaf(bf16_hi(w.z), b.y, s);
+  s = fmaf(bf16_lo(w.w), b.z, s);
+  s = fmaf(bf16_hi(w.w), b.w, s);
+  return s;
+}
+
+template <int EPI>
+__device__ void gemv_epilogue(const GemvArgs& a, int mt, const float* red, int tid) {
+  // tid in [0,128): one output row each
+  const int row = mt * kTileRows + tid;
+  float y = red[tid];
+  if constexpr (EPI == GEMV_F32 || EPI == GEMV_RESID) {
+    if (row < a.n_valid) {
+      if (a.bias) y += a.bias[row];
+      if constexpr (EPI == GEMV_F32) a.out[row] = y;
+      else a.out[row] += y;
+    }
+  } else if constexpr (EPI == GEMV_SILU) {
+    if (tid < 64) {
+      const int f = mt * 64 + tid;
+      if (f < a.n_valid) a.out[f] = silu(y) * red[tid + 64];
+    }
+  } else if constexpr (EPI == GEMV_QKV) {
+    const int hd = a.hd, h2 = hd >> 1;
+    const int q_rows = a.hq * hd, k_rows = a.hkv * hd;
+    if (row >= q_rows + 2 * k_rows) return;
+    const int d = row % hd;
+    const int head_base = tid - d;  // rows of one head never straddle a tile (hd | 128)
+    const bool is_v = row >= q_rows + k_rows;
+    if (is_v) {
+      const int kh = (row - q_rows - k_rows) / hd;
+      a.v_cache[(long)kh * a.cache_head_stride + (long)a.pos * hd + d] = f2bf(y);
+      return;
+    }
+    const bool is_q = row < q_rows;
+    float rstd = 1.0f;
+    const bf16* nw = is_q ? a.qn_w : a.kn_w;
+    if (nw) {
+      float ss = 0.f;
+      for (int i = 0; i < hd; ++i) ss = fmaf(red[head_base + i], red[head_base + i], ss);
+      rstd = rsqrtf(ss / hd + a.eps);
+    }
+    auto normed = [&](int dd) {
+      float v = red[head_base + dd] * rstd;
+      return nw ? v * bf2f(nw[dd]) : v;
+    };
+    const int f = d < h2 ? d : d - h2;
+    const float2 cs = a.rope[(long)a.pos * h2 + f];
+    float v = normed(d);
+    float o = d < h2 ? v * cs.x - normed(d + h2) * cs.y : v * cs.x + normed(d - h2) * cs.y;
+    if (is_q) {
+      a.q_out[row] = o;
+    } else {
+      const int kh = (row - q_rows) / hd;
+      a.k_cache[(long)kh * a.cache_head_stride + (long)a.pos * hd + d] = f2bf(o);
+    }
+  } else if constexpr (EPI == GEMV_ARGMAX) {
+    unsigned long long key = 0ull;
+    if (row < a.n_valid) {
+      a.out[row] = y;
+      key = argmax_key(y, static_cast<uint32_t>(row));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other > key ? other : key;
+    }
+    if ((tid & 31) == 0 && key) atomicMax(a.amax, key);
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int K = a.n_kb * kTileCols;
+  uint8_t* stages = smem;
+  float* xs = reinterpret_cast<float*>(smem + kGemvStages * kTileBytes);
+  float* red = xs + K;
+  float* scratch = red + kTileRows;  // 8 floats for block reductions
+  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
+  uint64_t* empty = full + kGemvStages;
+  int* flag = reinterpret_cast<int*>(empty + kGemvStages);
+
+  const int G = gridDim.x, c = blockIdx.x;
+  const long T = static_cast<long>(a.n_mt) * a.n_kb;
+  const long t0 = c * T / G, t1 = (c + 1) * T / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGemvStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kGemvConsumers / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kGemvConsumers / 32) {  // ---- producer warp ----
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (long t = t0; t < t1; ++t) {
+        const long i = t - t0;
+        const int s = static_cast<int>(i % kGemvStages);
+        if (i >= kGemvStages) mbar_wait(&empty[s], static_cast<uint32_t>(((i / kGemvStages) - 1) & 1));
+        mbar_arrive_expect_tx(&full[s], kTileBytes);
+        bulk_g2s_evict_first(stages + s * kTileBytes, a.w + t * kTileBytes, kTileBytes, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: x -> shared (fp32), optional fused RMSNorm ----
+  const int tid = threadIdx.x;
+  float ss = 0.f;
+  for (int k = tid; k < K; k += kGemvConsumers) {
+    float v = a.x[k];
+    xs[k] = v;
+    ss = fmaf(v, v, ss);
+  }
+  if (a.norm_w) {
+    ss = warp_sum(ss);
+    if (lane == 0) scratch[warp] = ss;
+    named_bar(1, kGemvConsumers);
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < kGemvConsumers / 32; ++w) tot += scratch[w];
+    const float rstd = rsqrtf(tot / K + a.eps);
+    for (int k = tid; k < K; k += kGemvConsumers) xs[k] = xs[k] * rstd * bf2f(a.norm_w[k]);
+  }
+  named_bar(1, kGemvConsumers);
+
+  const int rr = lane >> 3, ch = lane & 7;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int cur_mt = t0 < t1 ? static_cast<int>(t0 / a.n_kb) : -1;
+
+  auto flush = [&](int mt) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float v = acc[j];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      if (ch == 0) red[warp * 16 + rr + 4 * j] = v;
+      acc[j] = 0.f;
+    }
+    named_bar(1, kGemvConsumers);
+    const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
+    const int c_first = cta_of_tile(first, G, T);
+    const int n_contrib = cta_of_tile(last, G, T) - c_first + 1;
+    if (n_contrib == 1) {
+      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
+      named_bar(1, kGemvConsumers);
+      return;
+    }
+    const int slot = c - c_first;
+    float* mine = a.ws + (static_cast<long>(mt) * a.max_contrib + slot) * kTileRows;
+    if (tid < kTileRows) mine[tid] = red[tid];
+    __threadfence();
+    named_bar(1, kGemvConsumers);
+    if (tid == 0) {
+      const int old = atomicAdd(&a.counters[mt], 1);
+      *flag = (old == n_contrib - 1);
+    }
+    named_bar(1, kGemvConsumers);
+    if (*flag) {
+      __threadfence();
+      if (tid < kTileRows) {
+        const float* base = a.ws + static_cast<long>(mt) * a.max_contrib * kTileRows;
+        float s = 0.f;
+        for (int j = 0; j < n_contrib; ++j) s += __ldcg(base + j * kTileRows + tid);
+        red[tid] = s;
+      }
+      named_bar(1, kGemvConsumers);
+      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
+      if (tid == 0) a.counters[mt] = 0;
+    }
+    named_bar(1, kGemvConsumers);
+  };
+
+  for (long t = t0; t < t1; ++t) {
+    const int mt = static_cast<int>(t / a.n_kb);
+    const int kb = static_cast<int>(t - static_cast<long>(mt) * a.n_kb);
+    if (mt != cur_mt) {
+      flush(cur_mt);
+      cur_mt = mt;
+    }
+    const long i = t - t0;
+    const int s = static_cast<int>(i % kGemvStages);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / kGemvStages) & 1));
+    const uint8_t* st = stages + s * kTileBytes;
+    const float* xk = xs + kb * kTileCols;
+    const float4* xa = reinterpret_cast<const float4*>(xk + ((ch ^ rr) << 3));
+    const float4* xb = reinterpret_cast<const float4*>(xk + ((ch ^ (rr + 4)) << 3));
+    const float4 a0 = xa[0], a1 = xa[1], b0 = xb[0], b1 = xb[1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = warp * 16 + rr + 4 * j;
+      const uint4 wv = *reinterpret_cast<const uint4*>(st + row * 128 + ch * 16);
+      acc[j] += (j & 1) ? dot8(wv, b0, b1) : dot8(wv, a0, a1);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (cur_mt >= 0) flush(cur_mt);
+}
+
+int gemv_grid(int n_mt, int n_kb, int num_sms) {
+  long T = static_cast<long>(n_mt) * n_kb;
+  return static_cast<int>(T < num_sms ? T : num_sms);
+}
+
+int gemv_max_contrib(int n_mt, int n_kb, int grid) {
+  long T = static_cast<long>(n_mt) * n_kb;
+  int best = 1;
+  for (int mt = 0; mt < n_mt; ++mt) {
+    long first = static_cast<long>(mt) * n_kb, last = first + n_kb - 1;
+    int cf = static_cast<int>(((first + 1) * grid - 1) / T);
+    int cl = static_cast<int>(((last + 1) * grid - 1) / T);
+    if (cl - cf + 1 > best) best = cl - cf + 1;
+  }
+  return best;
+}
+
+static size_t gemv_smem(int n_kb) {
+  return static_cast<size_t>(kGemvStages) * kTileBytes + static_cast<size_t>(n_kb) * kTileCols * 4 +
+         kTileRows * 4 + 16 * 4 + 2 * kGemvStages * 8 + 16;
+}
+
+template <int EPI>
+static cudaError_t launch_t(const GemvArgs& a, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  gemv_kernel<EPI><<<grid, kGemvThreads, gemv_smem(a.n_kb), st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
+  if (gemv_smem(a.n_kb) > 227 * 1024) return cudaErrorInvalidValue;
+  switch (epi) {
+    case GEMV_F32: return launch_t<GEMV_F32>(a, grid, st);
+    case GEMV_RESID: return launch_t<GEMV_RESID>(a, grid, st);
+    case GEMV_SILU: return launch_t<GEMV_SILU>(a, grid, st);
+    case GEMV_QKV: return launch_t<GEMV_QKV>(a, grid, st);
+    case GEMV_ARGMAX: return launch_t<GEMV_ARGMAX>(a, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lsb

@@ -1,0 +1,134 @@
+// kernels.h -- host-side launch interface of the sm_100a kernels (shared by the
+// executor and the C-ABI test launchers).  Plain POD argument blocks; every
+// launcher enqueues on the given stream and returns cudaError_t.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lsb {
+
+typedef __nv_bfloat16 bf16;
+
+// ---------------- decode GEMV (batch 1) over tiled weights --------------------
+enum GemvEpi : int {
+  GEMV_F32 = 0,     // out[row] = y
+  GEMV_RESID = 1,   // out[row] += y           (fp32 residual stream)
+  GEMV_SILU = 2,    // out[g*64+i] = silu(y_gate) * y_up (gate/up interleaved per 64 rows)
+  GEMV_QKV = 3,     // per-head RMSNorm (q,k) + RoPE + q out + K/V cache append
+  GEMV_ARGMAX = 4,  // logits out + packed (value, index) atomicMax
+};
+
+struct GemvArgs {
+  const uint8_t* w;        // tiled weights, n_mt * n_kb tiles of 16 KiB
+  int n_mt, n_kb;          // 128-row tiles, 64-column k-blocks
+  const float* x;          // input vector, fp32 [n_kb*64]
+  const bf16* norm_w;      // fused RMSNorm weight over x (nullptr: none)
+  float eps;
+  float* ws;               // stream-K partials [n_mt][max_contrib][128]
+  int* counters;           // [n_mt], zero between launches (self-cleaning)
+  int max_contrib;
+  float* out;              // F32 / RESID / SILU / ARGMAX(logits)
+  const float* bias;       // optional per-row bias (F32/RESID)
+  int n_valid;             // rows that are real (vocab / padding guard)
+  // QKV epilogue
+  int hq, hkv, hd, pos;
+  const bf16* qn_w;        // q RMSNorm weight [hd] (nullptr: no q/k norm)
+  const bf16* kn_w;
+  const float2* rope;      // (cos, sin) table [max_pos][hd/2]
+  float* q_out;            // [hq*hd]
+  bf16* k_cache;           // [hkv][max_ctx][hd]
+  bf16* v_cache;
+  int cache_head_stride;   // max_ctx * hd
+  unsigned long long* amax;  // ARGMAX packed key
+};
+
+int gemv_max_contrib(int n_mt, int n_kb, int grid);
+int gemv_grid(int n_mt, int n_kb, int num_sms);
+cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st);
+
+// ---------------- tcgen05 GEMM: Y[T x N] = X[T x K] * W^T ---------------------
+enum GemmEpi : int {
+  GEMM_BF16 = 0,       // out_bf16 = acc (+bias)
+  GEMM_BF16_GELU = 1,  // out_bf16 = gelu_tanh(acc + bias)
+  GEMM_RESID_F32 = 2,  // out_f32 += acc (+bias)
+  GEMM_SILU_BF16 = 3,  // out_bf16[t, g*64+i] = silu(gate) * up
+  GEMM_F32 = 4,        // out_f32 = acc (+bias)
+};
+
+struct GemmArgs {
+  const uint8_t* w;   // tiled weights (n_mt x n_kb tiles)
+  int n_mt, n_kb;
+  int T;              // tokens (rows of X)
+  const CUtensorMap* x_map;  // X [T x n_kb*64] bf16 row-major, SWIZZLE_128B box {64, BN}
+  void* out;
+  long ldo;           // elements between consecutive tokens in out
+  const float* bias;  // per output feature (optional)
+  const bf16* bias_bf16;  // alternative bf16 bias (optional)
+  int n_valid;        // features < n_valid are real (bias / store guard)
+};
+
+int gemm_block_n(int T);
+cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st);
+// Encode a row-major bf16 [rows x cols] tensor map with box {64, box_rows}, SWIZZLE_128B.
+int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t ld_elems, uint32_t box_rows);
+
+// ---------------- attention --------------------------------------------------
+struct DecodeAttnArgs {
+  const float* q;          // [hq*hd]
+  const bf16* k_cache;     // [hkv][max_ctx][hd]
+  const bf16* v_cache;
+  int cache_head_stride;
+  int hq, hkv, hd, n_ctx;
+  float scale;
+  float* out;              // [hq*hd]
+  float* ws;               // partials
+  int* counters;           // [hkv]
+  int n_split;
+};
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
+
+struct FlashArgs {
+  const bf16* q;  long q_tok_stride, q_head_stride;   // q[t, h, d]
+  const bf16* k1; const bf16* v1; long k1_tok_stride, k1_head_stride; int len1;  // segment 1
+  const bf16* k2; const bf16* v2; long k2_tok_stride, k2_head_stride; int len2;  // segment 2
+  bf16* out;      long o_tok_stride, o_head_stride;
+  int Tq, hq, hkv, hd;
+  int causal;      // key j visible to query i iff j <= i + q_offset
+  int q_offset;
+  int seg_len;     // >0: block-diagonal attention over segments of seg_len tokens (ViT images)
+  float scale;
+};
+cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st);
+
+// ---------------- elementwise / norms ------------------------------------------
+cudaError_t launch_rmsnorm_rows(const float* x, const bf16* w, bf16* out, int T, int D, float eps,
+                                cudaStream_t st);
+cudaError_t launch_layernorm_rows(const float* x, const bf16* w, const bf16* b, bf16* out, int T,
+                                  int D, long ld_out, float eps, cudaStream_t st);
+cudaError_t launch_qk_norm_rope(const bf16* qkv, int T, int hq, int hkv, int hd, const bf16* qn_w,
+                                const bf16* kn_w, float eps, const float2* rope, int pos0,
+                                bf16* q_out, bf16* k_cache, bf16* v_cache, int cache_head_stride,
+                                cudaStream_t st);
+cudaError_t launch_embed_rows(const bf16* table, const int* ids, int n, int D, float* out,
+                              long ld_out, cudaStream_t st);
+cudaError_t launch_add_rows_bf16(float* x, const bf16* add, int T, int D, long period,
+                                 cudaStream_t st);
+cudaError_t launch_silu_inplace(float* x, int n, cudaStream_t st);
+cudaError_t launch_cast_f32_bf16(const float* x, bf16* out, long n, cudaStream_t st);
+cudaError_t launch_argmax_to_token(const unsigned long long* key, int* token_out, int* history,
+                                   int step, unsigned long long* key_reset, cudaStream_t st);
+cudaError_t launch_action_in(const float* actions, const bf16* w_in, const bf16* b_in,
+                             const float* temb, int n_tok, int a_dim, int D, float* out,
+                             cudaStream_t st);
+cudaError_t launch_time_embed(const float* t_scalar_table, int step, int dim, bf16* out,
+                              cudaStream_t st);
+cudaError_t launch_action_out_euler(const float* h, const bf16* norm_w, float eps,
+                                    const bf16* w_out, const bf16* b_out, int n_tok, int D,
+                                    int a_dim, float dt, float* actions, float* velocity,
+                                    cudaStream_t st);
+cudaError_t launch_fill_u64(unsigned long long* p, unsigned long long v, int n, cudaStream_t st);
+
+}  // namespace lsb

@@ -1,0 +1,295 @@
+"""sm_100a kernels vs plain PyTorch fp32 references of the same op.
+
+Tolerances (BF16 operands, fp32 accumulation):  GEMV/GEMM outputs within
+2e-3 * ||ref||_inf + 1e-3 (fp32 outputs) or 1.5e-2 relative (bf16 outputs);
+attention within 2e-2 absolute on O(1) outputs.  Determinism (bit-identical
+re-runs) is asserted where the kernel promises it.
+"""
+import math
+
+import pytest
+import torch
+
+from conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+if cuda_available():
+    from paper_2605_11678_b200 import kernels as K
+
+DEV = "cuda"
+
+
+def _close(got, ref, rel=2e-3, abs_=1e-3):
+    err = (got.float() - ref.float()).abs().max().item()
+    scale = ref.float().abs().max().item()
+    assert err <= rel * scale + abs_, f"max err {err} vs scale {scale}"
+
+
+def test_pack_roundtrip():
+    w = torch.randn(300, 200, device=DEV).to(torch.bfloat16)
+    buf = K.pack_tiled(w)
+    assert buf.numel() == 3 * 4 * 16384
+    assert torch.equal(K.unpack_tiled(buf, 300, 200), w)
+
+
+@pytest.mark.parametrize("n,k", [(384, 256), (6144, 4096), (4096, 12288), (1024, 4096)])
+def test_gemv_f32_and_determinism(n, k):
+    torch.manual_seed(0)
+    w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
+    x = torch.randn(k, device=DEV)
+    ws = K.GemvWorkspace(DEV)
+    out = torch.empty(n, device=DEV)
+    K.gemv(K.GEMV_F32, K.pack_tiled(w), n, k, x, out, ws)
+    ref = w.float() @ x
+    _close(out, ref)
+    out2 = torch.empty(n, device=DEV)
+    K.gemv(K.GEMV_F32, K.pack_tiled(w), n, k, x, out2, ws)
+    assert torch.equal(out, out2)
+    assert int(ws.counters.abs().sum()) == 0  # self-cleaning
+
+
+def test_gemv_fused_norm_resid_silu():
+    torch.manual_seed(1)
+    d, f = 1024, 2048
+    x = torch.randn(d, device=DEV) * 3
+    nw = (1 + 0.1 * torch.randn(d, device=DEV)).to(torch.bfloat16)
+    xn = x * torch.rsqrt((x * x).mean() + 1e-6) * nw.float()
+    gate = (torch.randn(f, d, device=DEV) * 0.02).to(torch.bfloat16)
+    up = (torch.randn(f, d, device=DEV) * 0.02).to(torch.bfloat16)
+    ws = K.GemvWorkspace(DEV)
+    h = torch.empty(f, device=DEV)
+    K.gemv(K.GEMV_SILU, K.pack_tiled(K.interleave_gate_up(gate, up)), 2 * f, d, x, h, ws,
+           norm_w=nw, n_valid=f)
+    ref = torch.nn.functional.silu(gate.float() @ xn) * (up.float() @ xn)
+    _close(h, ref, rel=5e-3)
+    down = (torch.randn(d, f, device=DEV) * 0.02).to(torch.bfloat16)
+    resid = torch.randn(d, device=DEV)
+    r0 = resid.clone()
+    K.gemv(K.GEMV_RESID, K.pack_tiled(down), d, f, h, resid, ws)
+    _close(resid, r0 + down.float() @ h)
+
+
+def _rope_table(max_pos, hd, theta):
+    inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
+    ang = torch.arange(max_pos, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.stack([ang.cos(), ang.sin()], -1).float().to(DEV).contiguous()
+
+
+def _rope_ref(x, cs):  # x [..., hd], cs [hd/2, 2]
+    h2 = x.shape[-1] // 2
+    c, s = cs[..., 0], cs[..., 1]
+    x1, x2 = x[..., :h2], x[..., h2:]
+    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+
+
+@pytest.mark.parametrize("hq,hkv,hd,d", [(32, 8, 128, 4096), (8, 2, 32, 256)])
+def test_gemv_qkv_epilogue(hq, hkv, hd, d):
+    torch.manual_seed(2)
+    n = (hq + 2 * hkv) * hd
+    w = (torch.randn(n, d, device=DEV) * 0.02).to(torch.bfloat16)
+    x = torch.randn(d, device=DEV)
+    nw = (1 + 0.1 * torch.randn(d, device=DEV)).to(torch.bfloat16)
+    qn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
+    kn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
+    max_ctx, pos = 64, 37
+    rope = _rope_table(max_ctx, hd, 1e6)
+    kc = torch.zeros(hkv, max_ctx, hd, dtype=torch.bfloat16, device=DEV)
+    vc = torch.zeros_like(kc)
+    q = torch.empty(hq * hd, device=DEV)
+    ws = K.GemvWorkspace(DEV)
+    K.gemv(K.GEMV_QKV, K.pack_tiled(w), n, d, x, q, ws, norm_w=nw,
+           qkv=dict(hq=hq, hkv=hkv, hd=hd, pos=pos, qn_w=qn, kn_w=kn, rope=rope, q_out=q,
+                    k_cache=kc, v_cache=vc, cache_head_stride=max_ctx * hd))
+    xn = x * torch.rsqrt((x * x).mean() + 1e-6) * nw.float()
+    y = w.float() @ xn
+    yq = y[:hq * hd].view(hq, hd)
+    yk = y[hq * hd:(hq + hkv) * hd].view(hkv, hd)
+    yv = y[(hq + hkv) * hd:].view(hkv, hd)
+
+    def hn(t, wt):
+        return t * torch.rsqrt((t * t).mean(-1, keepdim=True) + 1e-6) * wt.float()
+    qref = _rope_ref(hn(yq, qn), rope[pos])
+    kref = _rope_ref(hn(yk, kn), rope[pos])
+    _close(q.view(hq, hd), qref, rel=5e-3)
+    _close(kc[:, pos].float(), kref, rel=1.5e-2)
+    _close(vc[:, pos].float(), yv, rel=1.5e-2)
+
+
+def test_gemv_argmax():
+    torch.manual_seed(3)
+    n, d = 151936, 4096
+    w = (torch.randn(n, d, device=DEV) * 0.02).to(torch.bfloat16)
+    x = torch.randn(d, device=DEV)
+    logits = torch.empty(n, device=DEV)
+    amax = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ws = K.GemvWorkspace(DEV)
+    K.gemv(K.GEMV_ARGMAX, K.pack_tiled(w), n, d, x, logits, ws, amax=amax)
+    ref = w.float() @ x
+    _close(logits, ref)
+    key = int(amax.item()) & 0xFFFFFFFFFFFFFFFF
+    idx = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+    assert idx == int(torch.argmax(logits).item())
+
+
+@pytest.mark.parametrize("T,n,k", [(64, 384, 256), (100, 1152, 1152), (1024, 6144, 4096),
+                                   (64, 2048, 4096), (3072, 256, 1536)])
+def test_gemm_bf16(T, n, k):
+    torch.manual_seed(4)
+    w = (torch.randn(n, k, device=DEV) * 0.05).to(torch.bfloat16)
+    x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
+    out = torch.empty(T, n, dtype=torch.bfloat16, device=DEV)
+    K.gemm(K.GEMM_BF16, K.pack_tiled(w), n, k, x, out)
+    ref = x.float() @ w.float().t()
+    _close(out, ref, rel=1.5e-2, abs_=1e-2)
+
+
+def test_gemm_epilogues():
+    torch.manual_seed(5)
+    T, d, f = 200, 512, 1024
+    x = torch.randn(T, d, device=DEV).to(torch.bfloat16)
+    bias = torch.randn(f, device=DEV).to(torch.bfloat16)
+    w = (torch.randn(f, d, device=DEV) * 0.05).to(torch.bfloat16)
+    out = torch.empty(T, f, dtype=torch.bfloat16, device=DEV)
+    K.gemm(K.GEMM_BF16_GELU, K.pack_tiled(w), f, d, x, out, bias=bias)
+    ref = torch.nn.functional.gelu(x.float() @ w.float().t() + bias.float(), approximate="tanh")
+    _close(out, ref, rel=1.5e-2, abs_=1e-2)
+    gate = (torch.randn(f, d, device=DEV) * 0.05).to(torch.bfloat16)
+    up = (torch.randn(f, d, device=DEV) * 0.05).to(torch.bfloat16)
+    h = torch.empty(T, f, dtype=torch.bfloat16, device=DEV)
+    K.gemm(K.GEMM_SILU_BF16, K.pack_tiled(K.interleave_gate_up(gate, up)), 2 * f, d, x, h,
+           n_valid=f)
+    ref = torch.nn.functional.silu(x.float() @ gate.float().t()) * (x.float() @ up.float().t())
+    _close(h, ref, rel=1.5e-2, abs_=1e-2)
+    resid = torch.randn(T, d, device=DEV)
+    r0 = resid.clone()
+    down = (torch.randn(d, f, device=DEV) * 0.05).to(torch.bfloat16)
+    K.gemm(K.GEMM_RESID_F32, K.pack_tiled(down), d, f, h, resid)
+    _close(resid, r0 + h.float() @ down.float().t(), rel=5e-3, abs_=1e-2)
+
+
+def test_gemm_padded_k_and_n():
+    torch.manual_seed(6)
+    T, n, k = 96, 4304, 1152  # ViT fc1: N padded to 4352
+    w = (torch.randn(n, k, device=DEV) * 0.05).to(torch.bfloat16)
+    x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
+    out = torch.zeros(T, 4352, dtype=torch.bfloat16, device=DEV)
+    K.gemm(K.GEMM_BF16, K.pack_tiled(w), n, k, x, out, n_valid=n)
+    _close(out[:, :n], x.float() @ w.float().t(), rel=1.5e-2, abs_=1e-2)
+    assert out[:, n:].abs().max().item() == 0.0
+    w2 = (torch.randn(1152, n, device=DEV) * 0.05).to(torch.bfloat16)  # fc2: K padded
+    out2 = torch.empty(T, 1152, dtype=torch.bfloat16, device=DEV)
+    K.gemm(K.GEMM_BF16, K.pack_tiled(w2), 1152, n, out, out2)
+    _close(out2, out[:, :n].float() @ w2.float().t(), rel=1.5e-2, abs_=2e-2)
+
+
+@pytest.mark.parametrize("hq,hkv,hd,n_ctx,n_split", [(32, 8, 128, 1045, 18), (8, 2, 32, 24, 1),
+                                                     (32, 8, 128, 7, 4)])
+def test_decode_attention(hq, hkv, hd, n_ctx, n_split):
+    torch.manual_seed(7)
+    max_ctx = 1100
+    q = torch.randn(hq * hd, device=DEV)
+    kc = torch.randn(hkv, max_ctx, hd, device=DEV).to(torch.bfloat16)
+    vc = torch.randn(hkv, max_ctx, hd, device=DEV).to(torch.bfloat16)
+    out = torch.empty(hq * hd, device=DEV)
+    ws = torch.empty(hq * n_split * (hd + 2), device=DEV)
+    cnt = torch.zeros(hkv, dtype=torch.int32, device=DEV)
+    scale = 1 / math.sqrt(hd)
+    K.decode_attention(q, kc, vc, n_ctx, out, hq, hkv, hd, scale, ws, cnt, n_split)
+    g = hq // hkv
+    kk = kc[:, :n_ctx].float().repeat_interleave(g, 0)
+    vv = vc[:, :n_ctx].float().repeat_interleave(g, 0)
+    att = torch.softmax((q.view(hq, 1, hd) @ kk.transpose(1, 2)) * scale, -1)
+    ref = (att @ vv).view(-1)
+    _close(out, ref, rel=1e-3, abs_=2e-3)
+
+
+def _attn_ref(q, k, v, mask, scale):
+    # q [T, H, d], k/v [L, Hkv, d]
+    g = q.shape[1] // k.shape[1]
+    kk = k.float().repeat_interleave(g, 1).permute(1, 0, 2)
+    vv = v.float().repeat_interleave(g, 1).permute(1, 0, 2)
+    s = (q.float().permute(1, 0, 2) @ kk.transpose(1, 2)) * scale
+    s = s.masked_fill(~mask[None], float("-inf"))
+    return (torch.softmax(s, -1) @ vv).permute(1, 0, 2)
+
+
+def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0):
+    a = K.FlashArgs(q=q.data_ptr(), q_tok_stride=q.stride(0), q_head_stride=q.stride(1),
+                    k1=k1.data_ptr(), v1=v1.data_ptr(), k1_tok_stride=k1.stride(0),
+                    k1_head_stride=k1.stride(1), len1=k1.shape[0],
+                    k2=k2.data_ptr() if k2 is not None else 0,
+                    v2=v2.data_ptr() if v2 is not None else 0,
+                    k2_tok_stride=k2.stride(0) if k2 is not None else 0,
+                    k2_head_stride=k2.stride(1) if k2 is not None else 0,
+                    len2=k2.shape[0] if k2 is not None else 0,
+                    out=out.data_ptr(), o_tok_stride=out.stride(0), o_head_stride=out.stride(1),
+                    Tq=q.shape[0], hq=hq, hkv=hkv, hd=hd, causal=causal, q_offset=q_offset,
+                    seg_len=seg_len, scale=1 / math.sqrt(hd))
+    K.flash_attention(a)
+
+
+def test_flash_causal_prefill():
+    torch.manual_seed(8)
+    T, hq, hkv, hd = 333, 32, 8, 128
+    q = torch.randn(T, hq, hd, device=DEV).to(torch.bfloat16)
+    k = torch.randn(T, hkv, hd, device=DEV).to(torch.bfloat16)
+    v = torch.randn(T, hkv, hd, device=DEV).to(torch.bfloat16)
+    out = torch.empty(T, hq, hd, dtype=torch.bfloat16, device=DEV)
+    _flash(q, k, v, None, None, out, hq, hkv, hd, causal=1)
+    mask = torch.ones(T, T, dtype=torch.bool, device=DEV).tril()
+    _close(out, _attn_ref(q, k, v, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
+
+
+def test_flash_vit_block_diagonal_hd72():
+    torch.manual_seed(9)
+    n_img, per, h, hd = 3, 128, 4, 72
+    T = n_img * per
+    qkv = torch.randn(T, 3, h, hd, device=DEV).to(torch.bfloat16)
+    q, k, v = qkv[:, 0], qkv[:, 1], qkv[:, 2]
+    out = torch.empty(T, h, hd, dtype=torch.bfloat16, device=DEV)
+    _flash(q, k, v, None, None, out, h, h, hd, seg_len=per)
+    img = torch.arange(T, device=DEV) // per
+    mask = img[:, None] == img[None, :]
+    _close(out, _attn_ref(q, k, v, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
+
+
+def test_flash_two_segments_expert():
+    torch.manual_seed(10)
+    Tq, L1, hq, hkv, hd = 64, 530, 32, 8, 128
+    q = torch.randn(Tq, hq, hd, device=DEV).to(torch.bfloat16)
+    cache_k = torch.randn(hkv, 600, hd, device=DEV).to(torch.bfloat16)  # [head][pos][d]
+    cache_v = torch.randn(hkv, 600, hd, device=DEV).to(torch.bfloat16)
+    k2 = torch.randn(Tq, hkv, hd, device=DEV).to(torch.bfloat16)
+    v2 = torch.randn(Tq, hkv, hd, device=DEV).to(torch.bfloat16)
+    out = torch.empty(Tq, hq, hd, dtype=torch.bfloat16, device=DEV)
+    k1v = cache_k.permute(1, 0, 2)  # strided view [pos][head][d]
+    v1v = cache_v.permute(1, 0, 2)
+    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd)
+    kk = torch.cat([k1v[:L1], k2], 0)
+    vv = torch.cat([v1v[:L1], v2], 0)
+    mask = torch.ones(Tq, L1 + Tq, dtype=torch.bool, device=DEV)
+    _close(out, _attn_ref(q, kk, vv, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
+
+
+def test_qk_norm_rope_prefill_kernel():
+    torch.manual_seed(11)
+    T, hq, hkv, hd = 50, 8, 2, 32
+    qkv = torch.randn(T, (hq + 2 * hkv) * hd, device=DEV).to(torch.bfloat16)
+    qn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
+    kn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
+    rope = _rope_table(128, hd, 1e4)
+    q = torch.empty(T, hq, hd, dtype=torch.bfloat16, device=DEV)
+    kc = torch.zeros(hkv, 128, hd, dtype=torch.bfloat16, device=DEV)
+    vc = torch.zeros_like(kc)
+    K.qk_norm_rope(qkv, hq, hkv, hd, qn, kn, 1e-6, rope, 5, q, kc, vc)
+    x = qkv.float().view(T, hq + 2 * hkv, hd)
+
+    def hn(t, wt):
+        return t * torch.rsqrt((t * t).mean(-1, keepdim=True) + 1e-6) * wt.float()
+    cs = rope[5:5 + T][:, None]
+    _close(q, _rope_ref(hn(x[:, :hq], qn), cs), rel=1.5e-2, abs_=1e-2)
+    _close(kc[:, 5:5 + T].permute(1, 0, 2), _rope_ref(hn(x[:, hq:hq + hkv], kn), cs), rel=1.5e-2,
+           abs_=1e-2)
+    assert torch.equal(vc[:, 5:5 + T].permute(1, 0, 2), qkv.view(T, -1, hd)[:, hq + hkv:])
