@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: Alpamayo-R1-10B-shaped end-to-end latency under a 16 GB emulated
+VRAM cap with Pipelined Demand Layering on B200 (BASELINE.json metric:
+"Alpamayo-shape e2e latency (s) at 16GB VRAM cap; H2D GB/s; predictor error %").
+
+One step = one full inference (ViT over 4 camera images -> patch merger -> LM
+prefill over a 1024-token prompt -> 21 greedy decode steps -> 10 Euler steps
+of the flow-matching action expert) through the DFB executor, at the
+placement chosen by the native residency planner from a measured profile.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config alpamayo-r1-10b-shape|qwen3-vl-8b-lm-shape]
+
+Prints ONE JSON line (rank 0).  `value` = mean device latency per inference
+(s, lower is better) with inputs resident; `e2e` = the same through
+`DemandLayeringEngine.infer` with pinned host buffers (H2D of inputs and D2H
+of tokens/actions inside the timed region).  The streamed weights are larger
+than L2 (and the resident ones too), so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def _peaks():
+    try:
+        return json.loads(PEAKS_FILE.read_text()), "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path(tempfile.mkstemp(suffix=".csv")[1])
+
+    def __enter__(self):
+        try:
+            self.fh = self.path.open("w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in self.path.read_text().splitlines():
+                cols = [c.strip() for c in line.split(",")]
+                if len(cols) < 9:
+                    continue
+                try:
+                    sm.append(float(cols[1]))
+                    mx.append(float(cols[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, cols[5:9]):
+                    if v.lower() in ("active", "1", "0x1"):
+                        reasons.add(n)
+        except Exception:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_h2d_peak(torch, device, nbytes=1 << 30, reps=6):
+    """Pinned host -> HBM copy-engine peak (MEASURED_PEAKS.json has no H2D figure)."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    s = torch.cuda.Stream(device)
+    best = 0.0
+    for i in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            d.copy_(h, non_blocking=True)
+            e1.record(s)
+        s.synchronize()
+        if i:
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e6))
+    del h, d
+    return best
+
+
+def gemv_microbench(torch, device, n, k, reps=30):
+    """Dominant decode kernel alone: gate|up GEMV (+fused RMSNorm, SiLU*up)."""
+    from paper_2605_11678_b200 import kernels as K
+    w = K.pack_tiled((torch.randn(n, k, device=device) * 0.02).to(torch.bfloat16))
+    # rotate through several weight copies > L2 so every launch streams from HBM
+    copies = [w] + [w.clone() for _ in range(2)]
+    x = torch.randn(k, device=device)
+    nw = torch.ones(k, dtype=torch.bfloat16, device=device)
+    out = torch.empty(n // 2, device=device)
+    ws = K.GemvWorkspace(device)
+    s = torch.cuda.Stream(device)
+    with torch.cuda.stream(s):
+        for i in range(5):
+            K.gemv(K.GEMV_SILU, copies[i % 3], n, k, x, out, ws, norm_w=nw, n_valid=n // 2, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for i in range(reps):
+            K.gemv(K.GEMV_SILU, copies[i % 3], n, k, x, out, ws, norm_w=nw, n_valid=n // 2, stream=s)
+        e1.record(s)
+    s.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    algo_bytes = n * k * 2 + k * 4 + k * 2 + (n // 2) * 4
+    return {"bytes": algo_bytes, "ms": ms, "gbs": algo_bytes / (ms * 1e6)}
+
+
+def gemm_microbench(torch, device, T, n, k, reps=20):
+    from paper_2605_11678_b200 import kernels as K
+    w = K.pack_tiled((torch.randn(n, k, device=device) * 0.02).to(torch.bfloat16))
+    x = torch.randn(T, k, device=device).to(torch.bfloat16)
+    out = torch.empty(T, n, dtype=torch.bfloat16, device=device)
+    s = torch.cuda.Stream(device)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            K.gemm(K.GEMM_BF16, w, n, k, x, out, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            K.gemm(K.GEMM_BF16, w, n, k, x, out, stream=s)
+        e1.record(s)
+    s.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * T * n * k
+    return {"flops": flops, "ms": ms, "tflops": flops / (ms * 1e9)}
+
+
+def run_reference(args, cfg):
+    """Reference arm: the path on the box's host cores (oracle/cpu_baseline.py)."""
+    from oracle import cpu_baseline
+    _, rank, _ = _dist()
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    runs = [cpu_baseline.estimate(cfg) for _ in range(max(1, min(args.steps, 3)))]
+    value = statistics.fmean(r["value"] for r in runs)
+    info = runs[-1]
+    line = {
+        "impl": "reference", "metric": "Alpamayo-shape e2e latency (s) at 16GB VRAM cap",
+        "value": value, "unit": "s", "n_gpus": args.gpus, "steps": len(runs),
+        "warmup": 0, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights, seeded)",
+        "config": {"workload": cfg.name, "vram_cap_mb": args.vram_cap_mb},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": info["cores"], "kind": info["kind"],
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="alpamayo-r1-10b-shape")
+    ap.add_argument("--vram-cap-mb", type=float, default=16000.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=2)
+    ap.add_argument("--dump", default=None, help="directory for profile/plan/timeline artefacts")
+    args = ap.parse_args()
+
+    from paper_2605_11678_b200 import model as M
+    cfg = M.PRESETS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import paper_2605_11678_b200 as ls
+    from paper_2605_11678_b200.engine import DemandLayeringEngine
+
+    world, rank, local = _dist()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = torch.device("cuda", local)
+    peaks, peaks_src = _peaks()
+
+    h2d_peak = measure_h2d_peak(torch, device)
+    eng = DemandLayeringEngine(cfg, device=local, vram_cap_mb=args.vram_cap_mb, n_slots=2, seed=0)
+    prof = eng.profile_run(iterations=args.profile_iters, warmup=1)
+    plan = ls.plan_for_budget(prof, prof.hardware.vram_mb, include_simulated=True)
+    placement = plan.placement
+
+    # one timeline-recorded pipelined run at the plan: H2D and decode-layer HBM rates
+    inputs = M.synthetic_inputs(cfg, seed=0)
+    tl_run = eng.execute(placement, inputs=inputs)
+    tl = tl_run.timeline
+    dma_rates, dec_rates = [], []
+    kinds = {M.MODULE_NAMES[k]: k for k in cfg.kinds}
+    kv_bytes_tok = 2 * cfg.lm_hkv * cfg.lm_hd * 2
+    for e in tl.events:
+        dur = e.end_ms - e.start_ms
+        if dur <= 0:
+            continue
+        nbytes = eng.layer_bytes(kinds[e.module])
+        if e.engine is ls.Engine.COPY:
+            dma_rates.append(nbytes / (dur * 1e6))
+        elif e.module == "vlm" and e.phase == "decode" and e.layer in placement.for_module("vlm"):
+            ctx = cfg.prompt_len + e.invocation + 1
+            dec_rates.append((nbytes + ctx * kv_bytes_tok) / (dur * 1e6))
+    h2d_streamed = statistics.fmean(dma_rates) if dma_rates else None
+
+    # warm-up, then EXACTLY K timed steps (device events per step; barrier + sync both sides)
+    for _ in range(args.warmup):
+        eng.execute(placement, inputs=inputs, record_timeline=False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    step_ms = []
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            step_ms.append(eng.execute(placement, inputs=inputs, record_timeline=False).total_ms)
+        wall = time.perf_counter() - t_wall
+    torch.cuda.synchronize(device)
+    launches = eng.last_run_stats()
+    if dist:
+        dist.barrier()
+    ms = statistics.fmean(step_ms)
+    if dist:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # end-to-end through the public API with pinned host buffers
+    e2e_ms = [eng.infer(inputs, placement).e2e_ms for _ in range(args.steps)]
+    h2d_io, d2h_io = eng.io_bytes(cfg)
+
+    # predictor (Eq. 10) vs measured over a vlm-only interleaved sweep
+    pred = None
+    if not args.no_sweep:
+        vlm = prof.module("vlm")
+        kmax = plan.resident_count_per_module.get("vlm", 0)
+        ks = sorted({0, kmax // 4, kmax // 2, (3 * kmax) // 4, kmax})
+        measured = [(0, prof.calibration_total_s)]
+        for k in ks[1:]:
+            pl = ls.Placement({"vlm": ls.interleaved_indices(k, vlm.layers)})
+            measured.append((k, eng.execute(pl, inputs=inputs, record_timeline=False).total_ms / 1e3))
+        preds = ls.predict(prof.calibration_total_s, ls.slope_from_profile(vlm), ks)
+        rep = ls.validate(preds, measured)
+        pred = {"k": ks, "measured_s": [m for _, m in measured],
+                "predicted_s": [p.predicted_s for p in preds],
+                "error_pct": [r.error_pct for r in rep.rows], "max_abs_error_pct": rep.max_abs_error_pct,
+                "fitted_slope_s": rep.fitted_slope_s}
+        eng.set_placement(placement)
+
+    # dominant-kernel roofline: the decode gate|up GEMV (largest HBM stream of the step)
+    gv = gemv_microbench(torch, device, 2 * cfg.lm_ffn, cfg.lm_d)
+    gm = gemm_microbench(torch, device, cfg.prompt_len, (cfg.lm_hq + 2 * cfg.lm_hkv) * cfg.lm_hd, cfg.lm_d)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_baseline
+        info = cpu_baseline.estimate(cfg)
+        cpu = {"value": info["value"], "unit": "s", "cores": info["cores"], "kind": info["kind"],
+               "sample": info["sample"]}
+
+    mem = eng.memory()
+    sim_bound_s = plan.simulated_total_ms / 1e3
+    if args.dump:
+        out = Path(args.dump)
+        out.mkdir(parents=True, exist_ok=True)
+        ls.save_profile(prof, out / f"profile_{cfg.name}.json")
+        from paper_2605_11678_b200.planner import save_plan
+        save_plan(plan, out / f"plan_{cfg.name}.json")
+        ls.write_trace(tl, out / f"trace_{cfg.name}.csv")
+    line = {
+        "metric": "Alpamayo-shape e2e latency (s) at 16GB VRAM cap",
+        "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init BF16 weights, seeded inputs)",
+        "config": {"workload": cfg.name, "vram_cap_mb": args.vram_cap_mb,
+                   "prompt_tokens": cfg.prompt_len, "decode_steps": cfg.decode_steps,
+                   "euler_steps": cfg.euler_steps if cfg.has_expert else 0,
+                   "placement": plan.resident_count_per_module,
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+                   "l2": "inputs larger than L2 (21 GB streamed + resident weights per step)"},
+        "e2e": {"value": statistics.fmean(e2e_ms) / 1e3, "unit": "s",
+                "h2d_bytes_per_step": h2d_io, "d2h_bytes_per_step": d2h_io,
+                "streamed_weight_bytes_per_step": launches["h2d_bytes"]},
+        "h2d": {"streamed_layer_gbs": h2d_streamed, "peak_gbs": h2d_peak,
+                "frac": (h2d_streamed / h2d_peak) if h2d_streamed else None,
+                "peak_source": "measured on this box: pinned 1 GiB cudaMemcpyAsync, best of 5"},
+        "predictor": pred,
+        "lower_bound": {"dfbsim_total_s": sim_bound_s, "measured_over_bound": (ms / 1e3) / sim_bound_s,
+                        "note": "dfbsim total of the chosen placement on the measured profile"},
+        "roofline": {"bound": "hbm", "achieved": gv["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": gv["gbs"] / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": f"gemv_kernel<SILU> gate|up {2 * cfg.lm_ffn}x{cfg.lm_d} bf16 "
+                               f"({gv['bytes']} B/launch, {gv['ms'] * 1e3:.1f} us)",
+                     "peak_source": peaks_src,
+                     "decode_layer_gbs_live": statistics.fmean(dec_rates) if dec_rates else None},
+        "tensor": {"kernel": f"gemm_kernel tcgen05 prefill QKV T={cfg.prompt_len}",
+                   "achieved_tflops": gm["tflops"], "peak_tflops": peaks["bf16_tflops"],
+                   "frac": gm["tflops"] / peaks["bf16_tflops"]},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": launches["kernel_launches"] * args.steps,
+        "memory_mib": {k: round(v / 2 ** 20, 1) for k, v in mem.items()},
+        "wall_s_timed": wall,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -175,6 +175,107 @@ int ls_validate(const int64_t* pred_k, const double* pred_s, int32_t n_pred,
 int ls_resolve_intercept(const ls_profile* p, double calibration_total_s,
                          const ls_simconfig* cfg, double* intercept_s, int32_t* source);
 
+/* ==== 2. DFB transfer engine + model executor (CUDA, sm_100a) ============== */
+/* No reference function: the reference models this engine in
+ * dfbsim.simulate (pkg/src/layerswap/dfbsim.py:179-247) and the paper's
+ * Double Flat Buffer.  ls_exec_run executes the same
+ * protocol on the GPU and returns the same event schema (ls_event) with CUDA
+ * event timestamps, so timelines are interchangeable with ls_simulate's. */
+
+/* Alpamayo-R1-10B-shaped synthetic stack (shapes SURVEY 8d). */
+typedef struct ls_dims {
+  int32_t has_vit, has_expert;
+  /* ViT encoder + patch merger */
+  int32_t vit_layers, vit_d, vit_heads, vit_hd, vit_ffn, vit_patch_dim, vit_images,
+      vit_tokens_per_image;
+  /* language model (prefill + greedy decode) */
+  int32_t lm_layers, lm_d, lm_hq, lm_hkv, lm_hd, lm_ffn, vocab, prompt_prefix, prompt_suffix,
+      decode_steps;
+  /* flow-matching action expert */
+  int32_t ex_layers, ex_d, ex_hq, ex_hkv, ex_hd, ex_ffn, ex_tokens, action_dim, euler_steps,
+      time_dim;
+  float lm_eps, vit_eps, rope_theta, _pad;
+} ls_dims;
+
+#define LS_KIND_VIT 0
+#define LS_KIND_LM 1
+#define LS_KIND_EXPERT 2
+#define LS_LAYOUT_MAX 16
+typedef struct ls_layer_layout {
+  int32_t n_parts, _pad;
+  uint64_t offset[LS_LAYOUT_MAX];
+  uint64_t bytes[LS_LAYOUT_MAX];
+  uint64_t total;
+} ls_layer_layout;
+/* Flat per-layer buffer layout (one H2D copy per streamed layer). */
+int ls_layer_layout_of(const ls_dims* d, int32_t kind, ls_layer_layout* out);
+
+#define LS_N_GLOBAL 23
+/* Byte size of always-resident tensor `id` (0 when its module is absent). */
+int ls_global_size(const ls_dims* d, int32_t id, uint64_t* bytes);
+
+typedef struct ls_exec ls_exec;
+/* Device arena of cap_bytes (the emulated VRAM budget) holding DFB slots,
+ * always-resident tensors, KV cache, activations and resident layers. */
+int ls_exec_create(const ls_dims* d, int32_t device, uint64_t cap_bytes, int32_t n_slots,
+                   ls_exec** out);
+int ls_exec_destroy(ls_exec* e);
+int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr);
+/* Pinned host buffers of every layer of one module (streamed source). */
+int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_ptrs, int32_t n);
+/* Upload resident layers for a placement mask (module order vit, lm, expert). */
+int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n);
+/* out: cap, used, high_water, slots, always_resident, overhead, resident (bytes) */
+int ls_exec_memory(ls_exec* e, uint64_t out[7]);
+int ls_exec_streams(ls_exec* e, void** copy_stream, void** compute_stream);
+/* out: kernels launched, streamed-layer H2D copies, H2D bytes -- of the last run */
+int ls_exec_stats(ls_exec* e, int64_t out[3]);
+
+typedef struct ls_run_io {
+  int32_t on_host;         /* 1: pointers are pinned host memory (copies inside the run) */
+  int32_t _pad;
+  const void* patches;     /* bf16 [images*tokens_per_image x patch_dim] */
+  const int32_t* text_ids; /* [prompt_prefix + prompt_suffix] */
+  const float* noise;      /* [ex_tokens x action_dim] */
+  int32_t* tokens_out;     /* [decode_steps + 1] */
+  float* actions_out;      /* [ex_tokens x action_dim] */
+  float* logits_out;       /* optional [(decode_steps + 1) x vocab] (device only) */
+} ls_run_io;
+
+typedef struct ls_run_opts {
+  ls_simconfig cfg;
+  int32_t record_timeline; /* 1: per-layer CUDA event timestamps */
+} ls_run_opts;
+
+/* One inference.  total_ms: device time from the first layer transfer /
+ * compute to the last (events t0..t1); e2e_ms: including input/output copies. */
+int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_event* events,
+                int64_t capacity, int64_t* n_events, double* total_ms, double* e2e_ms);
+
+/* Page-locked host arena for streamed layers (cudaHostAlloc, portable). */
+int ls_host_alloc(uint64_t bytes, void** out);
+int ls_host_free(void* p);
+int ls_copy(void* dst, const void* src, uint64_t bytes);
+
+/* ==== 3. kernel launchers (raw device pointers, shapes, cudaStream_t) ====== */
+int ls_num_sms(int device, int32_t* out);
+int ls_gemv_plan(int32_t n_mt, int32_t n_kb, int32_t num_sms, int32_t* grid, int32_t* max_contrib);
+/* args points at the GemvArgs / DecodeAttnArgs / FlashArgs blocks of csrc/kernels.h */
+int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream);
+int ls_k_gemm(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, const void* x,
+              int32_t T, int64_t ldx, void* out, int64_t ldo, const float* bias,
+              const void* bias_bf16, int32_t n_valid, void* stream);
+int ls_k_decode_attention(const void* args, void* stream);
+int ls_k_flash_attention(const void* args, void* stream);
+int ls_k_rmsnorm_rows(const float* x, const void* w, void* out, int32_t T, int32_t D, float eps,
+                      void* stream);
+int ls_k_layernorm_rows(const float* x, const void* w, const void* b, void* out, int32_t T,
+                        int32_t D, int64_t ld_out, float eps, void* stream);
+int ls_k_qk_norm_rope(const void* qkv, int32_t T, int32_t hq, int32_t hkv, int32_t hd,
+                      const void* qn_w, const void* kn_w, float eps, const void* rope, int32_t pos0,
+                      void* q_out, void* k_cache, void* v_cache, int32_t cache_head_stride,
+                      void* stream);
+
 /* ---- CPython float helpers (exported for the parity tests) ---------------- */
 double ls_py_sum(const double* x, int64_t n);      /* builtins.sum, CPython 3.12 */
 double ls_py_floordiv(double a, double b);         /* float.__floordiv__          */

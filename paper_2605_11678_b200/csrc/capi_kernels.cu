@@ -26,6 +26,19 @@ int ls_num_sms(int device, int32_t* out) {
   return cuda_rc(e, "cudaDeviceGetAttribute");
 }
 
+/* Page-locked host memory for the streamed-layer arena (one H2D per layer). */
+int ls_host_alloc(uint64_t bytes, void** out) {
+  *out = nullptr;
+  return cuda_rc(cudaHostAlloc(out, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+}
+
+int ls_host_free(void* p) { return cuda_rc(cudaFreeHost(p), "cudaFreeHost"); }
+
+/* Synchronous copy between any two addresses (unified addressing). */
+int ls_copy(void* dst, const void* src, uint64_t bytes) {
+  return cuda_rc(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault), "cudaMemcpy");
+}
+
 int ls_gemv_plan(int32_t n_mt, int32_t n_kb, int32_t num_sms, int32_t* grid, int32_t* max_contrib) {
   *grid = gemv_grid(n_mt, n_kb, num_sms);
   *max_contrib = gemv_max_contrib(n_mt, n_kb, *grid);

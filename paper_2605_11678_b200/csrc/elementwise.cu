@@ -183,17 +183,17 @@ cudaError_t launch_fill_u64(unsigned long long* p, unsigned long long v, int n, 
 }
 
 // Sinusoidal flow-time features: out[i] = sin(t * f_i) | cos(t * f_i), f_i = 1e4^(-i/(dim/2)).
-__global__ void time_embed_kernel(const float* t_table, int step, int dim, bf16* out) {
+__global__ void time_embed_kernel(const float* t_table, int step, int dim, float* out) {
   const float t = t_table[step];
   const int half = dim / 2;
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
     const float f = expf(-9.210340371976184f * i / half);  // ln(1e4)
-    out[i] = f2bf(sinf(t * f));
-    out[half + i] = f2bf(cosf(t * f));
+    out[i] = sinf(t * f);
+    out[half + i] = cosf(t * f);
   }
 }
 
-cudaError_t launch_time_embed(const float* t_table, int step, int dim, bf16* out, cudaStream_t st) {
+cudaError_t launch_time_embed(const float* t_table, int step, int dim, float* out, cudaStream_t st) {
   time_embed_kernel<<<1, 128, 0, st>>>(t_table, step, dim, out);
   return cudaGetLastError();
 }

@@ -1,0 +1,902 @@
+// executor.cu -- the Double-Flat-Buffer (DFB) transfer engine and the native
+// executor of the Alpamayo-R1-10B-shaped stack.
+//
+// DFB protocol (schedule rules dfbsim.py:11-37):
+//   * one device arena of `cap` bytes emulates the VRAM budget; it holds the
+//     slot ring (n_slots x largest layer), always-resident tensors, KV cache,
+//     activations and the planner's resident layers -- nothing else is
+//     allocated on the device, so the budget is enforced, not just reported;
+//   * every streamed layer is ONE cudaMemcpyAsync from its flat pinned host
+//     buffer into slot (streamed_seq mod slots) on a dedicated copy stream;
+//   * dma_done[slot] (copy -> compute) and compute_done[slot] (compute ->
+//     copy) events implement the two-event hand-off; resident layers run on
+//     the compute stream with no transfer;
+//   * per-invocation barrier (copy stream waits for the invocation's last
+//     EXE) unless cross-invocation prefetch; SEQUENTIAL mode makes every DMA
+//     wait for the previous EXE;
+//   * optional timing events around every DMA and EXE produce a Timeline in
+//     the dfbsim event schema (module -> phase -> invocation -> layer order).
+// The host thread only enqueues: the whole inference (ViT -> merger -> LM
+// prefill -> greedy decode -> flow-matching expert) is issued without a
+// single host synchronisation; greedy tokens stay on the device.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/layerswap_b200.h"
+#include "kernels.h"
+
+namespace lsb {
+int set_error(int code, const char* fmt, ...);
+}
+using namespace lsb;
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      return set_error(LS_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__,     \
+                       __LINE__);                                                               \
+  } while (0)
+
+// Launch a kernel and count it (gpu_launches evidence for the bench).
+#define KL(x)        \
+  do {               \
+    CK(x);           \
+    ++e->launches;   \
+  } while (0)
+
+namespace {
+
+uint64_t tiled_bytes(int n, int k) {
+  return static_cast<uint64_t>((n + 127) / 128) * static_cast<uint64_t>((k + 63) / 64) * 16384ull;
+}
+int n_mt(int n) { return (n + 127) / 128; }
+int n_kb(int k) { return (k + 63) / 64; }
+uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+void layout_push(ls_layer_layout* L, uint64_t bytes) {
+  uint64_t off = L->n_parts ? align_up(L->offset[L->n_parts - 1] + L->bytes[L->n_parts - 1], 16) : 0;
+  L->offset[L->n_parts] = off;
+  L->bytes[L->n_parts] = bytes;
+  L->n_parts++;
+  L->total = off + bytes;
+}
+
+// LM / expert decoder layer: 0 qkv, 1 o, 2 gate|up (64-row interleave), 3 down,
+// 4 attn_norm, 5 mlp_norm, 6 q_norm, 7 k_norm.
+void layout_decoder(int d, int hq, int hkv, int hd, int ffn, ls_layer_layout* L) {
+  std::memset(L, 0, sizeof(*L));
+  layout_push(L, tiled_bytes((hq + 2 * hkv) * hd, d));
+  layout_push(L, tiled_bytes(d, hq * hd));
+  layout_push(L, tiled_bytes(2 * ffn, d));
+  layout_push(L, tiled_bytes(d, ffn));
+  layout_push(L, 2ull * d);
+  layout_push(L, 2ull * d);
+  layout_push(L, 2ull * hd);
+  layout_push(L, 2ull * hd);
+}
+
+// ViT block: 0 qkv, 1 proj, 2 fc1, 3 fc2, 4 qkv_b, 5 proj_b, 6 fc1_b, 7 fc2_b,
+// 8 ln1_w, 9 ln1_b, 10 ln2_w, 11 ln2_b.
+void layout_vit(int d, int h, int hd, int ffn, ls_layer_layout* L) {
+  std::memset(L, 0, sizeof(*L));
+  layout_push(L, tiled_bytes(3 * h * hd, d));
+  layout_push(L, tiled_bytes(d, h * hd));
+  layout_push(L, tiled_bytes(ffn, d));
+  layout_push(L, tiled_bytes(d, ffn));
+  layout_push(L, 2ull * 3 * h * hd);
+  layout_push(L, 2ull * d);
+  layout_push(L, 2ull * ffn);
+  layout_push(L, 2ull * d);
+  for (int i = 0; i < 4; ++i) layout_push(L, 2ull * d);
+}
+
+int vis_tokens(const ls_dims& d) {
+  return d.has_vit ? d.vit_images * d.vit_tokens_per_image / 4 : 0;
+}
+int prompt_len(const ls_dims& d) { return d.prompt_prefix + vis_tokens(d) + d.prompt_suffix; }
+int ctx_len(const ls_dims& d) { return prompt_len(d) + d.decode_steps; }
+int rope_rows(const ls_dims& d) { return ctx_len(d) + 1 + (d.has_expert ? d.ex_tokens : 0); }
+
+uint64_t global_bytes(const ls_dims& d, int id) {
+  const bool v = d.has_vit, x = d.has_expert;
+  const uint64_t vd = d.vit_d, md = 4ull * d.vit_d;
+  switch (id) {
+    case 0: return 2ull * d.vocab * d.lm_d;                        // embed (row-major)
+    case 1: return tiled_bytes(d.vocab, d.lm_d);                  // lm_head
+    case 2: return 2ull * d.lm_d;                                 // final norm
+    case 3: return 8ull * rope_rows(d) * (d.lm_hd / 2);           // rope (cos, sin)
+    case 4: return v ? tiled_bytes(d.vit_d, d.vit_patch_dim) : 0; // patch embed
+    case 5: return v ? 2 * vd : 0;
+    case 6: return v ? 2ull * d.vit_tokens_per_image * vd : 0;    // pos embed
+    case 7: case 8: return v ? 2 * vd : 0;                        // merger LN
+    case 9: return v ? tiled_bytes(static_cast<int>(md), static_cast<int>(md)) : 0;
+    case 10: return v ? 2 * md : 0;
+    case 11: return v ? tiled_bytes(d.lm_d, static_cast<int>(md)) : 0;
+    case 12: return v ? 2ull * d.lm_d : 0;
+    case 13: return x ? tiled_bytes(d.ex_d, d.time_dim) : 0;      // time MLP
+    case 14: return x ? 4ull * d.ex_d : 0;
+    case 15: return x ? tiled_bytes(d.ex_d, d.ex_d) : 0;
+    case 16: return x ? 4ull * d.ex_d : 0;
+    case 17: return x ? 2ull * d.ex_d * d.action_dim : 0;         // action in
+    case 18: return x ? 2ull * d.ex_d : 0;
+    case 19: return x ? 2ull * d.action_dim * d.ex_d : 0;         // action out
+    case 20: return x ? 2ull * d.action_dim : 0;
+    case 21: return x ? 2ull * d.ex_d : 0;                        // expert final norm
+    case 22: return x ? 4ull * d.euler_steps : 0;                 // flow-time schedule
+  }
+  return 0;
+}
+
+struct Arena {
+  char* base = nullptr;
+  uint64_t cap = 0, used = 0, high = 0;
+  char* alloc(uint64_t bytes, uint64_t align = 1024) {
+    uint64_t off = align_up(used, align);
+    if (off + bytes > cap) return nullptr;
+    used = off + bytes;
+    if (used > high) high = used;
+    return base + off;
+  }
+};
+
+struct GemvPlan {
+  int n, k, grid, max_contrib;
+};
+
+struct Module {
+  int kind;
+  int layers;
+  ls_layer_layout lay;
+  std::vector<const char*> host;
+  std::vector<char*> resident;  // nullptr: streamed
+  std::vector<int> phase_reps;
+};
+
+}  // namespace
+
+struct ls_exec {
+  ls_dims d;
+  int dev = 0, nsm = 148;
+  Arena ar;
+  cudaStream_t cs = nullptr, ss = nullptr;  // copy engine stream, compute stream
+  int n_slots = 2;
+  uint64_t slot_bytes = 0;
+  std::vector<char*> slots;
+  std::vector<cudaEvent_t> dma_done, comp_done;
+  cudaEvent_t inv_done = nullptr, exe_done = nullptr, ev_begin = nullptr, ev_t0 = nullptr,
+              ev_t1 = nullptr, ev_end = nullptr;
+  std::vector<cudaEvent_t> tev;  // timing event pool
+  std::vector<Module> mods;
+  char* g[LS_N_GLOBAL] = {};
+  uint64_t bytes_slots = 0, bytes_always = 0, bytes_overhead = 0, mark = 0;
+  int S = 0, ctx = 0, Tv = 0, Te = 0, vit_ffn_pad = 0, n_split = 1;
+  // activations
+  float *vit_h = nullptr, *lm_h = nullptr, *dec_h = nullptr, *dec_q = nullptr, *dec_attn = nullptr,
+        *dec_mlp = nullptr, *logits = nullptr, *attn_ws = nullptr, *gemv_ws = nullptr,
+        *ex_h = nullptr, *temb_in = nullptr, *temb_mid = nullptr, *temb = nullptr,
+        *actions = nullptr, *velocity = nullptr, *noise = nullptr;
+  bf16 *patches = nullptr, *vit_ln = nullptr, *vit_qkv = nullptr, *vit_attn = nullptr,
+       *vit_fc1 = nullptr, *merger_mid = nullptr, *lm_norm = nullptr, *lm_qkv = nullptr,
+       *lm_q = nullptr, *lm_attn = nullptr, *lm_mlp = nullptr, *kv = nullptr, *ex_norm = nullptr,
+       *ex_qkv = nullptr, *ex_q = nullptr, *ex_kv = nullptr, *ex_attn = nullptr, *ex_mlp = nullptr;
+  int *text_ids = nullptr, *token = nullptr, *hist = nullptr, *attn_cnt = nullptr,
+      *gemv_cnt = nullptr;
+  unsigned long long* amax = nullptr;
+  CUtensorMap m_patches, m_vit_ln, m_vit_attn, m_vit_fc1, m_merge_in, m_merger_mid, m_lm_norm,
+      m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
+  GemvPlan gp_qkv{}, gp_o{}, gp_gu{}, gp_down{}, gp_head{}, gp_t1{}, gp_t2{};
+  int64_t launches = 0, h2d_copies = 0;
+  uint64_t h2d_bytes = 0;
+
+  bf16* kc(int l) { return kv + static_cast<long>(l) * 2 * d.lm_hkv * (ctx + 1) * d.lm_hd; }
+  bf16* vc(int l) { return kc(l) + static_cast<long>(d.lm_hkv) * (ctx + 1) * d.lm_hd; }
+  int cache_stride() const { return (ctx + 1) * d.lm_hd; }
+};
+
+namespace {
+
+GemvPlan plan_gemv(int n, int k, int nsm) {
+  GemvPlan p{n, k, 0, 0};
+  p.grid = gemv_grid(n_mt(n), n_kb(k), nsm);
+  p.max_contrib = gemv_max_contrib(n_mt(n), n_kb(k), p.grid);
+  return p;
+}
+
+int alloc_into(ls_exec* e, void* dst_ptr, uint64_t bytes, uint64_t* counter) {
+  char* p = e->ar.alloc(bytes ? bytes : 16);
+  if (!p)
+    return set_error(LS_ERR_CAP,
+                     "emulated VRAM cap exceeded: need %llu more bytes (used %llu of %llu)",
+                     static_cast<unsigned long long>(bytes),
+                     static_cast<unsigned long long>(e->ar.used),
+                     static_cast<unsigned long long>(e->ar.cap));
+  *static_cast<char**>(dst_ptr) = p;
+  if (counter) *counter += bytes;
+  return LS_OK;
+}
+
+#define ALLOC(field, bytes, counter)                                      \
+  do {                                                                    \
+    int rc_ = alloc_into(e, &e->field, (bytes), &e->counter);             \
+    if (rc_) return rc_;                                                  \
+  } while (0)
+
+int tmap(CUtensorMap* m, const void* base, int rows, int cols, int ld) {
+  if (rows <= 0) return LS_OK;
+  int r = make_tmap_bf16(m, base, static_cast<uint64_t>(rows), static_cast<uint64_t>(cols),
+                         static_cast<uint64_t>(ld), static_cast<uint32_t>(gemm_block_n(rows)));
+  if (r) return set_error(LS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
+  return LS_OK;
+}
+
+// ---------------------------- launch helpers -----------------------------------
+
+int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensorMap& map, void* out,
+         long ldo, const void* bias_bf16 = nullptr, int n_valid = -1) {
+  GemmArgs a{};
+  a.w = reinterpret_cast<const uint8_t*>(w);
+  a.n_mt = n_mt(n);
+  a.n_kb = n_kb(k);
+  a.T = T;
+  a.out = out;
+  a.ldo = ldo;
+  a.bias_bf16 = static_cast<const bf16*>(bias_bf16);
+  a.n_valid = n_valid < 0 ? n : n_valid;
+  KL(launch_gemm(epi, a, map, e->ss));
+  return LS_OK;
+}
+
+int gemv(ls_exec* e, int epi, const GemvPlan& p, const char* w, const float* x, float* out,
+         const void* norm_w, const float* bias = nullptr, int n_valid = -1, GemvArgs* extra = nullptr) {
+  GemvArgs a = extra ? *extra : GemvArgs{};
+  a.w = reinterpret_cast<const uint8_t*>(w);
+  a.n_mt = n_mt(p.n);
+  a.n_kb = n_kb(p.k);
+  a.x = x;
+  a.norm_w = static_cast<const bf16*>(norm_w);
+  a.eps = e->d.lm_eps;
+  a.ws = e->gemv_ws;
+  a.counters = e->gemv_cnt;
+  a.max_contrib = p.max_contrib;
+  a.out = out;
+  a.bias = bias;
+  a.n_valid = n_valid < 0 ? p.n : n_valid;
+  a.amax = e->amax;
+  KL(launch_gemv(epi, a, p.grid, e->ss));
+  return LS_OK;
+}
+
+FlashArgs flash_base(int Tq, int hq, int hkv, int hd) {
+  FlashArgs f{};
+  f.Tq = Tq;
+  f.hq = hq;
+  f.hkv = hkv;
+  f.hd = hd;
+  f.scale = 1.0f / std::sqrt(static_cast<float>(hd));
+  return f;
+}
+
+#define RC(x)                \
+  do {                       \
+    int rc_ = (x);           \
+    if (rc_) return rc_;     \
+  } while (0)
+
+int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L) {
+  const ls_dims& d = e->d;
+  const int T = e->Tv, D = d.vit_d, H = d.vit_heads * d.vit_hd, F = d.vit_ffn;
+  const bf16* P = reinterpret_cast<const bf16*>(w);
+  auto part = [&](int i) { return w + L.offset[i]; };
+  (void)P;
+  KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(8), (const bf16*)part(9), e->vit_ln, T, D, D,
+                           d.vit_eps, e->ss));
+  RC(gemm(e, GEMM_BF16, part(0), 3 * H, D, T, e->m_vit_ln, e->vit_qkv, 3 * H, part(4)));
+  FlashArgs f = flash_base(T, d.vit_heads, d.vit_heads, d.vit_hd);
+  f.q = e->vit_qkv;
+  f.q_tok_stride = 3 * H;
+  f.q_head_stride = d.vit_hd;
+  f.k1 = e->vit_qkv + H;
+  f.v1 = e->vit_qkv + 2 * H;
+  f.k1_tok_stride = 3 * H;
+  f.k1_head_stride = d.vit_hd;
+  f.len1 = T;
+  f.out = e->vit_attn;
+  f.o_tok_stride = H;
+  f.o_head_stride = d.vit_hd;
+  f.seg_len = d.vit_tokens_per_image;
+  KL(launch_flash_attention(f, e->ss));
+  RC(gemm(e, GEMM_RESID_F32, part(1), D, H, T, e->m_vit_attn, e->vit_h, D, part(5)));
+  KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(10), (const bf16*)part(11), e->vit_ln, T, D,
+                           D, d.vit_eps, e->ss));
+  RC(gemm(e, GEMM_BF16_GELU, part(2), F, D, T, e->m_vit_ln, e->vit_fc1, e->vit_ffn_pad, part(6), F));
+  RC(gemm(e, GEMM_RESID_F32, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, D, part(7)));
+  return LS_OK;
+}
+
+int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
+  const ls_dims& d = e->d;
+  const int S = e->S, D = d.lm_d, QN = (d.lm_hq + 2 * d.lm_hkv) * d.lm_hd, AH = d.lm_hq * d.lm_hd;
+  auto part = [&](int i) { return w + L.offset[i]; };
+  KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(4), e->lm_norm, S, D, d.lm_eps, e->ss));
+  RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN));
+  KL(launch_qk_norm_rope(e->lm_qkv, S, d.lm_hq, d.lm_hkv, d.lm_hd, (const bf16*)part(6),
+                         (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], 0, e->lm_q,
+                         e->kc(l), e->vc(l), e->cache_stride(), e->ss));
+  FlashArgs f = flash_base(S, d.lm_hq, d.lm_hkv, d.lm_hd);
+  f.q = e->lm_q;
+  f.q_tok_stride = AH;
+  f.q_head_stride = d.lm_hd;
+  f.k1 = e->kc(l);
+  f.v1 = e->vc(l);
+  f.k1_tok_stride = d.lm_hd;
+  f.k1_head_stride = e->cache_stride();
+  f.len1 = S;
+  f.out = e->lm_attn;
+  f.o_tok_stride = AH;
+  f.o_head_stride = d.lm_hd;
+  f.causal = 1;
+  KL(launch_flash_attention(f, e->ss));
+  RC(gemm(e, GEMM_RESID_F32, part(1), D, AH, S, e->m_lm_attn, e->lm_h, D));
+  KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(5), e->lm_norm, S, D, d.lm_eps, e->ss));
+  RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.lm_ffn, D, S, e->m_lm_norm, e->lm_mlp, d.lm_ffn,
+          nullptr, d.lm_ffn));
+  RC(gemm(e, GEMM_RESID_F32, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h, D));
+  return LS_OK;
+}
+
+int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, int pos) {
+  const ls_dims& d = e->d;
+  auto part = [&](int i) { return w + L.offset[i]; };
+  GemvArgs q{};
+  q.hq = d.lm_hq;
+  q.hkv = d.lm_hkv;
+  q.hd = d.lm_hd;
+  q.pos = pos;
+  q.qn_w = (const bf16*)part(6);
+  q.kn_w = (const bf16*)part(7);
+  q.rope = (const float2*)e->g[3];
+  q.q_out = e->dec_q;
+  q.k_cache = e->kc(l);
+  q.v_cache = e->vc(l);
+  q.cache_head_stride = e->cache_stride();
+  RC(gemv(e, GEMV_QKV, e->gp_qkv, part(0), e->dec_h, e->dec_q, part(4), nullptr, -1, &q));
+  DecodeAttnArgs a{};
+  a.q = e->dec_q;
+  a.k_cache = e->kc(l);
+  a.v_cache = e->vc(l);
+  a.cache_head_stride = e->cache_stride();
+  a.hq = d.lm_hq;
+  a.hkv = d.lm_hkv;
+  a.hd = d.lm_hd;
+  a.n_ctx = pos + 1;
+  a.scale = 1.0f / std::sqrt(static_cast<float>(d.lm_hd));
+  a.out = e->dec_attn;
+  a.ws = e->attn_ws;
+  a.counters = e->attn_cnt;
+  a.n_split = std::min(e->n_split, std::max(1, (pos + 1 + 31) / 32));
+  KL(launch_decode_attention(a, e->ss));
+  RC(gemv(e, GEMV_RESID, e->gp_o, part(1), e->dec_attn, e->dec_h, nullptr));
+  RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn));
+  RC(gemv(e, GEMV_RESID, e->gp_down, part(3), e->dec_mlp, e->dec_h, nullptr));
+  return LS_OK;
+}
+
+int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
+  const ls_dims& d = e->d;
+  const int T = e->Te, D = d.ex_d, QN = (d.ex_hq + 2 * d.ex_hkv) * d.ex_hd, AH = d.ex_hq * d.ex_hd;
+  auto part = [&](int i) { return w + L.offset[i]; };
+  bf16* ek = e->ex_kv;
+  bf16* ev = e->ex_kv + static_cast<long>(d.ex_hkv) * T * d.ex_hd;
+  const long shift = static_cast<long>(e->ctx) * d.ex_hd;  // store index t, RoPE position ctx + t
+  KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(4), e->ex_norm, T, D, d.lm_eps, e->ss));
+  RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN));
+  KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
+                         (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], e->ctx, e->ex_q,
+                         ek - shift, ev - shift, T * d.ex_hd, e->ss));
+  FlashArgs f = flash_base(T, d.ex_hq, d.ex_hkv, d.ex_hd);
+  f.q = e->ex_q;
+  f.q_tok_stride = AH;
+  f.q_head_stride = d.ex_hd;
+  f.k1 = e->kc(l);
+  f.v1 = e->vc(l);
+  f.k1_tok_stride = d.lm_hd;
+  f.k1_head_stride = e->cache_stride();
+  f.len1 = e->ctx;
+  f.k2 = ek;
+  f.v2 = ev;
+  f.k2_tok_stride = d.ex_hd;
+  f.k2_head_stride = static_cast<long>(T) * d.ex_hd;
+  f.len2 = T;
+  f.out = e->ex_attn;
+  f.o_tok_stride = AH;
+  f.o_head_stride = d.ex_hd;
+  KL(launch_flash_attention(f, e->ss));
+  RC(gemm(e, GEMM_RESID_F32, part(1), D, AH, T, e->m_ex_attn, e->ex_h, D));
+  KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
+  RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.ex_ffn, D, T, e->m_ex_norm, e->ex_mlp, d.ex_ffn,
+          nullptr, d.ex_ffn));
+  RC(gemm(e, GEMM_RESID_F32, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, D));
+  return LS_OK;
+}
+
+// Work before / after each invocation (phase sweep) that is not a layer:
+// embeddings, merger, lm head + greedy argmax, flow-time MLP, Euler step.
+int pre_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* io) {
+  const ls_dims& d = e->d;
+  if (kind == LS_KIND_VIT) {
+    RC(gemm(e, GEMM_F32, e->g[4], d.vit_d, d.vit_patch_dim, e->Tv, e->m_patches, e->vit_h, d.vit_d,
+            e->g[5]));
+    KL(launch_add_rows_bf16(e->vit_h, (const bf16*)e->g[6], e->Tv, d.vit_d, d.vit_tokens_per_image,
+                            e->ss));
+  } else if (kind == LS_KIND_LM) {
+    if (phase == 0) {
+      KL(launch_embed_rows((const bf16*)e->g[0], e->text_ids, d.prompt_prefix, d.lm_d, e->lm_h,
+                           d.lm_d, e->ss));
+      KL(launch_embed_rows((const bf16*)e->g[0], e->text_ids + d.prompt_prefix, d.prompt_suffix,
+                           d.lm_d, e->lm_h + static_cast<long>(d.prompt_prefix + vis_tokens(d)) * d.lm_d,
+                           d.lm_d, e->ss));
+    } else {
+      KL(launch_embed_rows((const bf16*)e->g[0], e->token, 1, d.lm_d, e->dec_h, d.lm_d, e->ss));
+    }
+  } else {
+    if (inv == 0)
+      CK(cudaMemcpyAsync(e->actions, e->noise, 4ull * d.ex_tokens * d.action_dim,
+                         cudaMemcpyDeviceToDevice, e->ss));
+    KL(launch_time_embed((const float*)e->g[22], inv, d.time_dim, e->temb_in, e->ss));
+    RC(gemv(e, GEMV_F32, e->gp_t1, e->g[13], e->temb_in, e->temb_mid, nullptr, (const float*)e->g[14]));
+    KL(launch_silu_inplace(e->temb_mid, d.ex_d, e->ss));
+    RC(gemv(e, GEMV_F32, e->gp_t2, e->g[15], e->temb_mid, e->temb, nullptr, (const float*)e->g[16]));
+    KL(launch_action_in(e->actions, (const bf16*)e->g[17], (const bf16*)e->g[18], e->temb, e->Te,
+                        d.action_dim, d.ex_d, e->ex_h, e->ss));
+  }
+  (void)io;
+  return LS_OK;
+}
+
+int post_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* io) {
+  const ls_dims& d = e->d;
+  if (kind == LS_KIND_VIT) {
+    const int T4 = e->Tv / 4, MD = 4 * d.vit_d;
+    KL(launch_layernorm_rows(e->vit_h, (const bf16*)e->g[7], (const bf16*)e->g[8], e->vit_ln, e->Tv,
+                             d.vit_d, d.vit_d, d.vit_eps, e->ss));
+    RC(gemm(e, GEMM_BF16_GELU, e->g[9], MD, MD, T4, e->m_merge_in, e->merger_mid, MD, e->g[10]));
+    RC(gemm(e, GEMM_F32, e->g[11], d.lm_d, MD, T4, e->m_merger_mid,
+            e->lm_h + static_cast<long>(d.prompt_prefix) * d.lm_d, d.lm_d, e->g[12]));
+  } else if (kind == LS_KIND_LM) {
+    const int step = phase == 0 ? 0 : inv + 1;
+    const float* x = phase == 0 ? e->lm_h + static_cast<long>(e->S - 1) * d.lm_d : e->dec_h;
+    RC(gemv(e, GEMV_ARGMAX, e->gp_head, e->g[1], x, e->logits, e->g[2]));
+    KL(launch_argmax_to_token(e->amax, e->token, e->hist, step, e->amax, e->ss));
+    if (io->logits_out)
+      CK(cudaMemcpyAsync(io->logits_out + static_cast<long>(step) * d.vocab, e->logits,
+                         4ull * d.vocab, cudaMemcpyDeviceToDevice, e->ss));
+  } else {
+    KL(launch_action_out_euler(e->ex_h, (const bf16*)e->g[21], d.lm_eps, (const bf16*)e->g[19],
+                               (const bf16*)e->g[20], e->Te, d.ex_d, d.action_dim,
+                               -1.0f / d.euler_steps, e->actions, e->velocity, e->ss));
+  }
+  return LS_OK;
+}
+
+int run_layer(ls_exec* e, const Module& m, int phase, int inv, int l, const char* w) {
+  switch (m.kind) {
+    case LS_KIND_VIT: return vit_layer(e, w, m.lay);
+    case LS_KIND_LM:
+      return phase == 0 ? lm_prefill_layer(e, w, m.lay, l) : lm_decode_layer(e, w, m.lay, l, e->S + inv);
+    default: return expert_layer(e, w, m.lay, l);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ls_layer_layout_of(const ls_dims* d, int32_t kind, ls_layer_layout* out) {
+  if (kind == LS_KIND_VIT) layout_vit(d->vit_d, d->vit_heads, d->vit_hd, d->vit_ffn, out);
+  else if (kind == LS_KIND_LM) layout_decoder(d->lm_d, d->lm_hq, d->lm_hkv, d->lm_hd, d->lm_ffn, out);
+  else if (kind == LS_KIND_EXPERT) layout_decoder(d->ex_d, d->ex_hq, d->ex_hkv, d->ex_hd, d->ex_ffn, out);
+  else return set_error(LS_ERR_VALUE, "unknown module kind %d", kind);
+  return LS_OK;
+}
+
+int ls_global_size(const ls_dims* d, int32_t id, uint64_t* bytes) {
+  if (id < 0 || id >= LS_N_GLOBAL) return set_error(LS_ERR_VALUE, "bad global id %d", id);
+  *bytes = global_bytes(*d, id);
+  return LS_OK;
+}
+
+int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int32_t n_slots,
+                   ls_exec** out) {
+  ls_exec* e = new ls_exec();
+  e->d = *dims;
+  const ls_dims& d = e->d;
+  e->dev = device;
+  e->n_slots = n_slots < 1 ? 1 : n_slots;
+  auto fail = [&](int rc) {
+    ls_exec_destroy(e);
+    return rc;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return fail(set_error(LS_ERR_CUDA, "cudaSetDevice(%d) failed", device));
+  cudaDeviceGetAttribute(&e->nsm, cudaDevAttrMultiProcessorCount, device);
+  if (d.lm_hd != (d.has_expert ? d.ex_hd : d.lm_hd) || (d.has_expert && d.ex_hkv != d.lm_hkv))
+    return fail(set_error(LS_ERR_VALUE, "expert KV heads must match the LM's (joint attention)"));
+  e->S = prompt_len(d);
+  e->ctx = ctx_len(d);
+  e->Tv = d.has_vit ? d.vit_images * d.vit_tokens_per_image : 0;
+  e->Te = d.has_expert ? d.ex_tokens : 0;
+  e->vit_ffn_pad = n_kb(d.vit_ffn) * 64 > n_mt(d.vit_ffn) * 128 ? n_kb(d.vit_ffn) * 64 : n_mt(d.vit_ffn) * 128;
+  // modules in profile order
+  if (d.has_vit) {
+    Module m{LS_KIND_VIT, d.vit_layers, {}, {}, {}, {1}};
+    layout_vit(d.vit_d, d.vit_heads, d.vit_hd, d.vit_ffn, &m.lay);
+    e->mods.push_back(m);
+  }
+  {
+    Module m{LS_KIND_LM, d.lm_layers, {}, {}, {}, {1, d.decode_steps}};
+    layout_decoder(d.lm_d, d.lm_hq, d.lm_hkv, d.lm_hd, d.lm_ffn, &m.lay);
+    e->mods.push_back(m);
+  }
+  if (d.has_expert) {
+    Module m{LS_KIND_EXPERT, d.ex_layers, {}, {}, {}, {d.euler_steps}};
+    layout_decoder(d.ex_d, d.ex_hq, d.ex_hkv, d.ex_hd, d.ex_ffn, &m.lay);
+    e->mods.push_back(m);
+  }
+  for (auto& m : e->mods) {
+    m.host.assign(m.layers, nullptr);
+    m.resident.assign(m.layers, nullptr);
+    if (m.lay.total > e->slot_bytes) e->slot_bytes = m.lay.total;
+  }
+  if (cudaMalloc(&e->ar.base, cap_bytes) != cudaSuccess)
+    return fail(set_error(LS_ERR_CUDA, "cudaMalloc of the %llu-byte VRAM arena failed",
+                          static_cast<unsigned long long>(cap_bytes)));
+  e->ar.cap = cap_bytes;
+  if (cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->ss, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(set_error(LS_ERR_CUDA, "stream creation failed"));
+  // 1. DFB slot ring
+  for (int s = 0; s < e->n_slots; ++s) {
+    char* p = nullptr;
+    if (int rc = alloc_into(e, &p, e->slot_bytes, &e->bytes_slots)) return fail(rc);
+    e->slots.push_back(p);
+    cudaEvent_t a, b;
+    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    e->dma_done.push_back(a);
+    e->comp_done.push_back(b);
+  }
+  // 2. always-resident tensors
+  for (int i = 0; i < LS_N_GLOBAL; ++i) {
+    uint64_t b = global_bytes(d, i);
+    if (!b) continue;
+    if (int rc = alloc_into(e, &e->g[i], b, &e->bytes_always)) return fail(rc);
+  }
+  // 3. overhead: KV cache, activations, workspaces
+  {
+    const long S = e->S, Tv = e->Tv, Te = e->Te;
+    const int QN = (d.lm_hq + 2 * d.lm_hkv) * d.lm_hd, AH = d.lm_hq * d.lm_hd;
+    auto A = [&](void* dst, uint64_t bytes) { return alloc_into(e, dst, bytes, &e->bytes_overhead); };
+#define OV(field, bytes) \
+  if (int rc = A(&e->field, (bytes))) return fail(rc)
+    OV(kv, 2ull * d.lm_layers * 2 * d.lm_hkv * (e->ctx + 1) * d.lm_hd);
+    OV(lm_h, 4ull * S * d.lm_d);
+    OV(lm_norm, 2ull * S * d.lm_d);
+    OV(lm_qkv, 2ull * S * QN);
+    OV(lm_q, 2ull * S * AH);
+    OV(lm_attn, 2ull * S * AH);
+    OV(lm_mlp, 2ull * S * d.lm_ffn);
+    OV(text_ids, 4ull * (d.prompt_prefix + d.prompt_suffix + 1));
+    OV(dec_h, 4ull * d.lm_d);
+    OV(dec_q, 4ull * AH);
+    OV(dec_attn, 4ull * AH);
+    OV(dec_mlp, 4ull * d.lm_ffn);
+    OV(logits, 4ull * d.vocab);
+    OV(amax, 16);
+    OV(token, 16);
+    OV(hist, 4ull * (d.decode_steps + 1));
+    e->n_split = std::max(1, std::min(64, e->nsm / d.lm_hkv));
+    OV(attn_ws, 4ull * d.lm_hq * e->n_split * (d.lm_hd + 2));
+    OV(attn_cnt, 4ull * d.lm_hkv);
+    e->gp_qkv = plan_gemv(QN, d.lm_d, e->nsm);
+    e->gp_o = plan_gemv(d.lm_d, AH, e->nsm);
+    e->gp_gu = plan_gemv(2 * d.lm_ffn, d.lm_d, e->nsm);
+    e->gp_down = plan_gemv(d.lm_d, d.lm_ffn, e->nsm);
+    e->gp_head = plan_gemv(d.vocab, d.lm_d, e->nsm);
+    std::vector<GemvPlan> plans = {e->gp_qkv, e->gp_o, e->gp_gu, e->gp_down, e->gp_head};
+    if (d.has_expert) {
+      e->gp_t1 = plan_gemv(d.ex_d, d.time_dim, e->nsm);
+      e->gp_t2 = plan_gemv(d.ex_d, d.ex_d, e->nsm);
+      plans.push_back(e->gp_t1);
+      plans.push_back(e->gp_t2);
+    }
+    uint64_t ws = 0, cnt = 0;
+    for (auto& p : plans) {
+      ws = std::max<uint64_t>(ws, 4ull * n_mt(p.n) * p.max_contrib * 128);
+      cnt = std::max<uint64_t>(cnt, 4ull * n_mt(p.n));
+    }
+    OV(gemv_ws, ws);
+    OV(gemv_cnt, cnt);
+    if (d.has_vit) {
+      const int H = d.vit_heads * d.vit_hd;
+      OV(patches, 2ull * Tv * d.vit_patch_dim);
+      OV(vit_h, 4ull * Tv * d.vit_d);
+      OV(vit_ln, 2ull * Tv * d.vit_d);
+      OV(vit_qkv, 2ull * Tv * 3 * H);
+      OV(vit_attn, 2ull * Tv * H);
+      OV(vit_fc1, 2ull * Tv * e->vit_ffn_pad);
+      OV(merger_mid, 2ull * (Tv / 4) * 4 * d.vit_d);
+    }
+    if (d.has_expert) {
+      const int EQN = (d.ex_hq + 2 * d.ex_hkv) * d.ex_hd, EAH = d.ex_hq * d.ex_hd;
+      OV(ex_h, 4ull * Te * d.ex_d);
+      OV(ex_norm, 2ull * Te * d.ex_d);
+      OV(ex_qkv, 2ull * Te * EQN);
+      OV(ex_q, 2ull * Te * EAH);
+      OV(ex_kv, 2ull * 2 * d.ex_hkv * Te * d.ex_hd);
+      OV(ex_attn, 2ull * Te * EAH);
+      OV(ex_mlp, 2ull * Te * d.ex_ffn);
+      OV(temb_in, 4ull * d.time_dim);
+      OV(temb_mid, 4ull * d.ex_d);
+      OV(temb, 4ull * d.ex_d);
+      OV(actions, 4ull * Te * d.action_dim);
+      OV(velocity, 4ull * Te * d.action_dim);
+      OV(noise, 4ull * Te * d.action_dim);
+    }
+#undef OV
+    if (cudaMemset(e->ar.base, 0, e->ar.used) != cudaSuccess)
+      return fail(set_error(LS_ERR_CUDA, "arena memset failed"));
+    int rc = 0;
+    const int AHe = d.ex_hq * d.ex_hd;
+    if ((rc = tmap(&e->m_lm_norm, e->lm_norm, S, d.lm_d, d.lm_d)) ||
+        (rc = tmap(&e->m_lm_attn, e->lm_attn, S, AH, AH)) ||
+        (rc = tmap(&e->m_lm_mlp, e->lm_mlp, S, d.lm_ffn, d.lm_ffn)))
+      return fail(rc);
+    if (d.has_vit) {
+      const int H = d.vit_heads * d.vit_hd;
+      if ((rc = tmap(&e->m_patches, e->patches, Tv, d.vit_patch_dim, d.vit_patch_dim)) ||
+          (rc = tmap(&e->m_vit_ln, e->vit_ln, Tv, d.vit_d, d.vit_d)) ||
+          (rc = tmap(&e->m_vit_attn, e->vit_attn, Tv, H, H)) ||
+          (rc = tmap(&e->m_vit_fc1, e->vit_fc1, Tv, e->vit_ffn_pad, e->vit_ffn_pad)) ||
+          (rc = tmap(&e->m_merge_in, e->vit_ln, Tv / 4, 4 * d.vit_d, 4 * d.vit_d)) ||
+          (rc = tmap(&e->m_merger_mid, e->merger_mid, Tv / 4, 4 * d.vit_d, 4 * d.vit_d)))
+        return fail(rc);
+    }
+    if (d.has_expert) {
+      if ((rc = tmap(&e->m_ex_norm, e->ex_norm, Te, d.ex_d, d.ex_d)) ||
+          (rc = tmap(&e->m_ex_attn, e->ex_attn, Te, AHe, AHe)) ||
+          (rc = tmap(&e->m_ex_mlp, e->ex_mlp, Te, d.ex_ffn, d.ex_ffn)))
+        return fail(rc);
+    }
+  }
+  e->mark = e->ar.used;
+  cudaEvent_t* evs[] = {&e->inv_done, &e->exe_done};
+  for (auto p : evs) cudaEventCreateWithFlags(p, cudaEventDisableTiming);
+  cudaEvent_t* tevs[] = {&e->ev_begin, &e->ev_t0, &e->ev_t1, &e->ev_end};
+  for (auto p : tevs) cudaEventCreate(p);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(set_error(LS_ERR_CUDA, "setup failed"));
+  *out = e;
+  return LS_OK;
+}
+
+int ls_exec_destroy(ls_exec* e) {
+  if (!e) return LS_OK;
+  if (e->ss) cudaStreamSynchronize(e->ss);
+  if (e->cs) cudaStreamSynchronize(e->cs);
+  for (auto v : e->dma_done) cudaEventDestroy(v);
+  for (auto v : e->comp_done) cudaEventDestroy(v);
+  for (auto v : e->tev) cudaEventDestroy(v);
+  cudaEvent_t evs[] = {e->inv_done, e->exe_done, e->ev_begin, e->ev_t0, e->ev_t1, e->ev_end};
+  for (auto v : evs)
+    if (v) cudaEventDestroy(v);
+  if (e->cs) cudaStreamDestroy(e->cs);
+  if (e->ss) cudaStreamDestroy(e->ss);
+  if (e->ar.base) cudaFree(e->ar.base);
+  delete e;
+  return LS_OK;
+}
+
+int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr) {
+  if (id < 0 || id >= LS_N_GLOBAL) return set_error(LS_ERR_VALUE, "bad global id %d", id);
+  *dptr = e->g[id];
+  return LS_OK;
+}
+
+int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_ptrs, int32_t n) {
+  for (auto& m : e->mods) {
+    if (m.kind != kind) continue;
+    if (n != m.layers) return set_error(LS_ERR_VALUE, "expected %d host layers, got %d", m.layers, n);
+    for (int i = 0; i < n; ++i) m.host[i] = static_cast<const char*>(host_ptrs[i]);
+    return LS_OK;
+  }
+  return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
+}
+
+int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n) {
+  int64_t total = 0;
+  for (auto& m : e->mods) total += m.layers;
+  if (n != total) return set_error(LS_ERR_VALUE, "placement mask has %lld entries, expected %lld",
+                                   static_cast<long long>(n), static_cast<long long>(total));
+  CK(cudaStreamSynchronize(e->ss));
+  CK(cudaStreamSynchronize(e->cs));
+  e->ar.used = e->mark;
+  int64_t off = 0;
+  for (auto& m : e->mods) {
+    for (int l = 0; l < m.layers; ++l) {
+      m.resident[l] = nullptr;
+      if (!mask[off + l]) continue;
+      if (!m.host[l]) return set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind);
+      char* p = e->ar.alloc(m.lay.total, 256);
+      if (!p)
+        return set_error(LS_ERR_CAP,
+                         "resident layers exceed the emulated VRAM cap (%llu bytes used of %llu)",
+                         static_cast<unsigned long long>(e->ar.used),
+                         static_cast<unsigned long long>(e->ar.cap));
+      CK(cudaMemcpyAsync(p, m.host[l], m.lay.total, cudaMemcpyHostToDevice, e->cs));
+      m.resident[l] = p;
+    }
+    off += m.layers;
+  }
+  CK(cudaStreamSynchronize(e->cs));
+  return LS_OK;
+}
+
+int ls_exec_memory(ls_exec* e, uint64_t out[7]) {
+  out[0] = e->ar.cap;
+  out[1] = e->ar.used;
+  out[2] = e->ar.high;
+  out[3] = e->bytes_slots;
+  out[4] = e->bytes_always;
+  out[5] = e->bytes_overhead;
+  out[6] = e->ar.used - e->mark;
+  return LS_OK;
+}
+
+int ls_exec_stats(ls_exec* e, int64_t out[3]) {
+  out[0] = e->launches;    // kernels launched by the last run
+  out[1] = e->h2d_copies;  // streamed-layer transfers of the last run
+  out[2] = static_cast<int64_t>(e->h2d_bytes);
+  return LS_OK;
+}
+
+int ls_exec_streams(ls_exec* e, void** copy_stream, void** compute_stream) {
+  *copy_stream = e->cs;
+  *compute_stream = e->ss;
+  return LS_OK;
+}
+
+int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_event* events,
+                int64_t capacity, int64_t* n_events, double* total_ms, double* e2e_ms) {
+  const ls_dims& d = e->d;
+  const bool seq = opts->cfg.mode == LS_MODE_SEQUENTIAL;
+  const bool barrier = seq || !opts->cfg.cross_invocation_prefetch;
+  const int nsl = std::max(1, std::min(opts->cfg.slot_count, e->n_slots));
+  const bool timing = opts->record_timeline && events;
+  for (auto& m : e->mods)
+    for (int l = 0; l < m.layers; ++l)
+      if (!m.resident[l] && !m.host[l])
+        return set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind);
+  // timing event pool
+  int64_t need = 0;
+  for (auto& m : e->mods)
+    for (int r : m.phase_reps) need += 4ll * r * m.layers;
+  if (timing) {
+    if (capacity * 2 < need) return set_error(LS_ERR_VALUE, "event buffer too small");
+    while (static_cast<int64_t>(e->tev.size()) < need) {
+      cudaEvent_t v;
+      CK(cudaEventCreate(&v));
+      e->tev.push_back(v);
+    }
+  }
+  struct Rec {
+    int engine, module, phase, inv, layer, ev0, ev1;
+  };
+  std::vector<Rec> recs;
+  if (timing) recs.reserve(static_cast<size_t>(need / 2));
+  int next_ev = 0;
+  auto tick = [&](cudaStream_t s) {
+    cudaEventRecord(e->tev[next_ev], s);
+    return next_ev++;
+  };
+
+  e->launches = 0;
+  e->h2d_copies = 0;
+  e->h2d_bytes = 0;
+  const cudaMemcpyKind kin = io->on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CK(cudaEventRecord(e->ev_begin, e->ss));
+  if (d.has_vit && io->patches)
+    CK(cudaMemcpyAsync(e->patches, io->patches, 2ull * e->Tv * d.vit_patch_dim, kin, e->ss));
+  if (io->text_ids)
+    CK(cudaMemcpyAsync(e->text_ids, io->text_ids, 4ull * (d.prompt_prefix + d.prompt_suffix), kin, e->ss));
+  if (d.has_expert && io->noise)
+    CK(cudaMemcpyAsync(e->noise, io->noise, 4ull * e->Te * d.action_dim, kin, e->ss));
+  CK(cudaEventRecord(e->ev_t0, e->ss));
+  CK(cudaStreamWaitEvent(e->cs, e->ev_t0, 0));
+
+  std::vector<bool> slot_used(static_cast<size_t>(nsl), false);
+  bool pending_barrier = false;
+  for (int mi = 0; mi < static_cast<int>(e->mods.size()); ++mi) {
+    const Module& m = e->mods[mi];
+    for (int ph = 0; ph < static_cast<int>(m.phase_reps.size()); ++ph) {
+      for (int inv = 0; inv < m.phase_reps[ph]; ++inv) {
+        RC(pre_invocation(e, m.kind, ph, inv, io));
+        int sseq = 0;
+        for (int l = 0; l < m.layers; ++l) {
+          const char* w = m.resident[l];
+          int slot = -1, dma0 = -1, dma1 = -1;
+          if (!w) {
+            slot = sseq++ % nsl;
+            if (slot_used[slot]) CK(cudaStreamWaitEvent(e->cs, e->comp_done[slot], 0));
+            if (seq) CK(cudaStreamWaitEvent(e->cs, e->exe_done, 0));
+            if (pending_barrier) {
+              CK(cudaStreamWaitEvent(e->cs, e->inv_done, 0));
+              pending_barrier = false;
+            }
+            if (timing) dma0 = tick(e->cs);
+            CK(cudaMemcpyAsync(e->slots[slot], m.host[l], m.lay.total, cudaMemcpyHostToDevice, e->cs));
+            ++e->h2d_copies;
+            e->h2d_bytes += m.lay.total;
+            if (timing) dma1 = tick(e->cs);
+            CK(cudaEventRecord(e->dma_done[slot], e->cs));
+            CK(cudaStreamWaitEvent(e->ss, e->dma_done[slot], 0));
+            w = e->slots[slot];
+          }
+          int x0 = timing ? tick(e->ss) : -1;
+          RC(run_layer(e, m, ph, inv, l, w));
+          int x1 = timing ? tick(e->ss) : -1;
+          if (slot >= 0) {
+            CK(cudaEventRecord(e->comp_done[slot], e->ss));
+            slot_used[slot] = true;
+          }
+          if (seq) CK(cudaEventRecord(e->exe_done, e->ss));
+          if (timing) {
+            if (slot >= 0) recs.push_back({0, mi, ph, inv, l, dma0, dma1});
+            recs.push_back({1, mi, ph, inv, l, x0, x1});
+          }
+        }
+        if (barrier) {
+          CK(cudaEventRecord(e->inv_done, e->ss));
+          pending_barrier = true;
+        }
+        RC(post_invocation(e, m.kind, ph, inv, io));
+      }
+    }
+  }
+  CK(cudaEventRecord(e->ev_t1, e->ss));
+  const cudaMemcpyKind kout = io->on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (io->tokens_out)
+    CK(cudaMemcpyAsync(io->tokens_out, e->hist, 4ull * (d.decode_steps + 1), kout, e->ss));
+  if (d.has_expert && io->actions_out)
+    CK(cudaMemcpyAsync(io->actions_out, e->actions, 4ull * e->Te * d.action_dim, kout, e->ss));
+  CK(cudaEventRecord(e->ev_end, e->ss));
+  CK(cudaStreamSynchronize(e->ss));
+  CK(cudaStreamSynchronize(e->cs));
+  CK(cudaGetLastError());
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e->ev_t0, e->ev_t1));
+  *total_ms = ms;
+  CK(cudaEventElapsedTime(&ms, e->ev_begin, e->ev_end));
+  if (e2e_ms) *e2e_ms = ms;
+  int64_t n = 0;
+  if (timing) {
+    for (const Rec& r : recs) {
+      float a = 0.f, b = 0.f;
+      CK(cudaEventElapsedTime(&a, e->ev_t0, e->tev[r.ev0]));
+      CK(cudaEventElapsedTime(&b, e->ev_t0, e->tev[r.ev1]));
+      ls_event& x = events[n++];
+      x.engine = r.engine;
+      x.module = r.module;
+      x.phase = r.phase;
+      x._pad = 0;
+      x.invocation = r.inv;
+      x.layer = r.layer;
+      x.start_ms = a < 0 ? 0.0 : a;
+      x.end_ms = b < a ? a : b;
+    }
+  }
+  if (n_events) *n_events = n;
+  return LS_OK;
+}
+
+}  // extern "C"

@@ -123,7 +123,7 @@ cudaError_t launch_argmax_to_token(const unsigned long long* key, int* token_out
 cudaError_t launch_action_in(const float* actions, const bf16* w_in, const bf16* b_in,
                              const float* temb, int n_tok, int a_dim, int D, float* out,
                              cudaStream_t st);
-cudaError_t launch_time_embed(const float* t_scalar_table, int step, int dim, bf16* out,
+cudaError_t launch_time_embed(const float* t_scalar_table, int step, int dim, float* out,
                               cudaStream_t st);
 cudaError_t launch_action_out_euler(const float* h, const bf16* norm_w, float eps,
                                     const bf16* w_out, const bf16* b_out, int n_tok, int D,

@@ -1,0 +1,339 @@
+"""The B200 Pipelined Demand Layering engine: the real executor behind the
+reference's schedule model.
+
+`DemandLayeringEngine.execute(placement, config)` runs one Alpamayo-shaped
+inference through the native DFB executor (csrc/executor.cu) and returns the
+outputs plus a `dfbsim.Timeline` built from CUDA event timestamps -- the same
+type and event order as `dfbsim.simulate` (dfbsim.py:179-247), so measured and
+simulated timelines are directly comparable.  `profile_run` is the paper's
+Sequential-DL profiling pass that emits a reference-schema
+ModelProfile for the planner; `infer` is the end-to-end call with host
+buffers.  Weights live in a page-locked host arena (one flat buffer per
+layer); the device holds only what the emulated VRAM cap allows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import statistics
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from . import model as M
+from .dfbsim import Engine as EngineKind
+from .dfbsim import Mode, Placement, SimConfig, SimEvent, Timeline
+from .profile import HardwareProfile, ModelProfile, ModuleProfile, PhaseProfile
+
+MIB = 2 ** 20
+
+
+class RunIO(C.Structure):
+    _fields_ = [("on_host", C.c_int32), ("_pad", C.c_int32), ("patches", C.c_void_p),
+                ("text_ids", C.c_void_p), ("noise", C.c_void_p), ("tokens_out", C.c_void_p),
+                ("actions_out", C.c_void_p), ("logits_out", C.c_void_p)]
+
+
+class RunOpts(C.Structure):
+    _fields_ = [("cfg", _native.SimCfg), ("record_timeline", C.c_int32)]
+
+
+def _bind():
+    lib = _native.lib()
+    if getattr(lib, "_engine_bound", False):
+        return lib
+    vp = C.c_void_p
+    sigs = {
+        "ls_exec_create": [C.POINTER(M.Dims), C.c_int32, C.c_uint64, C.c_int32, C.POINTER(vp)],
+        "ls_exec_destroy": [vp],
+        "ls_exec_global_ptr": [vp, C.c_int32, C.POINTER(vp)],
+        "ls_exec_set_host_layers": [vp, C.c_int32, C.POINTER(vp), C.c_int32],
+        "ls_exec_set_placement": [vp, C.POINTER(C.c_uint8), C.c_int64],
+        "ls_exec_memory": [vp, C.POINTER(C.c_uint64)],
+        "ls_exec_streams": [vp, C.POINTER(vp), C.POINTER(vp)],
+        "ls_exec_stats": [vp, C.POINTER(C.c_int64)],
+        "ls_exec_run": [vp, C.POINTER(RunIO), C.POINTER(RunOpts), C.POINTER(_native.Event),
+                        C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                        C.POINTER(C.c_double)],
+        "ls_host_alloc": [C.c_uint64, C.POINTER(vp)],
+        "ls_host_free": [vp],
+        "ls_copy": [vp, vp, C.c_uint64],
+    }
+    for name, args in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    lib._engine_bound = True
+    return lib
+
+
+@dataclass
+class RunResult:
+    tokens: torch.Tensor            # int32 [decode_steps + 1] (greedy ids)
+    actions: torch.Tensor | None    # fp32 [ex_tokens x action_dim] (flow-matching output)
+    logits: torch.Tensor | None     # fp32 [(decode_steps + 1) x vocab] when requested
+    total_ms: float                 # device time, first DMA/EXE to last EXE
+    e2e_ms: float                   # including input/output copies
+    timeline: Timeline | None
+
+
+class HostArena:
+    """Page-locked host buffer (cudaHostAlloc) viewed as a torch uint8 tensor."""
+
+    def __init__(self, nbytes: int) -> None:
+        self._lib = _bind()
+        self.ptr = C.c_void_p()
+        _native.check(self._lib.ls_host_alloc(nbytes, C.byref(self.ptr)), RuntimeError)
+        self.nbytes = nbytes
+        raw = (C.c_uint8 * nbytes).from_address(self.ptr.value)
+        self.tensor = torch.frombuffer(raw, dtype=torch.uint8)
+
+    def close(self) -> None:
+        if self.ptr:
+            self.tensor = None
+            self._lib.ls_host_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+class DemandLayeringEngine:
+    """One GPU, one model, one emulated VRAM cap.  Not thread-safe (one
+    enqueue thread per GPU)."""
+
+    def __init__(self, cfg: M.ModelConfig = M.ALPAMAYO, *, device: int = 0,
+                 vram_cap_mb: float = 16000.0, n_slots: int = 2, seed: int = 0,
+                 keep_logical: bool = False) -> None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("DemandLayeringEngine needs a CUDA device (B200, sm_100a)")
+        self.lib = _bind()
+        self.cfg = cfg
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self.vram_cap_mb = vram_cap_mb
+        self.n_slots = n_slots
+        self.seed = seed
+        torch.cuda.set_device(device)
+        self._dims = cfg.dims()
+        self.handle = C.c_void_p()
+        _native.check(self.lib.ls_exec_create(C.byref(self._dims), device, int(vram_cap_mb * MIB),
+                                              n_slots, C.byref(self.handle)), RuntimeError)
+        self.kinds = cfg.kinds
+        self.layouts = {k: M.layer_layout(cfg, k) for k in self.kinds}
+        self.logical: dict | None = {"layers": {}, "globals": {}} if keep_logical else None
+        self.arenas: dict[int, HostArena] = {}
+        self._placement_key = None
+        self._init_globals()
+        self._init_layers()
+
+    # ---------------------------------------------------------------- setup --
+    def _global_ptr(self, gid: int) -> int:
+        p = C.c_void_p()
+        _native.check(self.lib.ls_exec_global_ptr(self.handle, gid, C.byref(p)), RuntimeError)
+        return p.value
+
+    def _init_globals(self) -> None:
+        tensors = M.global_tensors(self.cfg, self.seed, self.dev)
+        for gid, t in tensors.items():
+            raw = M.global_bytes_of(gid, t)
+            size = M.global_size(self.cfg, gid)
+            assert raw.numel() == size, (gid, raw.numel(), size)
+            _copy_to_device_ptr(self._global_ptr(gid), raw)
+            if self.logical is not None:
+                self.logical["globals"][gid] = t.float().cpu()
+        torch.cuda.synchronize()
+
+    def _init_layers(self) -> None:
+        for kind in self.kinds:
+            lay = self.layouts[kind]
+            n = self.cfg.layers_of(kind)
+            stride = (lay.total + 4095) // 4096 * 4096
+            arena = HostArena(stride * n)
+            self.arenas[kind] = arena
+            ptrs = (C.c_void_p * n)()
+            for layer in range(n):
+                t = M.layer_tensors(self.cfg, kind, layer, self.seed, self.dev)
+                buf = M.pack_layer(self.cfg, kind, t)
+                arena.tensor[layer * stride:layer * stride + lay.total].copy_(buf)
+                ptrs[layer] = arena.ptr.value + layer * stride
+                if self.logical is not None:
+                    self.logical["layers"][(kind, layer)] = {k: v.float().cpu() for k, v in t.items()}
+                del t, buf
+            _native.check(self.lib.ls_exec_set_host_layers(self.handle, kind, ptrs, n), RuntimeError)
+        torch.cuda.synchronize()
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.ls_exec_destroy(self.handle)
+            self.handle = C.c_void_p()
+        for a in self.arenas.values():
+            a.close()
+        self.arenas = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ accessors --
+    @property
+    def module_names(self) -> list[str]:
+        return [M.MODULE_NAMES[k] for k in self.kinds]
+
+    def memory(self) -> dict:
+        out = (C.c_uint64 * 7)()
+        _native.check(self.lib.ls_exec_memory(self.handle, out), RuntimeError)
+        keys = ("cap", "used", "high_water", "slots", "always_resident", "overhead", "resident")
+        return {k: out[i] for i, k in enumerate(keys)}
+
+    def last_run_stats(self) -> dict:
+        out = (C.c_int64 * 3)()
+        _native.check(self.lib.ls_exec_stats(self.handle, out), RuntimeError)
+        return {"kernel_launches": out[0], "h2d_copies": out[1], "h2d_bytes": out[2]}
+
+    def streams(self) -> tuple[int, int]:
+        cs, ss = C.c_void_p(), C.c_void_p()
+        _native.check(self.lib.ls_exec_streams(self.handle, C.byref(cs), C.byref(ss)), RuntimeError)
+        return cs.value, ss.value
+
+    def layer_bytes(self, kind: int) -> int:
+        return self.layouts[kind].total
+
+    def set_placement(self, placement: Placement) -> None:
+        key = tuple(sorted((k, tuple(sorted(v))) for k, v in placement.resident.items()))
+        if key == self._placement_key:
+            return
+        total = sum(self.cfg.layers_of(k) for k in self.kinds)
+        mask = (C.c_uint8 * total)()
+        off = 0
+        names = set(self.module_names)
+        for name in placement.resident:
+            if name not in names:
+                raise ValueError(f"placement references unknown module '{name}'")
+        for kind in self.kinds:
+            n = self.cfg.layers_of(kind)
+            for i in placement.for_module(M.MODULE_NAMES[kind]):
+                if not 0 <= i < n:
+                    raise ValueError(f"placement for module '{M.MODULE_NAMES[kind]}' has "
+                                     f"out-of-range layer index {i} (valid 0..{n - 1})")
+                mask[off + i] = 1
+            off += n
+        _native.check(self.lib.ls_exec_set_placement(self.handle, mask, total))
+        self._placement_key = key
+
+    # -------------------------------------------------------------- running --
+    def _event_capacity(self) -> int:
+        return sum(2 * r * self.cfg.layers_of(k) for k in self.kinds for r in self.cfg.repetitions(k))
+
+    def _timeline(self, events, n: int, total_ms: float) -> Timeline:
+        names = self.module_names
+        phases = [M.PHASES[k] for k in self.kinds]
+        kinds = (EngineKind.COPY, EngineKind.EXECUTE)
+        evs = tuple(SimEvent(kinds[e.engine], names[e.module], phases[e.module][e.phase],
+                             e.invocation, e.layer, e.start_ms, e.end_ms) for e in events[:n])
+        return Timeline(events=evs, total_ms=total_ms)
+
+    def _run(self, io: RunIO, config: SimConfig, record_timeline: bool):
+        opts = RunOpts(_native.simcfg(config), 1 if record_timeline else 0)
+        cap = self._event_capacity() if record_timeline else 0
+        events = (_native.Event * max(cap, 1))() if record_timeline else None
+        n = C.c_int64()
+        total = C.c_double()
+        e2e = C.c_double()
+        _native.check(self.lib.ls_exec_run(self.handle, C.byref(io), C.byref(opts), events, cap,
+                                           C.byref(n), C.byref(total), C.byref(e2e)), RuntimeError)
+        tl = self._timeline(events, n.value, total.value) if record_timeline else None
+        return total.value, e2e.value, tl
+
+    def execute(self, placement: Placement, config: SimConfig = SimConfig(), inputs: dict | None = None,
+                *, record_timeline: bool = True, want_logits: bool = False) -> RunResult:
+        """One inference with device-resident inputs (the reference executor
+        contract: (model, placement, config) -> Timeline, plus outputs)."""
+        self.set_placement(placement)
+        cfg = self.cfg
+        inputs = inputs or M.synthetic_inputs(cfg, 0)
+        dev_in = {k: v.to(self.dev).contiguous() for k, v in inputs.items()}
+        tokens = torch.zeros(cfg.decode_steps + 1, dtype=torch.int32, device=self.dev)
+        actions = (torch.zeros(cfg.ex_tokens, cfg.action_dim, device=self.dev)
+                   if cfg.has_expert else None)
+        logits = (torch.zeros(cfg.decode_steps + 1, cfg.vocab, device=self.dev)
+                  if want_logits else None)
+        torch.cuda.synchronize(self.dev)
+        io = RunIO(0, 0, _ptr(dev_in.get("patches")), _ptr(dev_in["text_ids"]),
+                   _ptr(dev_in.get("noise")), tokens.data_ptr(), _ptr(actions), _ptr(logits))
+        total, e2e, tl = self._run(io, config, record_timeline)
+        return RunResult(tokens, actions, logits, total, e2e, tl)
+
+    def infer(self, host_inputs: dict, placement: Placement | None = None,
+              config: SimConfig = SimConfig()) -> RunResult:
+        """End-to-end call with pinned HOST buffers: input H2D and output D2H
+        are inside the measured region (e2e_ms)."""
+        if placement is not None:
+            self.set_placement(placement)
+        cfg = self.cfg
+        pin = {k: v.contiguous().pin_memory() for k, v in host_inputs.items()}
+        tokens = torch.zeros(cfg.decode_steps + 1, dtype=torch.int32).pin_memory()
+        actions = torch.zeros(cfg.ex_tokens, cfg.action_dim).pin_memory() if cfg.has_expert else None
+        io = RunIO(1, 0, _ptr(pin.get("patches")), _ptr(pin["text_ids"]), _ptr(pin.get("noise")),
+                   tokens.data_ptr(), _ptr(actions), None)
+        total, e2e, _ = self._run(io, config, False)
+        return RunResult(tokens, actions, None, total, e2e, None)
+
+    @staticmethod
+    def io_bytes(cfg: M.ModelConfig) -> tuple[int, int]:
+        """Host->device and device->host bytes of one `infer` call."""
+        h2d = 4 * (cfg.prompt_prefix + cfg.prompt_suffix)
+        if cfg.has_vit:
+            h2d += 2 * cfg.vit_images * cfg.vit_tokens_per_image * cfg.vit_patch_dim
+        if cfg.has_expert:
+            h2d += 4 * cfg.ex_tokens * cfg.action_dim
+        d2h = 4 * (cfg.decode_steps + 1) + (4 * cfg.ex_tokens * cfg.action_dim if cfg.has_expert else 0)
+        return h2d, d2h
+
+    # ------------------------------------------------------------- profiling --
+    def profile_run(self, iterations: int = 3, warmup: int = 1, calibrate: bool = True,
+                    config: SimConfig = SimConfig()) -> ModelProfile:
+        """Sequential Demand Layering with every layer streamed; per-layer DMA
+        and EXE averaged per (module, phase) -> reference-schema profile."""
+        seq = SimConfig(mode=Mode.SEQUENTIAL, slot_count=config.slot_count)
+        samples: dict[tuple[str, str, str], list[float]] = {}
+        for it in range(warmup + iterations):
+            res = self.execute(Placement.empty(), seq)
+            if it < warmup:
+                continue
+            for e in res.timeline.events:
+                samples.setdefault((e.module, e.phase, e.engine.value), []).append(e.end_ms - e.start_ms)
+        mem = self.memory()
+        modules = []
+        dma_bytes, dma_ms = 0.0, 0.0
+        for kind in self.kinds:
+            name = M.MODULE_NAMES[kind]
+            phases = []
+            for ph, reps in zip(M.PHASES[kind], self.cfg.repetitions(kind)):
+                dma = statistics.fmean(samples[(name, ph, "copy")])
+                exe = statistics.fmean(samples[(name, ph, "execute")])
+                phases.append(PhaseProfile(name=ph, repetitions=reps, dma_ms=dma, exe_ms=exe))
+                dma_bytes += self.layer_bytes(kind) * len(samples[(name, ph, "copy")])
+                dma_ms += sum(samples[(name, ph, "copy")])
+            modules.append(ModuleProfile(name=name, layers=self.cfg.layers_of(kind),
+                                         layer_mem_mb=M.layer_mem_mb(self.cfg, kind),
+                                         phases=tuple(phases)))
+        calibration = None
+        if calibrate:
+            runs = [self.execute(Placement.empty(), config, record_timeline=False).total_ms
+                    for _ in range(2)]
+            calibration = min(runs) / 1000.0
+        hw = HardwareProfile(name=f"b200-cap{int(self.vram_cap_mb)}", vram_mb=float(self.vram_cap_mb),
+                             h2d_gbps=dma_bytes / (dma_ms * 1e6),
+                             overhead_mb=mem["overhead"] / MIB)
+        return ModelProfile(hardware=hw, modules=tuple(modules),
+                            always_resident_mb=mem["always_resident"] / MIB,
+                            calibration_total_s=calibration)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _copy_to_device_ptr(dst: int, src: torch.Tensor) -> None:
+    """Synchronous copy of a device uint8 tensor into a raw device address."""
+    _native.check(_bind().ls_copy(dst, src.data_ptr(), src.numel()), RuntimeError)
