@@ -1,0 +1,44 @@
+"""__graft_entry__.smoke(): one tiny end-to-end Alpamayo-shaped inference on
+cuda:0 through the DFB executor, checked against the fp32 oracle and against
+itself with a different placement (streamed vs resident bit-exact)."""
+from __future__ import annotations
+
+
+def run_smoke() -> None:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("smoke() needs cuda:0")
+    import paper_2605_11678_b200 as ls
+    from oracle.model_fp32 import FP32Model
+    from paper_2605_11678_b200 import model as M
+    from paper_2605_11678_b200.engine import DemandLayeringEngine
+
+    cfg = M.TINY_ALPAMAYO
+    eng = DemandLayeringEngine(cfg, vram_cap_mb=1024, n_slots=2, keep_logical=True)
+    try:
+        inputs = M.synthetic_inputs(cfg, seed=0)
+        a = eng.execute(ls.Placement.empty(), inputs=inputs, want_logits=True)
+        b = eng.execute(ls.Placement.of({"vlm": [0, 2], "expert": [1]}), inputs=inputs,
+                        want_logits=True, record_timeline=False)
+        assert torch.equal(a.tokens, b.tokens) and torch.equal(a.logits, b.logits)
+        assert torch.equal(a.actions, b.actions)
+        ref = FP32Model(cfg, eng.logical)
+        _, logits, actions = ref.run({k: v.cpu() for k, v in inputs.items()},
+                                     teacher_tokens=a.tokens.cpu()[:-1])
+        err = (a.logits.cpu() - logits).abs().max().item()
+        assert err <= 2e-2 * logits.abs().max().item(), f"logits err {err}"
+        aerr = (a.actions.cpu() - actions).abs().max().item()
+        assert aerr <= 2e-2 * actions.abs().max().item() + 2e-2, f"actions err {aerr}"
+        n = len(a.timeline.events)
+        print(f"smoke ok: {n} timeline events, logits max-abs err {err:.3e}, "
+              f"actions err {aerr:.3e}, tokens {a.tokens.tolist()}")
+    finally:
+        eng.close()
+
+
+if __name__ == "__main__":
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    run_smoke()
