@@ -185,6 +185,10 @@ int ls_resolve_intercept(const ls_profile* p, double calibration_total_s,
 /* Alpamayo-R1-10B-shaped synthetic stack (shapes SURVEY 8d). */
 typedef struct ls_dims {
   int32_t has_vit, has_expert;
+  /* 1: the token-embedding table stays in page-locked host memory and the
+   * GPU gathers the rows it needs (zero-copy over PCIe) instead of holding
+   * vocab x d bf16 (1.2 GB) under the VRAM cap. */
+  int32_t embed_on_host, _pad0;
   /* ViT encoder + patch merger */
   int32_t vit_layers, vit_d, vit_heads, vit_hd, vit_ffn, vit_patch_dim, vit_images,
       vit_tokens_per_image;
@@ -221,6 +225,8 @@ int ls_exec_create(const ls_dims* d, int32_t device, uint64_t cap_bytes, int32_t
                    ls_exec** out);
 int ls_exec_destroy(ls_exec* e);
 int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr);
+/* Point an always-resident slot at page-locked host memory (embed_on_host). */
+int ls_exec_set_global_host(ls_exec* e, int32_t id, void* host_ptr);
 /* Pinned host buffers of every layer of one module (streamed source). */
 int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_ptrs, int32_t n);
 /* Upload resident layers for a placement mask (module order vit, lm, expert). */

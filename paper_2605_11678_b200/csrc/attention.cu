@@ -17,6 +17,8 @@ namespace lsb {
 template <int HD, int G>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a) {
   constexpr int E = HD / 32;  // elements per lane
+  pdl_trigger();
+  pdl_wait();
   const int kh = blockIdx.x, split = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunk = (a.n_ctx + a.n_split - 1) / a.n_split;
@@ -129,13 +131,12 @@ template <int HD>
 static cudaError_t decode_hd(const DecodeAttnArgs& a, cudaStream_t st) {
   dim3 grid(a.hkv, a.n_split);
   switch (a.hq / a.hkv) {
-    case 1: decode_attn_kernel<HD, 1><<<grid, 128, 0, st>>>(a); break;
-    case 2: decode_attn_kernel<HD, 2><<<grid, 128, 0, st>>>(a); break;
-    case 4: decode_attn_kernel<HD, 4><<<grid, 128, 0, st>>>(a); break;
-    case 8: decode_attn_kernel<HD, 8><<<grid, 128, 0, st>>>(a); break;
+    case 1: return launch_k(decode_attn_kernel<HD, 1>, grid, dim3(128), 0, st, a);
+    case 2: return launch_k(decode_attn_kernel<HD, 2>, grid, dim3(128), 0, st, a);
+    case 4: return launch_k(decode_attn_kernel<HD, 4>, grid, dim3(128), 0, st, a);
+    case 8: return launch_k(decode_attn_kernel<HD, 8>, grid, dim3(128), 0, st, a);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
@@ -181,6 +182,8 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   bf16* qs = reinterpret_cast<bf16*>(fsm);
   bf16* ks = qs + BM * LD;
   bf16* vs = ks + BN * LD;
+  pdl_trigger();
+  pdl_wait();
 
   const int h = blockIdx.y, kvh = h / (a.hq / a.hkv);
   const int q0 = blockIdx.x * BM;
@@ -342,8 +345,7 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq);
-  flash_kernel<HD><<<grid, 128, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(flash_kernel<HD>, grid, dim3(128), smem, st, a);
 }
 
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {

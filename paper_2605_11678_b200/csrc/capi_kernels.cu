@@ -9,7 +9,15 @@
 
 namespace lsb {
 int set_error(int code, const char* fmt, ...);
+
+static thread_local bool g_pdl_next = false;
+void set_launch_pdl(bool on) { g_pdl_next = on; }
+bool take_launch_pdl() {
+  const bool v = g_pdl_next;
+  g_pdl_next = false;
+  return v;
 }
+}  // namespace lsb
 using namespace lsb;
 
 static int cuda_rc(cudaError_t e, const char* what) {

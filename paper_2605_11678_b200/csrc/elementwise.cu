@@ -20,6 +20,8 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 
 // RMSNorm over rows of an fp32 [T x D] residual stream -> bf16 GEMM operand.
 __global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, int D, float eps) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sh[32];
   const float* xr = x + static_cast<long>(blockIdx.x) * D;
   float ss = 0.f;
@@ -32,12 +34,13 @@ __global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, in
 cudaError_t launch_rmsnorm_rows(const float* x, const bf16* w, bf16* out, int T, int D, float eps,
                                 cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  rmsnorm_rows_kernel<<<T, 256, 0, st>>>(x, w, out, D, eps);
-  return cudaGetLastError();
+  return launch_k(rmsnorm_rows_kernel, dim3(T), dim3(256), 0, st, x, w, out, D, eps);
 }
 
 __global__ void layernorm_rows_kernel(const float* x, const bf16* w, const bf16* b, bf16* out,
                                       int D, long ld_out, float eps) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sh[32];
   const float* xr = x + static_cast<long>(blockIdx.x) * D;
   float s = 0.f;
@@ -57,8 +60,7 @@ __global__ void layernorm_rows_kernel(const float* x, const bf16* w, const bf16*
 cudaError_t launch_layernorm_rows(const float* x, const bf16* w, const bf16* b, bf16* out, int T,
                                   int D, long ld_out, float eps, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  layernorm_rows_kernel<<<T, 256, 0, st>>>(x, w, b, out, D, ld_out, eps);
-  return cudaGetLastError();
+  return launch_k(layernorm_rows_kernel, dim3(T), dim3(256), 0, st, x, w, b, out, D, ld_out, eps);
 }
 
 // Prefill q/k RMSNorm + RoPE; K,V appended to the cache at positions pos0+t.
@@ -67,6 +69,8 @@ __global__ void qk_norm_rope_kernel(const bf16* qkv, int hq, int hkv, int hd, co
                                     const bf16* kn_w, float eps, const float2* rope, int pos0,
                                     bf16* q_out, bf16* k_cache, bf16* v_cache,
                                     int cache_head_stride) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nh = hq + 2 * hkv;
@@ -111,12 +115,13 @@ cudaError_t launch_qk_norm_rope(const bf16* qkv, int T, int hq, int hkv, int hd,
                                 bf16* q_out, bf16* k_cache, bf16* v_cache, int cache_head_stride,
                                 cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  qk_norm_rope_kernel<<<T, 256, 0, st>>>(qkv, hq, hkv, hd, qn_w, kn_w, eps, rope, pos0, q_out,
+  return launch_k(qk_norm_rope_kernel, dim3(T), dim3(256), 0, st, qkv, hq, hkv, hd, qn_w, kn_w, eps, rope, pos0, q_out,
                                          k_cache, v_cache, cache_head_stride);
-  return cudaGetLastError();
 }
 
 __global__ void embed_rows_kernel(const bf16* table, const int* ids, int D, float* out, long ld) {
+  pdl_trigger();
+  pdl_wait();
   const int id = ids[blockIdx.x];
   const bf16* src = table + static_cast<long>(id) * D;
   float* dst = out + static_cast<long>(blockIdx.x) * ld;
@@ -126,12 +131,13 @@ __global__ void embed_rows_kernel(const bf16* table, const int* ids, int D, floa
 cudaError_t launch_embed_rows(const bf16* table, const int* ids, int n, int D, float* out,
                               long ld_out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  embed_rows_kernel<<<n, 256, 0, st>>>(table, ids, D, out, ld_out);
-  return cudaGetLastError();
+  return launch_k(embed_rows_kernel, dim3(n), dim3(256), 0, st, table, ids, D, out, ld_out);
 }
 
 // x[t, :] += add[t % period, :]   (learned ViT position embedding per image)
 __global__ void add_rows_kernel(float* x, const bf16* add, int D, int period) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const bf16* a = add + static_cast<long>(t % period) * D;
   float* xr = x + static_cast<long>(t) * D;
@@ -141,11 +147,12 @@ __global__ void add_rows_kernel(float* x, const bf16* add, int D, int period) {
 cudaError_t launch_add_rows_bf16(float* x, const bf16* add, int T, int D, long period,
                                  cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  add_rows_kernel<<<T, 256, 0, st>>>(x, add, D, static_cast<int>(period));
-  return cudaGetLastError();
+  return launch_k(add_rows_kernel, dim3(T), dim3(256), 0, st, x, add, D, static_cast<int>(period));
 }
 
 __global__ void cast_kernel(const float* x, bf16* out, long n) {
+  pdl_trigger();
+  pdl_wait();
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x)
     out[i] = f2bf(x[i]);
@@ -153,13 +160,14 @@ __global__ void cast_kernel(const float* x, bf16* out, long n) {
 
 cudaError_t launch_cast_f32_bf16(const float* x, bf16* out, long n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  cast_kernel<<<296, 256, 0, st>>>(x, out, n);
-  return cudaGetLastError();
+  return launch_k(cast_kernel, dim3(296), dim3(256), 0, st, x, out, n);
 }
 
 // Greedy decode bookkeeping: key -> token id (+ history), re-arm the key.
 __global__ void argmax_to_token_kernel(const unsigned long long* key, int* token_out, int* history,
                                        int step, unsigned long long* key_reset) {
+  pdl_trigger();
+  pdl_wait();
   const unsigned long long k = *key;
   const int idx = static_cast<int>(0xffffffffu - static_cast<uint32_t>(k & 0xffffffffull));
   *token_out = idx;
@@ -169,21 +177,23 @@ __global__ void argmax_to_token_kernel(const unsigned long long* key, int* token
 
 cudaError_t launch_argmax_to_token(const unsigned long long* key, int* token_out, int* history,
                                    int step, unsigned long long* key_reset, cudaStream_t st) {
-  argmax_to_token_kernel<<<1, 1, 0, st>>>(key, token_out, history, step, key_reset);
-  return cudaGetLastError();
+  return launch_k(argmax_to_token_kernel, dim3(1), dim3(1), 0, st, key, token_out, history, step, key_reset);
 }
 
 __global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v, int n) {
+  pdl_trigger();
+  pdl_wait();
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
 }
 
 cudaError_t launch_fill_u64(unsigned long long* p, unsigned long long v, int n, cudaStream_t st) {
-  fill_u64_kernel<<<1, 128, 0, st>>>(p, v, n);
-  return cudaGetLastError();
+  return launch_k(fill_u64_kernel, dim3(1), dim3(128), 0, st, p, v, n);
 }
 
 // Sinusoidal flow-time features: out[i] = sin(t * f_i) | cos(t * f_i), f_i = 1e4^(-i/(dim/2)).
 __global__ void time_embed_kernel(const float* t_table, int step, int dim, float* out) {
+  pdl_trigger();
+  pdl_wait();
   const float t = t_table[step];
   const int half = dim / 2;
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
@@ -194,13 +204,14 @@ __global__ void time_embed_kernel(const float* t_table, int step, int dim, float
 }
 
 cudaError_t launch_time_embed(const float* t_table, int step, int dim, float* out, cudaStream_t st) {
-  time_embed_kernel<<<1, 128, 0, st>>>(t_table, step, dim, out);
-  return cudaGetLastError();
+  return launch_k(time_embed_kernel, dim3(1), dim3(128), 0, st, t_table, step, dim, out);
 }
 
 // Action-token input: h[i, :] = W_in . a_i + b_in + temb   (K = action dim, tiny).
 __global__ void action_in_kernel(const float* actions, const bf16* w_in, const bf16* b_in,
                                  const float* temb, int a_dim, int D, float* out) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     float s = bf2f(b_in[d]) + temb[d];
@@ -212,14 +223,15 @@ __global__ void action_in_kernel(const float* actions, const bf16* w_in, const b
 cudaError_t launch_action_in(const float* actions, const bf16* w_in, const bf16* b_in,
                              const float* temb, int n_tok, int a_dim, int D, float* out,
                              cudaStream_t st) {
-  action_in_kernel<<<n_tok, 256, 0, st>>>(actions, w_in, b_in, temb, a_dim, D, out);
-  return cudaGetLastError();
+  return launch_k(action_in_kernel, dim3(n_tok), dim3(256), 0, st, actions, w_in, b_in, temb, a_dim, D, out);
 }
 
 // Final RMSNorm + velocity head (D -> a_dim) + explicit Euler step a += dt * v.
 __global__ void action_out_euler_kernel(const float* h, const bf16* norm_w, float eps,
                                         const bf16* w_out, const bf16* b_out, int D, int a_dim,
                                         float dt, float* actions, float* velocity) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sh[32];
   __shared__ float part[8][8];
   const int i = blockIdx.x;
@@ -250,20 +262,20 @@ cudaError_t launch_action_out_euler(const float* h, const bf16* norm_w, float ep
                                     int a_dim, float dt, float* actions, float* velocity,
                                     cudaStream_t st) {
   if (a_dim > 8) return cudaErrorInvalidValue;
-  action_out_euler_kernel<<<n_tok, 256, 0, st>>>(h, norm_w, eps, w_out, b_out, D, a_dim, dt,
+  return launch_k(action_out_euler_kernel, dim3(n_tok), dim3(256), 0, st, h, norm_w, eps, w_out, b_out, D, a_dim, dt,
                                                  actions, velocity);
-  return cudaGetLastError();
 }
 
 // SiLU in place (time-MLP hidden).
 __global__ void silu_kernel(float* x, int n) {
+  pdl_trigger();
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     x[i] = silu(x[i]);
 }
 
 cudaError_t launch_silu_inplace(float* x, int n, cudaStream_t st) {
-  silu_kernel<<<(n + 255) / 256, 256, 0, st>>>(x, n);
-  return cudaGetLastError();
+  return launch_k(silu_kernel, dim3((n + 255) / 256), dim3(256), 0, st, x, n);
 }
 
 }  // namespace lsb

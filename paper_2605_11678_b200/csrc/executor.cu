@@ -41,10 +41,19 @@ using namespace lsb;
   } while (0)
 
 // Launch a kernel and count it (gpu_launches evidence for the bench).
-#define KL(x)        \
-  do {               \
-    CK(x);           \
-    ++e->launches;   \
+// PDL only between two kernels: any event record/wait or memcpy on the
+// compute stream clears pdl_ok, so the next kernel launches fully serialised.
+#define KL(x)                                     \
+  do {                                            \
+    set_launch_pdl(e->use_pdl && e->pdl_ok);      \
+    CK(x);                                        \
+    e->pdl_ok = true;                             \
+    ++e->launches;                                \
+  } while (0)
+#define SSOP(x)            \
+  do {                     \
+    CK(x);                 \
+    e->pdl_ok = false;     \
   } while (0)
 
 namespace {
@@ -104,7 +113,7 @@ uint64_t global_bytes(const ls_dims& d, int id) {
   const bool v = d.has_vit, x = d.has_expert;
   const uint64_t vd = d.vit_d, md = 4ull * d.vit_d;
   switch (id) {
-    case 0: return 2ull * d.vocab * d.lm_d;                        // embed (row-major)
+    case 0: return d.embed_on_host ? 0 : 2ull * d.vocab * d.lm_d;  // embed (row-major)
     case 1: return tiled_bytes(d.vocab, d.lm_d);                  // lm_head
     case 2: return 2ull * d.lm_d;                                 // final norm
     case 3: return 8ull * rope_rows(d) * (d.lm_hd / 2);           // rope (cos, sin)
@@ -188,6 +197,7 @@ struct ls_exec {
   CUtensorMap m_patches, m_vit_ln, m_vit_attn, m_vit_fc1, m_merge_in, m_merger_mid, m_lm_norm,
       m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
   GemvPlan gp_qkv{}, gp_o{}, gp_gu{}, gp_down{}, gp_head{}, gp_t1{}, gp_t2{};
+  bool use_pdl = true, pdl_ok = false;
   int64_t launches = 0, h2d_copies = 0;
   uint64_t h2d_bytes = 0;
 
@@ -443,7 +453,7 @@ int pre_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* io
     }
   } else {
     if (inv == 0)
-      CK(cudaMemcpyAsync(e->actions, e->noise, 4ull * d.ex_tokens * d.action_dim,
+      SSOP(cudaMemcpyAsync(e->actions, e->noise, 4ull * d.ex_tokens * d.action_dim,
                          cudaMemcpyDeviceToDevice, e->ss));
     KL(launch_time_embed((const float*)e->g[22], inv, d.time_dim, e->temb_in, e->ss));
     RC(gemv(e, GEMV_F32, e->gp_t1, e->g[13], e->temb_in, e->temb_mid, nullptr, (const float*)e->g[14]));
@@ -471,7 +481,7 @@ int post_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* i
     RC(gemv(e, GEMV_ARGMAX, e->gp_head, e->g[1], x, e->logits, e->g[2]));
     KL(launch_argmax_to_token(e->amax, e->token, e->hist, step, e->amax, e->ss));
     if (io->logits_out)
-      CK(cudaMemcpyAsync(io->logits_out + static_cast<long>(step) * d.vocab, e->logits,
+      SSOP(cudaMemcpyAsync(io->logits_out + static_cast<long>(step) * d.vocab, e->logits,
                          4ull * d.vocab, cudaMemcpyDeviceToDevice, e->ss));
   } else {
     KL(launch_action_out_euler(e->ex_h, (const bf16*)e->g[21], d.lm_eps, (const bf16*)e->g[19],
@@ -703,6 +713,17 @@ int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr) {
   return LS_OK;
 }
 
+int ls_exec_set_global_host(ls_exec* e, int32_t id, void* host_ptr) {
+  if (id != 0 || !e->d.embed_on_host)
+    return set_error(LS_ERR_VALUE, "only the embedding table (id 0) may live on the host");
+  cudaPointerAttributes attr;
+  CK(cudaPointerGetAttributes(&attr, host_ptr));
+  if (attr.type != cudaMemoryTypeHost)
+    return set_error(LS_ERR_VALUE, "embedding table must be page-locked host memory");
+  e->g[0] = static_cast<char*>(attr.devicePointer ? attr.devicePointer : host_ptr);
+  return LS_OK;
+}
+
 int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_ptrs, int32_t n) {
   for (auto& m : e->mods) {
     if (m.kind != kind) continue;
@@ -797,6 +818,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   int next_ev = 0;
   auto tick = [&](cudaStream_t s) {
     cudaEventRecord(e->tev[next_ev], s);
+    if (s == e->ss) e->pdl_ok = false;
     return next_ev++;
   };
 
@@ -812,6 +834,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   if (d.has_expert && io->noise)
     CK(cudaMemcpyAsync(e->noise, io->noise, 4ull * e->Te * d.action_dim, kin, e->ss));
   CK(cudaEventRecord(e->ev_t0, e->ss));
+  e->pdl_ok = false;
   CK(cudaStreamWaitEvent(e->cs, e->ev_t0, 0));
 
   std::vector<bool> slot_used(static_cast<size_t>(nsl), false);
@@ -839,24 +862,24 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             e->h2d_bytes += m.lay.total;
             if (timing) dma1 = tick(e->cs);
             CK(cudaEventRecord(e->dma_done[slot], e->cs));
-            CK(cudaStreamWaitEvent(e->ss, e->dma_done[slot], 0));
+            SSOP(cudaStreamWaitEvent(e->ss, e->dma_done[slot], 0));
             w = e->slots[slot];
           }
           int x0 = timing ? tick(e->ss) : -1;
           RC(run_layer(e, m, ph, inv, l, w));
           int x1 = timing ? tick(e->ss) : -1;
           if (slot >= 0) {
-            CK(cudaEventRecord(e->comp_done[slot], e->ss));
+            SSOP(cudaEventRecord(e->comp_done[slot], e->ss));
             slot_used[slot] = true;
           }
-          if (seq) CK(cudaEventRecord(e->exe_done, e->ss));
+          if (seq) SSOP(cudaEventRecord(e->exe_done, e->ss));
           if (timing) {
             if (slot >= 0) recs.push_back({0, mi, ph, inv, l, dma0, dma1});
             recs.push_back({1, mi, ph, inv, l, x0, x1});
           }
         }
         if (barrier) {
-          CK(cudaEventRecord(e->inv_done, e->ss));
+          SSOP(cudaEventRecord(e->inv_done, e->ss));
           pending_barrier = true;
         }
         RC(post_invocation(e, m.kind, ph, inv, io));

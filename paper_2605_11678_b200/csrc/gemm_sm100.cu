@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* accf = empty + Cfg::kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 2);
 
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = blockIdx.x, n0 = blockIdx.y * BN;
   const int n_kb = a.n_kb;
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
+      pdl_wait();  // activations of the previous kernel
       const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kTileBytes;
       for (int kb = 0; kb < n_kb; ++kb) {
         const int s = kb % Cfg::kStages;
@@ -165,8 +167,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
     attr = true;
   }
   dim3 grid(a.n_mt, (a.T + BN - 1) / BN);
-  gemm_kernel<BN, EPI><<<grid, 192, Cfg::kSmem, st>>>(map, a);
-  return cudaGetLastError();
+  return launch_k(gemm_kernel<BN, EPI>, grid, dim3(192), Cfg::kSmem, st, map, a);
 }
 
 template <int BN>

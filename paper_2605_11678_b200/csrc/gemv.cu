@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   uint64_t* empty = full + kGemvStages;
   int* flag = reinterpret_cast<int*>(empty + kGemvStages);
 
+  pdl_trigger();
   const int G = gridDim.x, c = blockIdx.x;
   const long T = static_cast<long>(a.n_mt) * a.n_kb;
   const long t0 = c * T / G, t1 = (c + 1) * T / G;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   }
 
   // ---- consumers: x -> shared (fp32), optional fused RMSNorm ----
+  pdl_wait();  // x, workspace and outputs belong to the previous kernel until here
   const int tid = threadIdx.x;
   float ss = 0.f;
   for (int k = tid; k < K; k += kGemvConsumers) {
@@ -271,8 +273,7 @@ static cudaError_t launch_t(const GemvArgs& a, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  gemv_kernel<EPI><<<grid, kGemvThreads, gemv_smem(a.n_kb), st>>>(a);
-  return cudaGetLastError();
+  return launch_k(gemv_kernel<EPI>, dim3(grid), dim3(kGemvThreads), gemv_smem(a.n_kb), st, a);
 }
 
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st) {

@@ -11,6 +11,9 @@ namespace lsb {
 
 typedef __nv_bfloat16 bf16;
 
+// Programmatic dependent launch for the NEXT launch_* call on this thread.
+void set_launch_pdl(bool on);
+
 // ---------------- decode GEMV (batch 1) over tiled weights --------------------
 enum GemvEpi : int {
   GEMV_F32 = 0,     // out[row] = y

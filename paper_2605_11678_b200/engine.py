@@ -47,6 +47,7 @@ def _bind():
         "ls_exec_create": [C.POINTER(M.Dims), C.c_int32, C.c_uint64, C.c_int32, C.POINTER(vp)],
         "ls_exec_destroy": [vp],
         "ls_exec_global_ptr": [vp, C.c_int32, C.POINTER(vp)],
+        "ls_exec_set_global_host": [vp, C.c_int32, vp],
         "ls_exec_set_host_layers": [vp, C.c_int32, C.POINTER(vp), C.c_int32],
         "ls_exec_set_placement": [vp, C.POINTER(C.c_uint8), C.c_int64],
         "ls_exec_memory": [vp, C.POINTER(C.c_uint64)],
@@ -119,7 +120,7 @@ class DemandLayeringEngine:
         self.kinds = cfg.kinds
         self.layouts = {k: M.layer_layout(cfg, k) for k in self.kinds}
         self.logical: dict | None = {"layers": {}, "globals": {}} if keep_logical else None
-        self.arenas: dict[int, HostArena] = {}
+        self.arenas: dict = {}
         self._placement_key = None
         self._init_globals()
         self._init_layers()
@@ -134,9 +135,16 @@ class DemandLayeringEngine:
         tensors = M.global_tensors(self.cfg, self.seed, self.dev)
         for gid, t in tensors.items():
             raw = M.global_bytes_of(gid, t)
-            size = M.global_size(self.cfg, gid)
-            assert raw.numel() == size, (gid, raw.numel(), size)
-            _copy_to_device_ptr(self._global_ptr(gid), raw)
+            if gid == M.G_EMBED and self.cfg.embed_on_host:
+                arena = HostArena(raw.numel())
+                arena.tensor.copy_(raw)
+                self.arenas["embed"] = arena
+                _native.check(self.lib.ls_exec_set_global_host(self.handle, gid, arena.ptr),
+                              RuntimeError)
+            else:
+                size = M.global_size(self.cfg, gid)
+                assert raw.numel() == size, (gid, raw.numel(), size)
+                _copy_to_device_ptr(self._global_ptr(gid), raw)
             if self.logical is not None:
                 self.logical["globals"][gid] = t.float().cpu()
         torch.cuda.synchronize()

@@ -30,7 +30,7 @@ PHASES = {KIND_VIT: ("encode",), KIND_LM: ("prefill", "decode"), KIND_EXPERT: ("
 
 class Dims(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
-        "has_vit", "has_expert",
+        "has_vit", "has_expert", "embed_on_host", "_pad0",
         "vit_layers", "vit_d", "vit_heads", "vit_hd", "vit_ffn", "vit_patch_dim", "vit_images",
         "vit_tokens_per_image",
         "lm_layers", "lm_d", "lm_hq", "lm_hkv", "lm_hd", "lm_ffn", "vocab", "prompt_prefix",
@@ -51,6 +51,7 @@ class ModelConfig:
     name: str = "alpamayo-r1-10b-shape"
     has_vit: bool = True
     has_expert: bool = True
+    embed_on_host: bool = True         # token-embedding table gathered from pinned host memory
     vit_layers: int = 27
     vit_d: int = 1152
     vit_heads: int = 16
@@ -88,7 +89,8 @@ class ModelConfig:
         vals.pop("name")
         vals["has_vit"] = int(self.has_vit)
         vals["has_expert"] = int(self.has_expert)
-        return Dims(**vals, _pad=0.0)
+        vals["embed_on_host"] = int(self.embed_on_host)
+        return Dims(**vals, _pad=0.0, _pad0=0)
 
     @property
     def vis_tokens(self) -> int:

@@ -11,7 +11,7 @@ echo "launches per inference: $N"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -s $N -c $N --csv \
     --log-file $OUT/launches.csv python tools/profile_step.py --runs 2 > $OUT/launches.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:gemv_kernel<2>' -s 40 -c 2 -o $OUT/gemv_silu python tools/profile_step.py --runs 1 > $OUT/full_gemv.log 2>&1
+    -k 'regex:gemv_kernel<.int.2>' -s 40 -c 2 -o $OUT/gemv_silu python tools/profile_step.py --runs 1 > $OUT/full_gemv.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:gemm_kernel<128, 0>' -s 4 -c 2 -o $OUT/gemm_qkv python tools/profile_step.py --runs 1 > $OUT/full_gemm.log 2>&1
+    -k 'regex:gemm_kernel<.int.128, .int.0>' -s 4 -c 2 -o $OUT/gemm_qkv python tools/profile_step.py --runs 1 > $OUT/full_gemm.log 2>&1
 ls -la $OUT
