@@ -281,7 +281,7 @@ def main():
     pred = None
     if not args.no_sweep:
         vlm = prof.module("vlm")
-        kmax = plan.resident_count_per_module.get("vlm", 0)
+        kmax = min(plan.resident_count_per_module.get("vlm", 0), vlm.layers - 1)
         ks = sorted({0, kmax // 4, kmax // 2, (3 * kmax) // 4, kmax})
         measured = [(0, prof.calibration_total_s)]
         for k in ks[1:]:
