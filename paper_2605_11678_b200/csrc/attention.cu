@@ -41,25 +41,38 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
   }
   const bf16* kb = a.k_cache + static_cast<long>(kh) * a.cache_head_stride;
   const bf16* vb = a.v_cache + static_cast<long>(kh) * a.cache_head_stride;
-  for (int p = p0 + warp; p < p1; p += 4) {
-    float kv[E], vv[E];
+  // Each warp owns up to kPPW positions per round; all their K/V loads are
+  // issued before the first use so the memory latency is paid once.
+  constexpr int kPPW = 4;
+  for (int base = p0; base < p1; base += 4 * kPPW) {
+    bf16 kr[kPPW][E], vr[kPPW][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      kv[e] = bf2f(kb[static_cast<long>(p) * HD + lane * E + e]);
-      vv[e] = bf2f(vb[static_cast<long>(p) * HD + lane * E + e]);
+    for (int j = 0; j < kPPW; ++j) {
+      const int p = base + warp + 4 * j;
+      if (p < p1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          kr[j][e] = kb[static_cast<long>(p) * HD + lane * E + e];
+          vr[j][e] = vb[static_cast<long>(p) * HD + lane * E + e];
+        }
+      }
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float s = 0.f;
+    for (int j = 0; j < kPPW; ++j) {
+      if (base + warp + 4 * j >= p1) break;
 #pragma unroll
-      for (int e = 0; e < E; ++e) s = fmaf(qv[g][e], kv[e], s);
-      s = warp_sum(s);
-      const float mn = fmaxf(m[g], s);
-      const float corr = exp2f(m[g] - mn), pe = exp2f(s - mn);
-      l[g] = l[g] * corr + pe;
+      for (int g = 0; g < G; ++g) {
+        float s = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc[g][e] = acc[g][e] * corr + pe * vv[e];
-      m[g] = mn;
+        for (int e = 0; e < E; ++e) s = fmaf(qv[g][e], bf2f(kr[j][e]), s);
+        s = warp_sum(s);
+        const float mn = fmaxf(m[g], s);
+        const float corr = exp2f(m[g] - mn), pe = exp2f(s - mn);
+        l[g] = l[g] * corr + pe;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[g][e] = acc[g][e] * corr + pe * bf2f(vr[j][e]);
+        m[g] = mn;
+      }
     }
   }
   // combine the 4 warps of this CTA

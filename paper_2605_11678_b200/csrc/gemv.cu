@@ -20,7 +20,14 @@
 
 namespace lsb {
 
-constexpr int kGemvStages = 8;
+constexpr int kGemvMaxStages = 12;
+
+// Ring depth from the shared-memory left after x (fp32, K floats): 12 stages
+// (192 KiB in flight per SM) for K = 4096, 11 for K = 12288.
+__host__ __device__ inline int gemv_stages(int n_kb) {
+  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 1024) / kTileBytes;
+  return avail > kGemvMaxStages ? kGemvMaxStages : avail;
+}
 constexpr int kGemvConsumers = 256;  // 8 warps
 constexpr int kGemvThreads = kGemvConsumers + 32;
 
@@ -110,12 +117,13 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int K = a.n_kb * kTileCols;
   uint8_t* stages = smem;
-  float* xs = reinterpret_cast<float*>(smem + kGemvStages * kTileBytes);
+  const int NS = gemv_stages(a.n_kb);
+  float* xs = reinterpret_cast<float*>(smem + NS * kTileBytes);
   float* red = xs + K;
   float* scratch = red + kTileRows;  // 8 floats for block reductions
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
-  uint64_t* empty = full + kGemvStages;
-  int* flag = reinterpret_cast<int*>(empty + kGemvStages);
+  uint64_t* empty = full + kGemvMaxStages;
+  int* flag = reinterpret_cast<int*>(empty + kGemvMaxStages);
 
   pdl_trigger();
   const int G = gridDim.x, c = blockIdx.x;
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kGemvStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGemvConsumers / 32);
     }
@@ -137,8 +145,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       const uint64_t pol = policy_evict_first();
       for (long t = t0; t < t1; ++t) {
         const long i = t - t0;
-        const int s = static_cast<int>(i % kGemvStages);
-        if (i >= kGemvStages) mbar_wait(&empty[s], static_cast<uint32_t>(((i / kGemvStages) - 1) & 1));
+        const int s = static_cast<int>(i % NS);
+        if (i >= NS) mbar_wait(&empty[s], static_cast<uint32_t>(((i / NS) - 1) & 1));
         mbar_arrive_expect_tx(&full[s], kTileBytes);
         bulk_g2s_evict_first(stages + s * kTileBytes, a.w + t * kTileBytes, kTileBytes, &full[s], pol);
       }
@@ -223,8 +231,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       cur_mt = mt;
     }
     const long i = t - t0;
-    const int s = static_cast<int>(i % kGemvStages);
-    mbar_wait(&full[s], static_cast<uint32_t>((i / kGemvStages) & 1));
+    const int s = static_cast<int>(i % NS);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / NS) & 1));
     const uint8_t* st = stages + s * kTileBytes;
     const float* xk = xs + kb * kTileCols;
     const float4* xa = reinterpret_cast<const float4*>(xk + ((ch ^ rr) << 3));
@@ -260,8 +268,8 @@ int gemv_max_contrib(int n_mt, int n_kb, int grid) {
 }
 
 static size_t gemv_smem(int n_kb) {
-  return static_cast<size_t>(kGemvStages) * kTileBytes + static_cast<size_t>(n_kb) * kTileCols * 4 +
-         kTileRows * 4 + 16 * 4 + 2 * kGemvStages * 8 + 16;
+  return static_cast<size_t>(gemv_stages(n_kb)) * kTileBytes + static_cast<size_t>(n_kb) * kTileCols * 4 +
+         kTileRows * 4 + 16 * 4 + 2 * kGemvMaxStages * 8 + 16;
 }
 
 template <int EPI>

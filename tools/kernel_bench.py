@@ -1,0 +1,103 @@
+"""Kernel microbenchmarks at the Alpamayo decode / prefill shapes (CUDA events,
+weights rotated through copies larger than L2).  Used for ncu captures:
+
+    ncu --set full -k regex:gemv_kernel -s 10 -c 1 python tools/kernel_bench.py --only gemv
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+from paper_2605_11678_b200 import kernels as K  # noqa: E402
+
+
+def timed(fn, reps=20, warm=5):
+    s = torch.cuda.current_stream()
+    for _ in range(warm):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def bench_gemv(n, k, epi=K.GEMV_F32, copies=3):
+    dev = "cuda"
+    ws_ = [K.pack_tiled((torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)) for _ in range(copies)]
+    x = torch.randn(k, device=dev)
+    nw = torch.ones(k, dtype=torch.bfloat16, device=dev)
+    out = torch.zeros(n, device=dev)
+    ws = K.GemvWorkspace(dev)
+    it = [0]
+
+    def run():
+        w = ws_[it[0] % copies]
+        it[0] += 1
+        K.gemv(epi, w, n, k, x, out, ws, norm_w=nw, n_valid=n // 2 if epi == K.GEMV_SILU else n)
+    ms = timed(run)
+    b = n * k * 2 + k * 6 + n * 4
+    return {"kernel": f"gemv epi={epi} {n}x{k}", "us": ms * 1e3, "GBps": b / (ms * 1e6)}
+
+
+def bench_gemm(T, n, k, epi=K.GEMM_BF16):
+    dev = "cuda"
+    w = K.pack_tiled((torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16))
+    x = torch.randn(T, k, device=dev).to(torch.bfloat16)
+    ncol = n // 2 if epi == K.GEMM_SILU_BF16 else n
+    out = torch.zeros(T, ncol, dtype=torch.bfloat16 if epi != K.GEMM_RESID_F32 else torch.float32,
+                      device=dev)
+    ms = timed(lambda: K.gemm(epi, w, n, k, x, out, n_valid=ncol))
+    f = 2.0 * T * n * k
+    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}", "us": ms * 1e3, "TFLOPs": f / (ms * 1e9)}
+
+
+def bench_decode_attn(ctx=1045, hq=32, hkv=8, hd=128, n_split=18):
+    dev = "cuda"
+    max_ctx = 1100
+    q = torch.randn(hq * hd, device=dev)
+    kc = torch.randn(hkv, max_ctx, hd, device=dev).to(torch.bfloat16)
+    vc = torch.randn(hkv, max_ctx, hd, device=dev).to(torch.bfloat16)
+    out = torch.empty(hq * hd, device=dev)
+    ws = torch.empty(hq * 256 * (hd + 2), device=dev)
+    cnt = torch.zeros(hkv, dtype=torch.int32, device=dev)
+    ms = timed(lambda: K.decode_attention(q, kc, vc, ctx, out, hq, hkv, hd, 1 / math.sqrt(hd), ws,
+                                          cnt, n_split))
+    b = 2 * hkv * ctx * hd * 2
+    return {"kernel": f"decode_attn ctx={ctx} split={n_split}", "us": ms * 1e3, "GBps": b / (ms * 1e6)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="all")
+    args = ap.parse_args()
+    res = []
+    if args.only in ("all", "gemv"):
+        res.append(bench_gemv(24576, 4096, K.GEMV_SILU))
+        res.append(bench_gemv(4096, 12288, K.GEMV_RESID))
+        res.append(bench_gemv(6144, 4096, K.GEMV_F32))
+        res.append(bench_gemv(4096, 4096, K.GEMV_RESID))
+    if args.only in ("all", "attn"):
+        for s in (18, 66):
+            res.append(bench_decode_attn(n_split=s))
+    if args.only in ("all", "gemm"):
+        res.append(bench_gemm(1024, 6144, 4096))
+        res.append(bench_gemm(1024, 24576, 4096, K.GEMM_SILU_BF16))
+        res.append(bench_gemm(1024, 4096, 12288, K.GEMM_RESID_F32))
+        res.append(bench_gemm(64, 4096, 2048, K.GEMM_RESID_F32))
+        res.append(bench_gemm(3072, 3456, 1152))
+    for r in res:
+        print(json.dumps(r))
+
+
+if __name__ == "__main__":
+    main()
