@@ -7,30 +7,59 @@
 // flash_attention: many queries (LM prefill, ViT, action expert) with
 //   bf16 mma.sync m16n8k16 tiles, online softmax in fp32, causal /
 //   block-diagonal (per image) / two-segment KV (expert: VLM cache + own).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace lsb {
 
 // ------------------------------- decode ---------------------------------------
+//
+// grid (hkv, n_split), 128 threads.  Each CTA owns <= kDecChunk consecutive
+// positions of one KV head: its K and V rows are contiguous in the cache, so
+// two 1-D bulk copies (TMA engine) land them in shared memory with a single
+// mbarrier wait -- one memory latency per CTA instead of one per position.
+// The GQA group's G query heads stay in registers; per-CTA partials
+// (max, sum, O) are merged by the last CTA of the head in split order.
+
+constexpr int kDecChunk = 64;
 
 template <int HD, int G>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a) {
   constexpr int E = HD / 32;  // elements per lane
+  extern __shared__ __align__(16) uint8_t dsm[];
+  bf16* ks = reinterpret_cast<bf16*>(dsm);
+  bf16* vs = ks + kDecChunk * HD;
+  float* comb = reinterpret_cast<float*>(vs + kDecChunk * HD);  // combine scratch
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float sm_m[4][G], sm_l[4][G];
+  __shared__ int s_last;
   pdl_trigger();
-  pdl_wait();
   const int kh = blockIdx.x, split = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
   const int chunk = (a.n_ctx + a.n_split - 1) / a.n_split;
   const int p0 = split * chunk, p1 = min(a.n_ctx, p0 + chunk);
+  const int np = max(p1 - p0, 0);
+  if (threadIdx.x == 0 && np > 0) {
+    const uint32_t bytes = static_cast<uint32_t>(np * HD * 2);
+    mbar_arrive_expect_tx(&bar, 2 * bytes);
+    const long off = static_cast<long>(kh) * a.cache_head_stride + static_cast<long>(p0) * HD;
+    bulk_g2s(ks, a.k_cache + off, bytes, &bar);
+    bulk_g2s(vs, a.v_cache + off, bytes, &bar);
+  }
   const float sl2 = a.scale * 1.4426950408889634f;
-
   float qv[G][E];
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
     for (int e = 0; e < E; ++e) qv[g][e] = a.q[(kh * G + g) * HD + lane * E + e] * sl2;
-
   float m[G], l[G], acc[G][E];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -39,46 +68,30 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[g][e] = 0.f;
   }
-  const bf16* kb = a.k_cache + static_cast<long>(kh) * a.cache_head_stride;
-  const bf16* vb = a.v_cache + static_cast<long>(kh) * a.cache_head_stride;
-  // Each warp owns up to kPPW positions per round; all their K/V loads are
-  // issued before the first use so the memory latency is paid once.
-  constexpr int kPPW = 4;
-  for (int base = p0; base < p1; base += 4 * kPPW) {
-    bf16 kr[kPPW][E], vr[kPPW][E];
+  if (np > 0) mbar_wait(&bar, 0);
+  for (int j = warp; j < np; j += 4) {
+    float kv[E], vv[E];
 #pragma unroll
-    for (int j = 0; j < kPPW; ++j) {
-      const int p = base + warp + 4 * j;
-      if (p < p1) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          kr[j][e] = kb[static_cast<long>(p) * HD + lane * E + e];
-          vr[j][e] = vb[static_cast<long>(p) * HD + lane * E + e];
-        }
-      }
+    for (int e = 0; e < E; ++e) {
+      kv[e] = bf2f(ks[j * HD + lane * E + e]);
+      vv[e] = bf2f(vs[j * HD + lane * E + e]);
     }
 #pragma unroll
-    for (int j = 0; j < kPPW; ++j) {
-      if (base + warp + 4 * j >= p1) break;
+    for (int g = 0; g < G; ++g) {
+      float sc = 0.f;
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float s = 0.f;
+      for (int e = 0; e < E; ++e) sc = fmaf(qv[g][e], kv[e], sc);
+      sc = warp_sum(sc);
+      const float mn = fmaxf(m[g], sc);
+      const float corr = exp2f(m[g] - mn), pe = exp2f(sc - mn);
+      l[g] = l[g] * corr + pe;
 #pragma unroll
-        for (int e = 0; e < E; ++e) s = fmaf(qv[g][e], bf2f(kr[j][e]), s);
-        s = warp_sum(s);
-        const float mn = fmaxf(m[g], s);
-        const float corr = exp2f(m[g] - mn), pe = exp2f(s - mn);
-        l[g] = l[g] * corr + pe;
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc[g][e] = acc[g][e] * corr + pe * bf2f(vr[j][e]);
-        m[g] = mn;
-      }
+      for (int e = 0; e < E; ++e) acc[g][e] = acc[g][e] * corr + pe * vv[e];
+      m[g] = mn;
     }
   }
-  // combine the 4 warps of this CTA
-  __shared__ float sm_m[4][G], sm_l[4][G];
-  __shared__ float sm_o[4][G][HD];
-  __shared__ int s_last;
+  // ---- merge the 4 warps (shared memory) ----
+  float* sm_o = comb;  // [4][G][HD]
   if (lane == 0)
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -88,9 +101,8 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm_o[warp][g][lane * E + e] = acc[g][e];
+    for (int e = 0; e < E; ++e) sm_o[(warp * G + g) * HD + lane * E + e] = acc[g][e];
   __syncthreads();
-  // thread layout for the combine: idx over G*HD
   const int W = HD + 2;  // workspace record: M, L, O[HD]
   for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
     const int g = idx / HD, d = idx % HD;
@@ -101,7 +113,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
       for (int w = 0; w < 4; ++w) {
         const float f = exp2f(sm_m[w][g] - M);
         L += sm_l[w][g] * f;
-        O += sm_o[w][g][d] * f;
+        O += sm_o[(w * G + g) * HD + d] * f;
       }
     const int h = kh * G + g;
     if (a.n_split == 1) {
@@ -122,32 +134,56 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // ---- last CTA: coalesced load of all G*n_split records, then merge in split order ----
+  float* recs = comb;  // [G][n_split][W]  (fits: host caps n_split * G * W floats)
+  const float* base = a.ws + static_cast<long>(kh * G) * a.n_split * W;
+  const int total = G * a.n_split * W;
+  for (int i = threadIdx.x; i < total; i += 128) recs[i] = __ldcg(base + i);
+  __syncthreads();
   for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
     const int g = idx / HD, d = idx % HD, h = kh * G + g;
-    const float* rec = a.ws + static_cast<long>(h) * a.n_split * W;
+    const float* r = recs + g * a.n_split * W;
     float M = -INFINITY;
-    for (int s = 0; s < a.n_split; ++s) M = fmaxf(M, __ldcg(rec + s * W));
+    for (int sp = 0; sp < a.n_split; ++sp) M = fmaxf(M, r[sp * W]);
     float L = 0.f, O = 0.f;
-    for (int s = 0; s < a.n_split; ++s) {
-      const float ms = __ldcg(rec + s * W);
+    for (int sp = 0; sp < a.n_split; ++sp) {
+      const float ms = r[sp * W];
       if (ms == -INFINITY) continue;
       const float f = exp2f(ms - M);
-      L += __ldcg(rec + s * W + 1) * f;
-      O += __ldcg(rec + s * W + 2 + d) * f;
+      L += r[sp * W + 1] * f;
+      O += r[sp * W + 2 + d] * f;
     }
     a.out[h * HD + d] = O / L;
   }
   if (threadIdx.x == 0) a.counters[kh] = 0;
 }
 
+int decode_attn_splits(int n_ctx) { return (n_ctx + kDecChunk - 1) / kDecChunk; }
+
+template <int HD, int G>
+static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
+  const size_t kv = 2ull * kDecChunk * HD * 2;
+  const size_t comb = 4ull * std::max<size_t>(4ull * G * HD, static_cast<size_t>(G) * a.n_split * (HD + 2));
+  const size_t smem = kv + comb;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_k(decode_attn_kernel<HD, G>, dim3(a.hkv, a.n_split), dim3(128), smem, st, a);
+}
+
 template <int HD>
 static cudaError_t decode_hd(const DecodeAttnArgs& a, cudaStream_t st) {
-  dim3 grid(a.hkv, a.n_split);
+  if ((a.n_ctx + a.n_split - 1) / a.n_split > kDecChunk) return cudaErrorInvalidValue;
   switch (a.hq / a.hkv) {
-    case 1: return launch_k(decode_attn_kernel<HD, 1>, grid, dim3(128), 0, st, a);
-    case 2: return launch_k(decode_attn_kernel<HD, 2>, grid, dim3(128), 0, st, a);
-    case 4: return launch_k(decode_attn_kernel<HD, 4>, grid, dim3(128), 0, st, a);
-    case 8: return launch_k(decode_attn_kernel<HD, 8>, grid, dim3(128), 0, st, a);
+    case 1: return decode_launch<HD, 1>(a, st);
+    case 2: return decode_launch<HD, 2>(a, st);
+    case 4: return decode_launch<HD, 4>(a, st);
+    case 8: return decode_launch<HD, 8>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -386,7 +386,7 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.out = e->dec_attn;
   a.ws = e->attn_ws;
   a.counters = e->attn_cnt;
-  a.n_split = std::min(e->n_split, std::max(1, (pos + 1 + 15) / 16));  // <= 16 positions per CTA
+  a.n_split = decode_attn_splits(pos + 1);  // <= 64 positions per CTA
   KL(launch_decode_attention(a, e->ss));
   RC(gemv(e, GEMV_RESID, e->gp_o, part(1), e->dec_attn, e->dec_h, nullptr));
   RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn));
@@ -606,7 +606,7 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     OV(amax, 16);
     OV(token, 16);
     OV(hist, 4ull * (d.decode_steps + 1));
-    e->n_split = std::max(1, (e->ctx + 1 + 15) / 16);
+    e->n_split = decode_attn_splits(e->ctx + 1);
     OV(attn_ws, 4ull * d.lm_hq * e->n_split * (d.lm_hd + 2));
     OV(attn_cnt, 4ull * d.lm_hkv);
     e->gp_qkv = plan_gemv(QN, d.lm_d, e->nsm);

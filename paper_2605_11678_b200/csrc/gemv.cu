@@ -143,12 +143,19 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   if (warp == kGemvConsumers / 32) {  // ---- producer warp ----
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      for (long t = t0; t < t1; ++t) {
-        const long i = t - t0;
-        const int s = static_cast<int>(i % NS);
-        if (i >= NS) mbar_wait(&empty[s], static_cast<uint32_t>(((i / NS) - 1) & 1));
+      // stage / round counters advance incrementally: no 64-bit div or mod per tile
+      const uint8_t* src = a.w + t0 * kTileBytes;
+      int s = 0;
+      uint32_t round = 0;
+      for (int n = static_cast<int>(t1 - t0); n > 0; --n) {
+        if (round) mbar_wait(&empty[s], (round - 1) & 1);
         mbar_arrive_expect_tx(&full[s], kTileBytes);
-        bulk_g2s_evict_first(stages + s * kTileBytes, a.w + t * kTileBytes, kTileBytes, &full[s], pol);
+        bulk_g2s_evict_first(stages + s * kTileBytes, src, kTileBytes, &full[s], pol);
+        src += kTileBytes;
+        if (++s == NS) {
+          s = 0;
+          ++round;
+        }
       }
     }
     return;
@@ -223,16 +230,17 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     named_bar(1, kGemvConsumers);
   };
 
-  for (long t = t0; t < t1; ++t) {
-    const int mt = static_cast<int>(t / a.n_kb);
-    const int kb = static_cast<int>(t - static_cast<long>(mt) * a.n_kb);
-    if (mt != cur_mt) {
+  int kb = t0 < t1 ? static_cast<int>(t0 - static_cast<long>(cur_mt) * a.n_kb) : 0;
+  int s = 0;
+  uint32_t round = 0;
+  for (int n = static_cast<int>(t1 - t0), mt = cur_mt; n > 0; --n) {
+    if (kb == a.n_kb) {
+      kb = 0;
+      ++mt;
       flush(cur_mt);
       cur_mt = mt;
     }
-    const long i = t - t0;
-    const int s = static_cast<int>(i % NS);
-    mbar_wait(&full[s], static_cast<uint32_t>((i / NS) & 1));
+    mbar_wait(&full[s], round & 1);
     const uint8_t* st = stages + s * kTileBytes;
     const float* xk = xs + kb * kTileCols;
     const float4* xa = reinterpret_cast<const float4*>(xk + ((ch ^ rr) << 3));
@@ -246,6 +254,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    ++kb;
+    if (++s == NS) {
+      s = 0;
+      ++round;
+    }
   }
   if (cur_mt >= 0) flush(cur_mt);
 }

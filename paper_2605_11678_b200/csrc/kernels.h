@@ -92,6 +92,8 @@ struct DecodeAttnArgs {
   int n_split;
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
+// splits so every CTA covers <= 64 positions (the kernel requires it)
+int decode_attn_splits(int n_ctx);
 
 struct FlashArgs {
   const bf16* q;  long q_tok_stride, q_head_stride;   // q[t, h, d]
