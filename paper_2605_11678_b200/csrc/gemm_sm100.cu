@@ -50,7 +50,9 @@ __global__ void __launch_bounds__(192, 1)
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x, n0 = blockIdx.y * BN;
+  // token tiles vary fastest: the CTAs sharing one weight m-tile are co-resident,
+  // so each weight byte comes from HBM once and from L2 for the other token tiles
+  const int mt = blockIdx.y, n0 = blockIdx.x * BN;
   const int n_kb = a.n_kb;
 
   if (threadIdx.x == 0) {
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-int gemm_block_n(int T) { return T <= 64 ? 64 : 128; }
+int gemm_block_n(int T) { return T <= 64 ? 64 : (T <= 256 ? 128 : 256); }
 
 template <int BN, int EPI>
 static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
@@ -166,7 +168,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(a.n_mt, (a.T + BN - 1) / BN);
+  dim3 grid((a.T + BN - 1) / BN, a.n_mt);
   return launch_k(gemm_kernel<BN, EPI>, grid, dim3(192), Cfg::kSmem, st, map, a);
 }
 
@@ -186,7 +188,8 @@ cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cuda
   if (a.T <= 0) return cudaSuccess;
   switch (gemm_block_n(a.T)) {
     case 64: return launch_epi<64>(epi, a, map, st);
-    default: return launch_epi<128>(epi, a, map, st);
+    case 128: return launch_epi<128>(epi, a, map, st);
+    default: return launch_epi<256>(epi, a, map, st);
   }
 }
 
