@@ -236,7 +236,7 @@ def main():
     inputs = M.synthetic_inputs(cfg, seed=0)
     tl_run = eng.execute(placement, inputs=inputs)
     tl = tl_run.timeline
-    dma_rates, dec_rates = [], []
+    dma_rates, eff_rates, dec_rates = [], [], []
     kinds = {M.MODULE_NAMES[k]: k for k in cfg.kinds}
     kv_bytes_tok = 2 * cfg.lm_hkv * cfg.lm_hd * 2
     for e in tl.events:
@@ -245,7 +245,8 @@ def main():
             continue
         nbytes = eng.layer_bytes(kinds[e.module])
         if e.engine is ls.Engine.COPY:
-            dma_rates.append(nbytes / (dur * 1e6))
+            dma_rates.append(eng.stream_bytes[kinds[e.module]][e.layer] / (dur * 1e6))
+            eff_rates.append(nbytes / (dur * 1e6))
         elif e.module == "vlm" and e.phase == "decode" and e.layer in placement.for_module("vlm"):
             ctx = cfg.prompt_len + e.invocation + 1
             dec_rates.append((nbytes + ctx * kv_bytes_tok) / (dur * 1e6))
@@ -289,10 +290,18 @@ def main():
             measured.append((k, eng.execute(pl, inputs=inputs, record_timeline=False).total_ms / 1e3))
         preds = ls.predict(prof.calibration_total_s, ls.slope_from_profile(vlm), ks)
         rep = ls.validate(preds, measured)
+        # the schedule model (dfbsim) on the same measured profile, as a predictor
+        sims = [ls.simulated_total(prof, ls.Placement({"vlm": ls.interleaved_indices(k, vlm.layers)}
+                                                      if k else {})) / 1e3 for k in ks]
+        model_err = [(s - m) / m * 100.0 for s, (_, m) in zip(sims, measured)]
         pred = {"k": ks, "measured_s": [m for _, m in measured],
                 "predicted_s": [p.predicted_s for p in preds],
                 "error_pct": [r.error_pct for r in rep.rows], "max_abs_error_pct": rep.max_abs_error_pct,
-                "fitted_slope_s": rep.fitted_slope_s}
+                "fitted_slope_s": rep.fitted_slope_s,
+                "eq10_note": "reference Eq. 10 (linear in k); departs at k near L-1 where prefill "
+                             "runs of resident layers exceed the consecutive limit floor(dma/exe)",
+                "dfbsim_predicted_s": sims, "dfbsim_error_pct": model_err,
+                "dfbsim_max_abs_error_pct": max(abs(x) for x in model_err)}
         eng.set_placement(placement)
 
     # dominant-kernel roofline: the decode gate|up GEMV (largest HBM stream of the step)
@@ -332,6 +341,8 @@ def main():
                 "streamed_weight_bytes_per_step": launches["h2d_bytes"]},
         "h2d": {"streamed_layer_gbs": h2d_streamed, "peak_gbs": h2d_peak,
                 "frac": (h2d_streamed / h2d_peak) if h2d_streamed else None,
+                "effective_weight_gbs": statistics.fmean(eff_rates) if eff_rates else None,
+                "ecf_modules": [M.MODULE_NAMES[k] for k in eng.ecf_kinds],
                 "peak_source": "measured on this box: pinned 1 GiB cudaMemcpyAsync, best of 5"},
         "predictor": pred,
         "lower_bound": {"dfbsim_total_s": sim_bound_s, "measured_over_bound": (ms / 1e3) / sim_bound_s,

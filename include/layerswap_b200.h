@@ -229,6 +229,13 @@ int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr);
 int ls_exec_set_global_host(ls_exec* e, int32_t id, void* host_ptr);
 /* Pinned host buffers of every layer of one module (streamed source). */
 int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_ptrs, int32_t n);
+/* ECF-compressed host blobs of one module's layers: streamed layers of that
+ * module are transferred compressed (bytes[i] each) into the tail of their
+ * DFB slot and decoded on the GPU into the slot head.  Only accepted when
+ * layer bytes + blob bytes fit in one slot, so the VRAM accounting is
+ * unchanged (slots = slot_count x largest layer, dfbsim.py:266). */
+int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* host_ptrs,
+                                const uint64_t* bytes, int32_t n);
 /* Upload resident layers for a placement mask (module order vit, lm, expert). */
 int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n);
 /* out: cap, used, high_water, slots, always_resident, overhead, resident (bytes) */
@@ -272,6 +279,8 @@ int ls_k_gemm(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, cons
               int32_t T, int64_t ldx, void* out, int64_t ldo, const float* bias,
               const void* bias_bf16, int32_t n_valid, void* stream);
 int ls_k_decode_attention(const void* args, void* stream);
+/* Lossless exponent-coded BF16 (ECF) blob -> BF16 words (decode + exception patch). */
+int ls_k_ecf_decode(const void* blob, void* out, void* stream);
 int ls_k_flash_attention(const void* args, void* stream);
 int ls_k_rmsnorm_rows(const float* x, const void* w, void* out, int32_t T, int32_t D, float eps,
                       void* stream);

@@ -79,6 +79,14 @@ int ls_k_gemm(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void
   return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm");
 }
 
+int ls_k_ecf_decode(const void* blob, void* out, void* stream) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  return cuda_rc(launch_ecf_decode(static_cast<const uint8_t*>(blob), out, nsm,
+                                   static_cast<cudaStream_t>(stream)),
+                 "ls_k_ecf_decode");
+}
+
 int ls_k_decode_attention(const void* args, void* stream) {
   return cuda_rc(launch_decode_attention(*static_cast<const DecodeAttnArgs*>(args),
                                          static_cast<cudaStream_t>(stream)),

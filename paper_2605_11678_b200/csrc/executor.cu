@@ -162,6 +162,9 @@ struct Module {
   std::vector<const char*> host;
   std::vector<char*> resident;  // nullptr: streamed
   std::vector<int> phase_reps;
+  bool ecf = false;                 // stream ECF-compressed blobs
+  std::vector<const char*> host_ecf;
+  std::vector<uint64_t> ecf_bytes;
 };
 
 }  // namespace
@@ -734,6 +737,32 @@ int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_pt
   return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
 }
 
+int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* host_ptrs,
+                                const uint64_t* bytes, int32_t n) {
+  for (auto& m : e->mods) {
+    if (m.kind != kind) continue;
+    if (n != m.layers) return set_error(LS_ERR_VALUE, "expected %d host layers, got %d", m.layers, n);
+    uint64_t worst = 0;
+    for (int i = 0; i < n; ++i) worst = std::max<uint64_t>(worst, bytes[i]);
+    if (align_up(m.lay.total, 256) + worst + 256 > e->slot_bytes)
+      return set_error(LS_ERR_VALUE,
+                       "compressed staging does not fit in a DFB slot (layer %llu + blob %llu > "
+                       "slot %llu bytes)",
+                       static_cast<unsigned long long>(m.lay.total),
+                       static_cast<unsigned long long>(worst),
+                       static_cast<unsigned long long>(e->slot_bytes));
+    m.host_ecf.assign(n, nullptr);
+    m.ecf_bytes.assign(n, 0);
+    for (int i = 0; i < n; ++i) {
+      m.host_ecf[i] = static_cast<const char*>(host_ptrs[i]);
+      m.ecf_bytes[i] = bytes[i];
+    }
+    m.ecf = true;
+    return LS_OK;
+  }
+  return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
+}
+
 int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n) {
   int64_t total = 0;
   for (auto& m : e->mods) total += m.layers;
@@ -848,6 +877,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
         for (int l = 0; l < m.layers; ++l) {
           const char* w = m.resident[l];
           int slot = -1, dma0 = -1, dma1 = -1;
+          const uint8_t* ecf_src = nullptr;
           if (!w) {
             slot = sseq++ % nsl;
             if (slot_used[slot]) CK(cudaStreamWaitEvent(e->cs, e->comp_done[slot], 0));
@@ -856,16 +886,26 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
               CK(cudaStreamWaitEvent(e->cs, e->inv_done, 0));
               pending_barrier = false;
             }
+            // ECF: blob lands in the slot's tail, decoded into its head on the compute stream
+            const uint64_t nbytes = m.ecf ? m.ecf_bytes[l] : m.lay.total;
+            char* dst = m.ecf ? e->slots[slot] + ((e->slot_bytes - nbytes) & ~uint64_t(255))
+                              : e->slots[slot];
             if (timing) dma0 = tick(e->cs);
-            CK(cudaMemcpyAsync(e->slots[slot], m.host[l], m.lay.total, cudaMemcpyHostToDevice, e->cs));
+            CK(cudaMemcpyAsync(dst, m.ecf ? m.host_ecf[l] : m.host[l], nbytes,
+                               cudaMemcpyHostToDevice, e->cs));
             ++e->h2d_copies;
-            e->h2d_bytes += m.lay.total;
+            e->h2d_bytes += nbytes;
             if (timing) dma1 = tick(e->cs);
             CK(cudaEventRecord(e->dma_done[slot], e->cs));
             SSOP(cudaStreamWaitEvent(e->ss, e->dma_done[slot], 0));
             w = e->slots[slot];
+            if (m.ecf) ecf_src = reinterpret_cast<const uint8_t*>(dst);
           }
           int x0 = timing ? tick(e->ss) : -1;
+          if (ecf_src) {
+            KL(launch_ecf_decode(ecf_src, const_cast<char*>(w), e->nsm, e->ss));
+            ++e->launches;  // decode + exception patch
+          }
           RC(run_layer(e, m, ph, inv, l, w));
           int x1 = timing ? tick(e->ss) : -1;
           if (slot >= 0) {

@@ -136,4 +136,19 @@ cudaError_t launch_action_out_euler(const float* h, const bf16* norm_w, float ep
                                     cudaStream_t st);
 cudaError_t launch_fill_u64(unsigned long long* p, unsigned long long v, int n, cudaStream_t st);
 
+// ---------------- ECF: lossless exponent-coded BF16 for streamed layers ----------
+// Self-describing blob: this 64-byte header, then the SM plane (n_words bytes),
+// the 4-bit code plane (n_words/2 bytes), exception word indices (u32) and
+// exception exponents (u8); every section 16-byte aligned.  n_words % 16 == 0.
+struct EcfHeader {
+  uint32_t magic;  // 'ECF1'
+  uint32_t n_exc;
+  uint64_t n_words;
+  uint64_t off_sm, off_code, off_idx, off_exp;
+  uint8_t codebook[16];  // exponent of code c (code 15 = escape -> exponent from exceptions)
+};
+static_assert(sizeof(EcfHeader) == 64, "ECF header is 64 bytes");
+// decode + exception patch (two kernels) from a device blob into `out`
+cudaError_t launch_ecf_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st);
+
 }  // namespace lsb

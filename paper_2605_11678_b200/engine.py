@@ -20,6 +20,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _native
+from . import ecf
 from . import model as M
 from .dfbsim import Engine as EngineKind
 from .dfbsim import Mode, Placement, SimConfig, SimEvent, Timeline
@@ -49,6 +50,8 @@ def _bind():
         "ls_exec_global_ptr": [vp, C.c_int32, C.POINTER(vp)],
         "ls_exec_set_global_host": [vp, C.c_int32, vp],
         "ls_exec_set_host_layers": [vp, C.c_int32, C.POINTER(vp), C.c_int32],
+        "ls_exec_set_host_layers_ecf": [vp, C.c_int32, C.POINTER(vp), C.POINTER(C.c_uint64),
+                                        C.c_int32],
         "ls_exec_set_placement": [vp, C.POINTER(C.c_uint8), C.c_int64],
         "ls_exec_memory": [vp, C.POINTER(C.c_uint64)],
         "ls_exec_streams": [vp, C.POINTER(vp), C.POINTER(vp)],
@@ -102,7 +105,7 @@ class DemandLayeringEngine:
 
     def __init__(self, cfg: M.ModelConfig = M.ALPAMAYO, *, device: int = 0,
                  vram_cap_mb: float = 16000.0, n_slots: int = 2, seed: int = 0,
-                 keep_logical: bool = False) -> None:
+                 keep_logical: bool = False, ecf: bool = True) -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("DemandLayeringEngine needs a CUDA device (B200, sm_100a)")
         self.lib = _bind()
@@ -112,6 +115,7 @@ class DemandLayeringEngine:
         self.vram_cap_mb = vram_cap_mb
         self.n_slots = n_slots
         self.seed = seed
+        self.use_ecf = ecf
         torch.cuda.set_device(device)
         self._dims = cfg.dims()
         self.handle = C.c_void_p()
@@ -150,6 +154,9 @@ class DemandLayeringEngine:
         torch.cuda.synchronize()
 
     def _init_layers(self) -> None:
+        slot = max(self.layouts[k].total for k in self.kinds)
+        self.stream_bytes = {}
+        self.ecf_kinds = []
         for kind in self.kinds:
             lay = self.layouts[kind]
             n = self.cfg.layers_of(kind)
@@ -157,15 +164,38 @@ class DemandLayeringEngine:
             arena = HostArena(stride * n)
             self.arenas[kind] = arena
             ptrs = (C.c_void_p * n)()
+            # ECF only where layer + blob fit one DFB slot (no change to VRAM accounting)
+            want_ecf = self.use_ecf and _a256(lay.total) + int(0.8 * lay.total) + 256 <= slot
+            blobs = []
             for layer in range(n):
                 t = M.layer_tensors(self.cfg, kind, layer, self.seed, self.dev)
                 buf = M.pack_layer(self.cfg, kind, t)
                 arena.tensor[layer * stride:layer * stride + lay.total].copy_(buf)
                 ptrs[layer] = arena.ptr.value + layer * stride
+                if want_ecf:
+                    blobs.append(ecf.compress(buf))
                 if self.logical is not None:
                     self.logical["layers"][(kind, layer)] = {k: v.float().cpu() for k, v in t.items()}
                 del t, buf
             _native.check(self.lib.ls_exec_set_host_layers(self.handle, kind, ptrs, n), RuntimeError)
+            self.stream_bytes[kind] = [lay.total] * n
+            if blobs and _a256(lay.total) + max(b.numel() for b in blobs) + 256 <= slot:
+                sizes = [b.numel() for b in blobs]
+                strides = [(s + 4095) // 4096 * 4096 for s in sizes]
+                earena = HostArena(sum(strides))
+                self.arenas[("ecf", kind)] = earena
+                eptrs = (C.c_void_p * n)()
+                nbytes = (C.c_uint64 * n)(*sizes)
+                off = 0
+                for i, b in enumerate(blobs):
+                    earena.tensor[off:off + sizes[i]].copy_(b)
+                    eptrs[i] = earena.ptr.value + off
+                    off += strides[i]
+                _native.check(self.lib.ls_exec_set_host_layers_ecf(self.handle, kind, eptrs, nbytes, n),
+                              RuntimeError)
+                self.stream_bytes[kind] = sizes
+                self.ecf_kinds.append(kind)
+            del blobs
         torch.cuda.synchronize()
 
     def close(self) -> None:
@@ -327,7 +357,8 @@ class DemandLayeringEngine:
                 dma = statistics.fmean(samples[(name, ph, "copy")])
                 exe = statistics.fmean(samples[(name, ph, "execute")])
                 phases.append(PhaseProfile(name=ph, repetitions=reps, dma_ms=dma, exe_ms=exe))
-                dma_bytes += self.layer_bytes(kind) * len(samples[(name, ph, "copy")])
+                dma_bytes += (statistics.fmean(self.stream_bytes[kind])
+                              * len(samples[(name, ph, "copy")]))
                 dma_ms += sum(samples[(name, ph, "copy")])
             modules.append(ModuleProfile(name=name, layers=self.cfg.layers_of(kind),
                                          layer_mem_mb=M.layer_mem_mb(self.cfg, kind),
@@ -347,6 +378,10 @@ class DemandLayeringEngine:
 
 def _ptr(t):
     return None if t is None else t.data_ptr()
+
+
+def _a256(v: int) -> int:
+    return (v + 255) // 256 * 256
 
 
 def _copy_to_device_ptr(dst: int, src: torch.Tensor) -> None:
