@@ -24,8 +24,11 @@ def _a16(v: int) -> int:
 
 def compress(buf: torch.Tensor) -> torch.Tensor:
     """uint8 tensor (BF16 words, any device) -> ECF blob (uint8, same device)."""
-    assert buf.dtype == torch.uint8 and buf.numel() % 32 == 0, "need whole 16-word groups"
+    assert buf.dtype == torch.uint8 and buf.numel() % 2 == 0, "need whole BF16 words"
     dev = buf.device
+    pad = (-buf.numel()) % 32  # whole 16-word groups; the decoder may write <= 30 bytes past the end
+    if pad:
+        buf = torch.cat([buf, torch.zeros(pad, dtype=torch.uint8, device=dev)])
     w = buf.view(torch.int16).to(torch.int32) & 0xFFFF
     n = w.numel()
     e = (w >> 7) & 0xFF
@@ -66,10 +69,10 @@ def decompress_gpu(blob: torch.Tensor, n_bytes: int, stream=None) -> torch.Tenso
     fn = lib.ls_k_ecf_decode
     fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     fn.restype = C.c_int
-    out = torch.empty(n_bytes, dtype=torch.uint8, device=blob.device)
+    out = torch.empty(n_bytes + 32, dtype=torch.uint8, device=blob.device)
     s = stream if stream is not None else torch.cuda.current_stream()
     _native.check(fn(blob.data_ptr(), out.data_ptr(), s.cuda_stream), RuntimeError)
-    return out
+    return out[:n_bytes]
 
 
 def decompress_cpu(blob: torch.Tensor) -> torch.Tensor:

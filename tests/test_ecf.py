@@ -22,6 +22,13 @@ def test_cpu_roundtrip_and_ratio():
     assert blob.numel() / buf.numel() < 0.76
 
 
+def test_cpu_roundtrip_ragged_length():
+    buf = _weights(1_000)[:-18]  # not a whole 16-word group
+    out = ecf.decompress_cpu(ecf.compress(buf))
+    assert torch.equal(out[:buf.numel()], buf)
+    assert not out[buf.numel():].any()
+
+
 @pytest.mark.gpu
 @pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")
 def test_gpu_decoder_bit_exact():
