@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--vram-cap-mb", type=float, default=16000.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="per-invocation barrier (reference default) instead of cross-invocation prefetch")
     ap.add_argument("--profile-iters", type=int, default=2)
     ap.add_argument("--dump", default=None, help="directory for profile/plan/timeline artefacts")
     args = ap.parse_args()
@@ -228,13 +230,14 @@ def main():
 
     h2d_peak = measure_h2d_peak(torch, device)
     eng = DemandLayeringEngine(cfg, device=local, vram_cap_mb=args.vram_cap_mb, n_slots=2, seed=0)
-    prof = eng.profile_run(iterations=args.profile_iters, warmup=1)
-    plan = ls.plan_for_budget(prof, prof.hardware.vram_mb, include_simulated=True)
+    sim_cfg = ls.SimConfig(cross_invocation_prefetch=not args.no_prefetch)
+    prof = eng.profile_run(iterations=args.profile_iters, warmup=1, config=sim_cfg)
+    plan = ls.plan_for_budget(prof, prof.hardware.vram_mb, sim_cfg, include_simulated=True)
     placement = plan.placement
 
     # one timeline-recorded pipelined run at the plan: H2D and decode-layer HBM rates
     inputs = M.synthetic_inputs(cfg, seed=0)
-    tl_run = eng.execute(placement, inputs=inputs)
+    tl_run = eng.execute(placement, sim_cfg, inputs=inputs)
     tl = tl_run.timeline
     dma_rates, eff_rates, dec_rates = [], [], []
     kinds = {M.MODULE_NAMES[k]: k for k in cfg.kinds}
@@ -254,7 +257,7 @@ def main():
 
     # warm-up, then EXACTLY K timed steps (device events per step; barrier + sync both sides)
     for _ in range(args.warmup):
-        eng.execute(placement, inputs=inputs, record_timeline=False)
+        eng.execute(placement, sim_cfg, inputs=inputs, record_timeline=False)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(device)
@@ -262,7 +265,7 @@ def main():
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):
-            step_ms.append(eng.execute(placement, inputs=inputs, record_timeline=False).total_ms)
+            step_ms.append(eng.execute(placement, sim_cfg, inputs=inputs, record_timeline=False).total_ms)
         wall = time.perf_counter() - t_wall
     torch.cuda.synchronize(device)
     launches = eng.last_run_stats()
@@ -275,7 +278,7 @@ def main():
         ms = float(t.item())
 
     # end-to-end through the public API with pinned host buffers
-    e2e_ms = [eng.infer(inputs, placement).e2e_ms for _ in range(args.steps)]
+    e2e_ms = [eng.infer(inputs, placement, sim_cfg).e2e_ms for _ in range(args.steps)]
     h2d_io, d2h_io = eng.io_bytes(cfg)
 
     # predictor (Eq. 10) vs measured over a vlm-only interleaved sweep
@@ -287,12 +290,13 @@ def main():
         measured = [(0, prof.calibration_total_s)]
         for k in ks[1:]:
             pl = ls.Placement({"vlm": ls.interleaved_indices(k, vlm.layers)})
-            measured.append((k, eng.execute(pl, inputs=inputs, record_timeline=False).total_ms / 1e3))
+            measured.append((k, eng.execute(pl, sim_cfg, inputs=inputs,
+                                            record_timeline=False).total_ms / 1e3))
         preds = ls.predict(prof.calibration_total_s, ls.slope_from_profile(vlm), ks)
         rep = ls.validate(preds, measured)
         # the schedule model (dfbsim) on the same measured profile, as a predictor
         sims = [ls.simulated_total(prof, ls.Placement({"vlm": ls.interleaved_indices(k, vlm.layers)}
-                                                      if k else {})) / 1e3 for k in ks]
+                                                      if k else {}), sim_cfg) / 1e3 for k in ks]
         model_err = [(s - m) / m * 100.0 for s, (_, m) in zip(sims, measured)]
         pred = {"k": ks, "measured_s": [m for _, m in measured],
                 "predicted_s": [p.predicted_s for p in preds],
@@ -334,6 +338,8 @@ def main():
                    "prompt_tokens": cfg.prompt_len, "decode_steps": cfg.decode_steps,
                    "euler_steps": cfg.euler_steps if cfg.has_expert else 0,
                    "placement": plan.resident_count_per_module,
+                   "sim_config": {"mode": sim_cfg.mode.value, "slot_count": sim_cfg.slot_count,
+                                  "cross_invocation_prefetch": sim_cfg.cross_invocation_prefetch},
                    "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
                    "l2": "inputs larger than L2 (21 GB streamed + resident weights per step)"},
         "e2e": {"value": statistics.fmean(e2e_ms) / 1e3, "unit": "s",

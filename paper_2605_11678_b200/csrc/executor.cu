@@ -593,13 +593,17 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     auto A = [&](void* dst, uint64_t bytes) { return alloc_into(e, dst, bytes, &e->bytes_overhead); };
 #define OV(field, bytes) \
   if (int rc = A(&e->field, (bytes))) return fail(rc)
+    // Phase scratch: ViT (0), LM prefill (1) and expert (2) activations are never
+    // live at the same time, so they share one region sized for the largest set.
+    std::vector<std::pair<char**, uint64_t>> sets[3], alias;
+#define SC(set, field, bytes) sets[set].push_back({reinterpret_cast<char**>(&e->field), (bytes)})
     OV(kv, 2ull * d.lm_layers * 2 * d.lm_hkv * (e->ctx + 1) * d.lm_hd);
     OV(lm_h, 4ull * S * d.lm_d);
-    OV(lm_norm, 2ull * S * d.lm_d);
-    OV(lm_qkv, 2ull * S * QN);
-    OV(lm_q, 2ull * S * AH);
-    OV(lm_attn, 2ull * S * AH);
-    OV(lm_mlp, 2ull * S * d.lm_ffn);
+    SC(1, lm_norm, 2ull * S * d.lm_d);
+    SC(1, lm_qkv, 2ull * S * QN);
+    SC(1, lm_q, 2ull * S * AH);
+    SC(1, lm_attn, 2ull * S * AH);
+    SC(1, lm_mlp, 2ull * S * d.lm_ffn);
     OV(text_ids, 4ull * (d.prompt_prefix + d.prompt_suffix + 1));
     OV(dec_h, 4ull * d.lm_d);
     OV(dec_q, 4ull * AH);
@@ -633,23 +637,25 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     OV(gemv_cnt, cnt);
     if (d.has_vit) {
       const int H = d.vit_heads * d.vit_hd;
-      OV(patches, 2ull * Tv * d.vit_patch_dim);
-      OV(vit_h, 4ull * Tv * d.vit_d);
-      OV(vit_ln, 2ull * Tv * d.vit_d);
-      OV(vit_qkv, 2ull * Tv * 3 * H);
-      OV(vit_attn, 2ull * Tv * H);
-      OV(vit_fc1, 2ull * Tv * e->vit_ffn_pad);
-      OV(merger_mid, 2ull * (Tv / 4) * 4 * d.vit_d);
+      SC(0, vit_h, 4ull * Tv * d.vit_d);
+      SC(0, vit_ln, 2ull * Tv * d.vit_d);
+      SC(0, vit_qkv, 2ull * Tv * 3 * H);
+      SC(0, vit_attn, 2ull * Tv * H);
+      // dead-by-then buffers alias the qkv|attn pair: patches (before layer 0),
+      // fc1 output (after proj consumed attn), merger hidden (after the last layer)
+      alias.push_back({reinterpret_cast<char**>(&e->patches), 2ull * Tv * d.vit_patch_dim});
+      alias.push_back({reinterpret_cast<char**>(&e->vit_fc1), 2ull * Tv * e->vit_ffn_pad});
+      alias.push_back({reinterpret_cast<char**>(&e->merger_mid), 2ull * (Tv / 4) * 4 * d.vit_d});
     }
     if (d.has_expert) {
       const int EQN = (d.ex_hq + 2 * d.ex_hkv) * d.ex_hd, EAH = d.ex_hq * d.ex_hd;
-      OV(ex_h, 4ull * Te * d.ex_d);
-      OV(ex_norm, 2ull * Te * d.ex_d);
-      OV(ex_qkv, 2ull * Te * EQN);
-      OV(ex_q, 2ull * Te * EAH);
-      OV(ex_kv, 2ull * 2 * d.ex_hkv * Te * d.ex_hd);
-      OV(ex_attn, 2ull * Te * EAH);
-      OV(ex_mlp, 2ull * Te * d.ex_ffn);
+      SC(2, ex_h, 4ull * Te * d.ex_d);
+      SC(2, ex_norm, 2ull * Te * d.ex_d);
+      SC(2, ex_qkv, 2ull * Te * EQN);
+      SC(2, ex_q, 2ull * Te * EAH);
+      SC(2, ex_kv, 2ull * 2 * d.ex_hkv * Te * d.ex_hd);
+      SC(2, ex_attn, 2ull * Te * EAH);
+      SC(2, ex_mlp, 2ull * Te * d.ex_ffn);
       OV(temb_in, 4ull * d.time_dim);
       OV(temb_mid, 4ull * d.ex_d);
       OV(temb, 4ull * d.ex_d);
@@ -657,6 +663,31 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       OV(velocity, 4ull * Te * d.action_dim);
       OV(noise, 4ull * Te * d.action_dim);
     }
+    // ViT aliases start at vit_qkv (entry 2 of set 0)
+    uint64_t scratch = 0, alias_off = 0;
+    for (int si = 0; si < 3; ++si) {
+      uint64_t sz = 0;
+      for (size_t i = 0; i < sets[si].size(); ++i) {
+        sz = align_up(sz, 1024);
+        if (si == 0 && i == 2) alias_off = sz;
+        sz += sets[si][i].second;
+      }
+      if (si == 0)
+        for (auto& f : alias) sz = std::max(sz, alias_off + f.second);
+      scratch = std::max(scratch, sz);
+    }
+    char* base = nullptr;
+    if (int rc = A(&base, scratch)) return fail(rc);
+    for (auto& s : sets) {
+      uint64_t off = 0;
+      for (auto& f : s) {
+        off = align_up(off, 1024);
+        *f.first = base + off;
+        off += f.second;
+      }
+    }
+    for (auto& f : alias) *f.first = base + alias_off;
+#undef SC
 #undef OV
     if (cudaMemset(e->ar.base, 0, e->ar.used) != cudaSuccess)
       return fail(set_error(LS_ERR_CUDA, "arena memset failed"));
