@@ -188,7 +188,11 @@ typedef struct ls_dims {
   /* 1: the token-embedding table stays in page-locked host memory and the
    * GPU gathers the rows it needs (zero-copy over PCIe) instead of holding
    * vocab x d bf16 (1.2 GB) under the VRAM cap. */
-  int32_t embed_on_host, _pad0;
+  int32_t embed_on_host;
+  /* tensor parallelism: this rank holds 1/tp_world of every layer (per-rank
+   * head / FFN counts below); row-parallel outputs are all-reduced (NCCL). */
+  int32_t tp_world, tp_rank;
+  int32_t tp_force; /* 1: take the all-reduce path even at tp_world == 1 (tests) */
   /* ViT encoder + patch merger */
   int32_t vit_layers, vit_d, vit_heads, vit_hd, vit_ffn, vit_patch_dim, vit_images,
       vit_tokens_per_image;
@@ -225,6 +229,10 @@ int ls_exec_create(const ls_dims* d, int32_t device, uint64_t cap_bytes, int32_t
                    ls_exec** out);
 int ls_exec_destroy(ls_exec* e);
 int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr);
+/* NCCL communicator for tensor parallelism (dims.tp_world > 1): every rank
+ * passes the 128-byte id rank 0 obtained from ls_nccl_unique_id. */
+int ls_nccl_unique_id(uint8_t out[128]);
+int ls_exec_set_tp(ls_exec* e, const uint8_t id[128]);
 /* Point an always-resident slot at page-locked host memory (embed_on_host). */
 int ls_exec_set_global_host(ls_exec* e, int32_t id, void* host_ptr);
 /* Pinned host buffers of every layer of one module (streamed source). */

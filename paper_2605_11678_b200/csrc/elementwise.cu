@@ -2,6 +2,8 @@
 // embeddings, the action-expert input/output heads and small glue kernels.
 // All HBM-bound and tiny next to the weight streams; one CTA per row where a
 // row reduction is needed, vectorised 16-byte accesses where rows allow.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -276,6 +278,32 @@ __global__ void silu_kernel(float* x, int n) {
 
 cudaError_t launch_silu_inplace(float* x, int n, cudaStream_t st) {
   return launch_k(silu_kernel, dim3((n + 255) / 256), dim3(256), 0, st, x, n);
+}
+
+// x += y (tensor-parallel partial sums after the all-reduce), float4 vectorised.
+__global__ void add_f32_kernel(float* __restrict__ x, const float* __restrict__ y, long n) {
+  pdl_trigger();
+  pdl_wait();
+  const long n4 = n / 4;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(x)[i];
+    const float4 b = reinterpret_cast<const float4*>(y)[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    reinterpret_cast<float4*>(x)[i] = a;
+  }
+  for (long i = 4 * n4 + blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    x[i] += y[i];
+}
+
+cudaError_t launch_add_f32(float* x, const float* y, long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const long blocks = std::min<long>((n / 4 + 255) / 256 + 1, 1184);
+  return launch_k(add_f32_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, x, y, n);
 }
 
 }  // namespace lsb

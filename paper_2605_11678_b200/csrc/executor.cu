@@ -19,6 +19,9 @@
 // The host thread only enqueues: the whole inference (ViT -> merger -> LM
 // prefill -> greedy decode -> flow-matching expert) is issued without a
 // single host synchronisation; greedy tokens stay on the device.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -57,6 +60,38 @@ using namespace lsb;
   } while (0)
 
 namespace {
+
+// NCCL is resolved at run time (torch's bundled libnccl.so.2 is already mapped
+// in-process), so the library has no link-time NCCL dependency.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+      api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+      api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+      api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy &&
+               api.error_string;
+    }
+  }
+  return api;
+}
 
 uint64_t tiled_bytes(int n, int k) {
   return static_cast<uint64_t>((n + 127) / 128) * static_cast<uint64_t>((k + 63) / 64) * 16384ull;
@@ -201,6 +236,13 @@ struct ls_exec {
       m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
   GemvPlan gp_qkv{}, gp_o{}, gp_gu{}, gp_down{}, gp_head{}, gp_t1{}, gp_t2{};
   bool use_pdl = true, pdl_ok = false;
+  // tensor parallelism: row-parallel outputs go to tp_buf, are summed across
+  // ranks by NCCL on the compute stream, then added into the residual stream
+  int tp_world = 1, tp_rank = 0;
+  bool tp_on = false;
+  ncclComm_t comm = nullptr;
+  float* tp_buf = nullptr;
+  uint64_t tp_buf_elems = 0;
   int64_t launches = 0, h2d_copies = 0;
   uint64_t h2d_bytes = 0;
 
@@ -298,6 +340,33 @@ FlashArgs flash_base(int Tq, int hq, int hkv, int hd) {
     if (rc_) return rc_;     \
   } while (0)
 
+// Row-parallel projections (o-proj, down-proj, ViT proj / fc2) into the fp32
+// residual stream dst[T x n]: the fused RESID epilogue on one GPU; under tensor
+// parallelism the partial product goes to tp_buf, is summed across ranks by
+// NCCL on the compute stream, and is then added.
+int tp_reduce_add(ls_exec* e, float* dst, long count) {
+  NcclApi& api = nccl_api();
+  ncclResult_t r = api.all_reduce(e->tp_buf, e->tp_buf, static_cast<size_t>(count), ncclFloat32,
+                                  ncclSum, e->comm, e->ss);
+  if (r != ncclSuccess) return set_error(LS_ERR_NCCL, "ncclAllReduce: %s", api.error_string(r));
+  e->pdl_ok = false;
+  KL(launch_add_f32(dst, e->tp_buf, count, e->ss));
+  return LS_OK;
+}
+
+int resid_gemm(ls_exec* e, const char* w, int n, int k, int T, const CUtensorMap& map, float* dst,
+               const void* bias_bf16 = nullptr) {
+  if (!e->tp_on) return gemm(e, GEMM_RESID_F32, w, n, k, T, map, dst, n, bias_bf16);
+  RC(gemm(e, GEMM_F32, w, n, k, T, map, e->tp_buf, n, bias_bf16));
+  return tp_reduce_add(e, dst, static_cast<long>(T) * n);
+}
+
+int resid_gemv(ls_exec* e, const GemvPlan& p, const char* w, const float* x, float* dst) {
+  if (!e->tp_on) return gemv(e, GEMV_RESID, p, w, x, dst, nullptr);
+  RC(gemv(e, GEMV_F32, p, w, x, e->tp_buf, nullptr));
+  return tp_reduce_add(e, dst, p.n);
+}
+
 int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L) {
   const ls_dims& d = e->d;
   const int T = e->Tv, D = d.vit_d, H = d.vit_heads * d.vit_hd, F = d.vit_ffn;
@@ -321,11 +390,11 @@ int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L) {
   f.o_head_stride = d.vit_hd;
   f.seg_len = d.vit_tokens_per_image;
   KL(launch_flash_attention(f, e->ss));
-  RC(gemm(e, GEMM_RESID_F32, part(1), D, H, T, e->m_vit_attn, e->vit_h, D, part(5)));
+  RC(resid_gemm(e, part(1), D, H, T, e->m_vit_attn, e->vit_h, part(5)));
   KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(10), (const bf16*)part(11), e->vit_ln, T, D,
                            D, d.vit_eps, e->ss));
   RC(gemm(e, GEMM_BF16_GELU, part(2), F, D, T, e->m_vit_ln, e->vit_fc1, e->vit_ffn_pad, part(6), F));
-  RC(gemm(e, GEMM_RESID_F32, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, D, part(7)));
+  RC(resid_gemm(e, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, part(7)));
   return LS_OK;
 }
 
@@ -352,11 +421,11 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l)
   f.o_head_stride = d.lm_hd;
   f.causal = 1;
   KL(launch_flash_attention(f, e->ss));
-  RC(gemm(e, GEMM_RESID_F32, part(1), D, AH, S, e->m_lm_attn, e->lm_h, D));
+  RC(resid_gemm(e, part(1), D, AH, S, e->m_lm_attn, e->lm_h));
   KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(5), e->lm_norm, S, D, d.lm_eps, e->ss));
   RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.lm_ffn, D, S, e->m_lm_norm, e->lm_mlp, d.lm_ffn,
           nullptr, d.lm_ffn));
-  RC(gemm(e, GEMM_RESID_F32, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h, D));
+  RC(resid_gemm(e, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h));
   return LS_OK;
 }
 
@@ -391,9 +460,9 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.counters = e->attn_cnt;
   a.n_split = decode_attn_splits(pos + 1);  // <= 64 positions per CTA
   KL(launch_decode_attention(a, e->ss));
-  RC(gemv(e, GEMV_RESID, e->gp_o, part(1), e->dec_attn, e->dec_h, nullptr));
+  RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h));
   RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn));
-  RC(gemv(e, GEMV_RESID, e->gp_down, part(3), e->dec_mlp, e->dec_h, nullptr));
+  RC(resid_gemv(e, e->gp_down, part(3), e->dec_mlp, e->dec_h));
   return LS_OK;
 }
 
@@ -427,11 +496,11 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
   f.o_tok_stride = AH;
   f.o_head_stride = d.ex_hd;
   KL(launch_flash_attention(f, e->ss));
-  RC(gemm(e, GEMM_RESID_F32, part(1), D, AH, T, e->m_ex_attn, e->ex_h, D));
+  RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h));
   KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
   RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.ex_ffn, D, T, e->m_ex_norm, e->ex_mlp, d.ex_ffn,
           nullptr, d.ex_ffn));
-  RC(gemm(e, GEMM_RESID_F32, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, D));
+  RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h));
   return LS_OK;
 }
 
@@ -664,6 +733,17 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       OV(noise, 4ull * Te * d.action_dim);
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
+    e->tp_world = std::max(1, d.tp_world);
+    e->tp_rank = d.tp_rank;
+    e->tp_on = e->tp_world > 1 || d.tp_force;
+    if (e->tp_on) {
+      uint64_t m1 = std::max<uint64_t>(static_cast<uint64_t>(S) * d.lm_d,
+                                       static_cast<uint64_t>(Tv) * d.vit_d);
+      uint64_t m2 = std::max<uint64_t>(static_cast<uint64_t>(Te) * d.ex_d,
+                                       static_cast<uint64_t>(d.lm_d));
+      e->tp_buf_elems = std::max(m1, m2);
+      OV(tp_buf, 4ull * e->tp_buf_elems);
+    }
     uint64_t scratch = 0, alias_off = 0;
     for (int si = 0; si < 3; ++si) {
       uint64_t sz = 0;
@@ -734,6 +814,7 @@ int ls_exec_destroy(ls_exec* e) {
   cudaEvent_t evs[] = {e->inv_done, e->exe_done, e->ev_begin, e->ev_t0, e->ev_t1, e->ev_end};
   for (auto v : evs)
     if (v) cudaEventDestroy(v);
+  if (e->comm && nccl_api().ok) nccl_api().comm_destroy(e->comm);
   if (e->cs) cudaStreamDestroy(e->cs);
   if (e->ss) cudaStreamDestroy(e->ss);
   if (e->ar.base) cudaFree(e->ar.base);
@@ -744,6 +825,29 @@ int ls_exec_destroy(ls_exec* e) {
 int ls_exec_global_ptr(ls_exec* e, int32_t id, void** dptr) {
   if (id < 0 || id >= LS_N_GLOBAL) return set_error(LS_ERR_VALUE, "bad global id %d", id);
   *dptr = e->g[id];
+  return LS_OK;
+}
+
+int ls_nccl_unique_id(uint8_t out[128]) {
+  NcclApi& api = nccl_api();
+  if (!api.ok) return set_error(LS_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  ncclResult_t r = api.get_unique_id(&id);
+  if (r != ncclSuccess) return set_error(LS_ERR_NCCL, "ncclGetUniqueId: %s", api.error_string(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &id, 128);
+  return LS_OK;
+}
+
+int ls_exec_set_tp(ls_exec* e, const uint8_t id_bytes[128]) {
+  if (!e->tp_on) return set_error(LS_ERR_VALUE, "executor was created without tensor parallelism");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return set_error(LS_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  std::memcpy(&id, id_bytes, 128);
+  CK(cudaSetDevice(e->dev));
+  ncclResult_t r = api.comm_init_rank(&e->comm, e->tp_world, id, e->tp_rank);
+  if (r != ncclSuccess) return set_error(LS_ERR_NCCL, "ncclCommInitRank: %s", api.error_string(r));
   return LS_OK;
 }
 
@@ -854,6 +958,8 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   const bool barrier = seq || !opts->cfg.cross_invocation_prefetch;
   const int nsl = std::max(1, std::min(opts->cfg.slot_count, e->n_slots));
   const bool timing = opts->record_timeline && events;
+  if (e->tp_on && !e->comm)
+    return set_error(LS_ERR_VALUE, "tensor-parallel executor has no communicator (ls_exec_set_tp)");
   for (auto& m : e->mods)
     for (int l = 0; l < m.layers; ++l)
       if (!m.resident[l] && !m.host[l])

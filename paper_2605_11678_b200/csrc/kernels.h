@@ -122,6 +122,7 @@ cudaError_t launch_embed_rows(const bf16* table, const int* ids, int n, int D, f
 cudaError_t launch_add_rows_bf16(float* x, const bf16* add, int T, int D, long period,
                                  cudaStream_t st);
 cudaError_t launch_silu_inplace(float* x, int n, cudaStream_t st);
+cudaError_t launch_add_f32(float* x, const float* y, long n, cudaStream_t st);  // x += y
 cudaError_t launch_cast_f32_bf16(const float* x, bf16* out, long n, cudaStream_t st);
 cudaError_t launch_argmax_to_token(const unsigned long long* key, int* token_out, int* history,
                                    int step, unsigned long long* key_reset, cudaStream_t st);

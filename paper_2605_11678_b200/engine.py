@@ -62,6 +62,8 @@ def _bind():
         "ls_host_alloc": [C.c_uint64, C.POINTER(vp)],
         "ls_host_free": [vp],
         "ls_copy": [vp, vp, C.c_uint64],
+        "ls_nccl_unique_id": [C.POINTER(C.c_uint8)],
+        "ls_exec_set_tp": [vp, C.POINTER(C.c_uint8)],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -105,10 +107,23 @@ class DemandLayeringEngine:
 
     def __init__(self, cfg: M.ModelConfig = M.ALPAMAYO, *, device: int = 0,
                  vram_cap_mb: float = 16000.0, n_slots: int = 2, seed: int = 0,
-                 keep_logical: bool = False, ecf: bool = True) -> None:
+                 keep_logical: bool = False, ecf: bool = True, tp_world: int = 1,
+                 tp_rank: int = 0, tp_id: bytes | None = None, tp_force: bool = False) -> None:
+        """tp_world > 1: this engine is rank `tp_rank` of a tensor-parallel group;
+        it holds and streams only its shard of every layer (model.tp_config /
+        shard_layer_tensors) and all-reduces row-parallel outputs with NCCL
+        (`tp_id` = the 128-byte id from `nccl_unique_id()` on rank 0)."""
         if not torch.cuda.is_available():
             raise RuntimeError("DemandLayeringEngine needs a CUDA device (B200, sm_100a)")
         self.lib = _bind()
+        self.full_cfg = cfg
+        self.tp_world, self.tp_rank = tp_world, tp_rank
+        self.tp_on = tp_world > 1 or tp_force
+        if self.tp_on:
+            import dataclasses as _dc
+            cfg = _dc.replace(M.tp_config(cfg, tp_world), tp_rank=tp_rank, tp_force=int(tp_force))
+            if tp_id is None and tp_world == 1:
+                tp_id = nccl_unique_id()
         self.cfg = cfg
         self.device = device
         self.dev = torch.device("cuda", device)
@@ -121,6 +136,11 @@ class DemandLayeringEngine:
         self.handle = C.c_void_p()
         _native.check(self.lib.ls_exec_create(C.byref(self._dims), device, int(vram_cap_mb * MIB),
                                               n_slots, C.byref(self.handle)), RuntimeError)
+        if self.tp_on:
+            if tp_id is None or len(tp_id) != 128:
+                raise ValueError("tensor parallelism needs the 128-byte NCCL id from rank 0")
+            idbuf = (C.c_uint8 * 128)(*tp_id)
+            _native.check(self.lib.ls_exec_set_tp(self.handle, idbuf), RuntimeError)
         self.kinds = cfg.kinds
         self.layouts = {k: M.layer_layout(cfg, k) for k in self.kinds}
         self.logical: dict | None = {"layers": {}, "globals": {}} if keep_logical else None
@@ -168,8 +188,10 @@ class DemandLayeringEngine:
             want_ecf = self.use_ecf and _a256(lay.total) + int(0.8 * lay.total) + 256 <= slot
             blobs = []
             for layer in range(n):
-                t = M.layer_tensors(self.cfg, kind, layer, self.seed, self.dev)
-                buf = M.pack_layer(self.cfg, kind, t)
+                t = M.layer_tensors(self.full_cfg, kind, layer, self.seed, self.dev)
+                shard = M.shard_layer_tensors(self.full_cfg, kind, t, self.tp_world, self.tp_rank)
+                buf = M.pack_layer(self.cfg, kind, shard)
+                del shard
                 arena.tensor[layer * stride:layer * stride + lay.total].copy_(buf)
                 ptrs[layer] = arena.ptr.value + layer * stride
                 if want_ecf:
@@ -374,6 +396,13 @@ class DemandLayeringEngine:
         return ModelProfile(hardware=hw, modules=tuple(modules),
                             always_resident_mb=mem["always_resident"] / MIB,
                             calibration_total_s=calibration)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id (rank 0) for DemandLayeringEngine(tp_world > 1)."""
+    buf = (C.c_uint8 * 128)()
+    _native.check(_bind().ls_nccl_unique_id(buf), RuntimeError)
+    return bytes(buf)
 
 
 def _ptr(t):

@@ -30,7 +30,7 @@ PHASES = {KIND_VIT: ("encode",), KIND_LM: ("prefill", "decode"), KIND_EXPERT: ("
 
 class Dims(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
-        "has_vit", "has_expert", "embed_on_host", "_pad0",
+        "has_vit", "has_expert", "embed_on_host", "tp_world", "tp_rank", "tp_force",
         "vit_layers", "vit_d", "vit_heads", "vit_hd", "vit_ffn", "vit_patch_dim", "vit_images",
         "vit_tokens_per_image",
         "lm_layers", "lm_d", "lm_hq", "lm_hkv", "lm_hd", "lm_ffn", "vocab", "prompt_prefix",
@@ -52,6 +52,9 @@ class ModelConfig:
     has_vit: bool = True
     has_expert: bool = True
     embed_on_host: bool = True         # token-embedding table gathered from pinned host memory
+    tp_world: int = 1                  # tensor-parallel degree this config is a shard of
+    tp_rank: int = 0
+    tp_force: int = 0                  # all-reduce path even at tp_world == 1 (tests)
     vit_layers: int = 27
     vit_d: int = 1152
     vit_heads: int = 16
@@ -90,7 +93,7 @@ class ModelConfig:
         vals["has_vit"] = int(self.has_vit)
         vals["has_expert"] = int(self.has_expert)
         vals["embed_on_host"] = int(self.embed_on_host)
-        return Dims(**vals, _pad=0.0, _pad0=0)
+        return Dims(**vals, _pad=0.0)
 
     @property
     def vis_tokens(self) -> int:
@@ -307,3 +310,87 @@ def describe(cfg: ModelConfig) -> dict:
 
 
 _ = math  # (kept for callers computing scales)
+
+
+# ----------------------------- tensor parallelism --------------------------------
+# north_star: every streamed layer is split across N GPUs so each GPU fetches 1/N
+# of it over its own PCIe link (Megatron column/row parallel).
+#   column-parallel: q/k/v heads, gate/up FFN features, ViT fc1 features
+#   row-parallel:    o-proj, down-proj, ViT proj/fc2 (partial sums -> all-reduce)
+# Norms are replicated; row-parallel biases live on rank 0 only (others zero).
+# FFN shards are zero-padded to 64-feature multiples (gate|up interleave unit).
+
+def _ceil_to(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+def tp_config(cfg: ModelConfig, world: int) -> ModelConfig:
+    """Per-rank ModelConfig for a TP degree (heads / FFN divided, d unchanged)."""
+    if world == 1:
+        return cfg
+    for name, v in (("lm_hq", cfg.lm_hq), ("lm_hkv", cfg.lm_hkv)):
+        if v % world:
+            raise ValueError(f"{name}={v} is not divisible by TP degree {world}")
+    kw = {"lm_hq": cfg.lm_hq // world, "lm_hkv": cfg.lm_hkv // world,
+          "lm_ffn": _ceil_to(-(-cfg.lm_ffn // world), 64)}
+    if cfg.has_vit:
+        if cfg.vit_heads % world:
+            raise ValueError(f"vit_heads={cfg.vit_heads} is not divisible by TP degree {world}")
+        kw.update(vit_heads=cfg.vit_heads // world, vit_ffn=-(-cfg.vit_ffn // world))
+    if cfg.has_expert:
+        if cfg.ex_hq % world or cfg.ex_hkv % world:
+            raise ValueError("expert heads are not divisible by the TP degree")
+        kw.update(ex_hq=cfg.ex_hq // world, ex_hkv=cfg.ex_hkv // world,
+                  ex_ffn=_ceil_to(-(-cfg.ex_ffn // world), 64))
+    return dataclasses.replace(cfg, name=f"{cfg.name}-tp{world}", tp_world=world, **kw)
+
+
+def _rows(t: torch.Tensor, lo: int, hi: int, n: int) -> torch.Tensor:
+    """Rows [lo, hi) of t, zero-padded to n rows."""
+    out = torch.zeros((n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    hi = min(hi, t.shape[0])
+    if hi > lo:
+        out[:hi - lo] = t[lo:hi]
+    return out
+
+
+def _cols(t: torch.Tensor, lo: int, hi: int, n: int) -> torch.Tensor:
+    return _rows(t.t(), lo, hi, n).t().contiguous()
+
+
+def shard_layer_tensors(cfg: ModelConfig, kind: int, t: dict, world: int, rank: int) -> dict:
+    """Logical tensors of one layer -> this rank's shard (tp_config shapes)."""
+    if world == 1:
+        return t
+    sc = tp_config(cfg, world)
+    if kind == KIND_VIT:
+        h, hd, d = sc.vit_heads, cfg.vit_hd, cfg.vit_d
+        F = sc.vit_ffn
+        qkv = t["qkv"].view(3, cfg.vit_heads, hd, d)[:, rank * h:(rank + 1) * h].reshape(3 * h * hd, d)
+        qkv_b = t["qkv_b"].view(3, cfg.vit_heads, hd)[:, rank * h:(rank + 1) * h].reshape(-1)
+        lo = rank * h * hd
+        out = {"qkv": qkv.contiguous(), "qkv_b": qkv_b.contiguous(),
+               "proj": t["proj"][:, lo:lo + h * hd].contiguous(),
+               "fc1": _rows(t["fc1"], rank * F, (rank + 1) * F, F),
+               "fc1_b": _rows(t["fc1_b"], rank * F, (rank + 1) * F, F),
+               "fc2": _cols(t["fc2"], rank * F, (rank + 1) * F, F)}
+        zero_unless_0 = (lambda x: x if rank == 0 else torch.zeros_like(x))
+        out["proj_b"] = zero_unless_0(t["proj_b"])
+        out["fc2_b"] = zero_unless_0(t["fc2_b"])
+        for n in ("ln1_w", "ln1_b", "ln2_w", "ln2_b"):
+            out[n] = t[n]
+        return out
+    if kind == KIND_LM:
+        hq, hkv, hd, F, Ff = sc.lm_hq, sc.lm_hkv, cfg.lm_hd, sc.lm_ffn, cfg.lm_ffn // world
+    else:
+        hq, hkv, hd, F, Ff = sc.ex_hq, sc.ex_hkv, cfg.ex_hd, sc.ex_ffn, -(-cfg.ex_ffn // world)
+    qlo, klo = rank * hq * hd, rank * hkv * hd
+    flo = rank * Ff
+    return {"q": t["q"][qlo:qlo + hq * hd].contiguous(),
+            "k": t["k"][klo:klo + hkv * hd].contiguous(),
+            "v": t["v"][klo:klo + hkv * hd].contiguous(),
+            "o": t["o"][:, qlo:qlo + hq * hd].contiguous(),
+            "gate": _rows(t["gate"], flo, flo + Ff, F), "up": _rows(t["up"], flo, flo + Ff, F),
+            "down": _cols(t["down"], flo, flo + Ff, F),
+            "attn_norm": t["attn_norm"], "mlp_norm": t["mlp_norm"],
+            "q_norm": t["q_norm"], "k_norm": t["k_norm"]}

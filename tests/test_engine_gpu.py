@@ -193,3 +193,21 @@ def test_vram_cap_is_enforced():
             eng.set_placement(ls.Placement.of({"vlm": range(fit + 1)}))
     finally:
         eng.close()
+
+
+def test_tensor_parallel_path_bit_exact_at_world_1():
+    """The TP plumbing (row-parallel outputs -> NCCL all-reduce -> residual add)
+    on one GPU: a 1-rank communicator must reproduce the fused path bit for bit."""
+    base = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=2)
+    tp = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=2, tp_force=True)
+    try:
+        inputs = M.synthetic_inputs(M.TINY_ALPAMAYO, seed=4)
+        pl = ls.Placement.of({"vlm": [1], "expert": [0]})
+        a = base.execute(pl, inputs=inputs, want_logits=True, record_timeline=False)
+        b = tp.execute(pl, inputs=inputs, want_logits=True, record_timeline=False)
+        assert torch.equal(a.logits, b.logits) and torch.equal(a.tokens, b.tokens)
+        assert torch.equal(a.actions, b.actions)
+        assert tp.memory()["overhead"] > base.memory()["overhead"]  # tp_buf is accounted
+    finally:
+        base.close()
+        tp.close()
