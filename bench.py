@@ -201,7 +201,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="alpamayo-r1-10b-shape")
-    ap.add_argument("--vram-cap-mb", type=float, default=16000.0)
+    ap.add_argument("--vram-cap-mb", type=float, default=None,
+                    help="emulated per-GPU VRAM cap (default 16000; 12000 per GPU under --tp, config 5)")
+    ap.add_argument("--tp", action="store_true",
+                    help="N>1: tensor-parallel shards of every layer (per-GPU PCIe fetch + NCCL "
+                         "all-reduce) instead of independent replicas")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-prefetch", action="store_true",
@@ -229,10 +233,26 @@ def main():
     peaks, peaks_src = _peaks()
 
     h2d_peak = measure_h2d_peak(torch, device)
-    eng = DemandLayeringEngine(cfg, device=local, vram_cap_mb=args.vram_cap_mb, n_slots=2, seed=0)
+    tp = bool(args.tp and world > 1)
+    if args.vram_cap_mb is None:
+        args.vram_cap_mb = 12000.0 if tp else 16000.0
+    tp_id = None
+    if tp:
+        from paper_2605_11678_b200.engine import nccl_unique_id
+        idt = torch.zeros(128, dtype=torch.uint8, device=device)
+        if rank == 0:
+            idt.copy_(torch.tensor(list(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        tp_id = bytes(idt.cpu().tolist())
+    eng = DemandLayeringEngine(cfg, device=local, vram_cap_mb=args.vram_cap_mb, n_slots=2, seed=0,
+                               tp_world=world if tp else 1, tp_rank=rank if tp else 0, tp_id=tp_id)
     sim_cfg = ls.SimConfig(cross_invocation_prefetch=not args.no_prefetch)
     prof = eng.profile_run(iterations=args.profile_iters, warmup=1, config=sim_cfg)
     plan = ls.plan_for_budget(prof, prof.hardware.vram_mb, sim_cfg, include_simulated=True)
+    if dist:  # every rank executes rank 0's plan (identical collective sequence, one schedule)
+        box = [plan]
+        dist.broadcast_object_list(box, 0)
+        plan = box[0]
     placement = plan.placement
 
     # one timeline-recorded pipelined run at the plan: H2D and decode-layer HBM rates
@@ -241,7 +261,7 @@ def main():
     tl = tl_run.timeline
     dma_rates, eff_rates, dec_rates = [], [], []
     kinds = {M.MODULE_NAMES[k]: k for k in cfg.kinds}
-    kv_bytes_tok = 2 * cfg.lm_hkv * cfg.lm_hd * 2
+    kv_bytes_tok = 2 * eng.cfg.lm_hkv * eng.cfg.lm_hd * 2  # this rank's KV heads
     for e in tl.events:
         dur = e.end_ms - e.start_ms
         if dur <= 0:
@@ -340,7 +360,8 @@ def main():
                    "placement": plan.resident_count_per_module,
                    "sim_config": {"mode": sim_cfg.mode.value, "slot_count": sim_cfg.slot_count,
                                   "cross_invocation_prefetch": sim_cfg.cross_invocation_prefetch},
-                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+                   "parallelism": (f"tp{world}" if tp else f"replicas{world}") if world > 1
+                   else "single-gpu",
                    "l2": "inputs larger than L2 (21 GB streamed + resident weights per step)"},
         "e2e": {"value": statistics.fmean(e2e_ms) / 1e3, "unit": "s",
                 "h2d_bytes_per_step": h2d_io, "d2h_bytes_per_step": d2h_io,
