@@ -879,7 +879,8 @@ int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* hos
     if (n != m.layers) return set_error(LS_ERR_VALUE, "expected %d host layers, got %d", m.layers, n);
     uint64_t worst = 0;
     for (int i = 0; i < n; ++i) worst = std::max<uint64_t>(worst, bytes[i]);
-    if (align_up(m.lay.total, 256) + worst + 256 > e->slot_bytes)
+    // the decoder writes whole 1024-word units: up to 2046 bytes past the layer
+    if (align_up(m.lay.total + 2048, 256) + worst + 256 > e->slot_bytes)
       return set_error(LS_ERR_VALUE,
                        "compressed staging does not fit in a DFB slot (layer %llu + blob %llu > "
                        "slot %llu bytes)",

@@ -185,7 +185,7 @@ class DemandLayeringEngine:
             self.arenas[kind] = arena
             ptrs = (C.c_void_p * n)()
             # ECF only where layer + blob fit one DFB slot (no change to VRAM accounting)
-            want_ecf = self.use_ecf and _a256(lay.total) + int(0.8 * lay.total) + 256 <= slot
+            want_ecf = self.use_ecf and _a256(lay.total + 2048) + int(0.75 * lay.total) + 256 <= slot
             blobs = []
             for layer in range(n):
                 t = M.layer_tensors(self.full_cfg, kind, layer, self.seed, self.dev)
@@ -201,7 +201,7 @@ class DemandLayeringEngine:
                 del t, buf
             _native.check(self.lib.ls_exec_set_host_layers(self.handle, kind, ptrs, n), RuntimeError)
             self.stream_bytes[kind] = [lay.total] * n
-            if blobs and _a256(lay.total) + max(b.numel() for b in blobs) + 256 <= slot:
+            if blobs and _a256(lay.total + 2048) + max(b.numel() for b in blobs) + 256 <= slot:
                 sizes = [b.numel() for b in blobs]
                 strides = [(s + 4095) // 4096 * 4096 for s in sizes]
                 earena = HostArena(sum(strides))
