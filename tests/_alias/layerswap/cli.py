@@ -1,8 +1,3 @@
-"""Test-only stand-in for `layerswap.cli` providing the one helper the
-reference conftest imports (bundled_fixture_dir, cli.py:36-41)."""
-import os
-from pathlib import Path
-
-
-def bundled_fixture_dir() -> Path:
-    return Path(os.environ["LAYERSWAP_REF_FIXTURES"])
+"""Test-only alias of `layerswap.cli` -> paper_2605_11678_b200.cli."""
+from paper_2605_11678_b200.cli import *  # noqa: F401,F403
+from paper_2605_11678_b200.cli import bundled_fixture_dir, main  # noqa: F401
