@@ -236,8 +236,6 @@ struct ls_exec {
       m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
   GemvPlan gp_qkv{}, gp_o{}, gp_gu{}, gp_down{}, gp_head{}, gp_t1{}, gp_t2{};
   bool use_pdl = true, pdl_ok = false;
-  bool use_megakernel = true;     // persistent decode-layer kernel (single GPU)
-  unsigned* grid_bar = nullptr;   // its grid barrier state
   // tensor parallelism: row-parallel outputs go to tp_buf, are summed across
   // ranks by NCCL on the compute stream, then added into the residual stream
   int tp_world = 1, tp_rank = 0;
@@ -434,46 +432,6 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l)
 int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, int pos) {
   const ls_dims& d = e->d;
   auto part = [&](int i) { return w + L.offset[i]; };
-  if (e->use_megakernel && !e->tp_on) {  // one persistent kernel for the whole layer
-    DecodeLayerArgs k{};
-    const GemvPlan* plans[4] = {&e->gp_qkv, &e->gp_o, &e->gp_gu, &e->gp_down};
-    int max_kb = 0;
-    for (int p = 0; p < 4; ++p) {
-      k.w[p] = reinterpret_cast<const uint8_t*>(part(p));
-      k.n_mt[p] = n_mt(plans[p]->n);
-      k.n_kb[p] = n_kb(plans[p]->k);
-      max_kb = std::max(max_kb, k.n_kb[p]);
-      k.max_contrib = std::max(k.max_contrib, plans[p]->max_contrib);
-    }
-    k.stages = decode_layer_stages(max_kb);
-    k.attn_norm = (const bf16*)part(4);
-    k.mlp_norm = (const bf16*)part(5);
-    k.eps = d.lm_eps;
-    k.hq = d.lm_hq;
-    k.hkv = d.lm_hkv;
-    k.hd = d.lm_hd;
-    k.pos = pos;
-    k.ffn = d.lm_ffn;
-    k.qn_w = (const bf16*)part(6);
-    k.kn_w = (const bf16*)part(7);
-    k.rope = (const float2*)e->g[3];
-    k.k_cache = e->kc(l);
-    k.v_cache = e->vc(l);
-    k.cache_head_stride = e->cache_stride();
-    k.h = e->dec_h;
-    k.q = e->dec_q;
-    k.attn = e->dec_attn;
-    k.mlp = e->dec_mlp;
-    k.ws = e->gemv_ws;
-    k.counters = e->gemv_cnt;
-    k.attn_ws = e->attn_ws;
-    k.attn_cnt = e->attn_cnt;
-    k.n_split = decode_attn_splits(pos + 1);
-    k.scale = 1.0f / std::sqrt(static_cast<float>(d.lm_hd));
-    k.barrier = e->grid_bar;
-    KL(launch_decode_layer(k, e->nsm, e->ss));
-    return LS_OK;
-  }
   GemvArgs q{};
   q.hq = d.lm_hq;
   q.hkv = d.lm_hkv;
@@ -727,7 +685,6 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     e->n_split = decode_attn_splits(e->ctx + 1);
     OV(attn_ws, 4ull * d.lm_hq * e->n_split * (d.lm_hd + 2));
     OV(attn_cnt, 4ull * d.lm_hkv);
-    OV(grid_bar, 64);
     e->gp_qkv = plan_gemv(QN, d.lm_d, e->nsm);
     e->gp_o = plan_gemv(d.lm_d, AH, e->nsm);
     e->gp_gu = plan_gemv(2 * d.lm_ffn, d.lm_d, e->nsm);

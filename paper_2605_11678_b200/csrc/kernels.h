@@ -51,37 +51,6 @@ int gemv_max_contrib(int n_mt, int n_kb, int grid);
 int gemv_grid(int n_mt, int n_kb, int num_sms);
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st);
 
-// ---------------- persistent decode layer (QKV -> attention -> O -> gate|up -> down) --
-struct DecodeLayerArgs {
-  const uint8_t* w[4];     // tiled qkv, o, gate|up, down
-  int n_mt[4], n_kb[4];
-  int stages;              // ring depth (decode_layer_stages)
-  const bf16* attn_norm;
-  const bf16* mlp_norm;
-  float eps;
-  int hq, hkv, hd, pos, ffn;
-  const bf16* qn_w;
-  const bf16* kn_w;
-  const float2* rope;
-  bf16* k_cache;
-  bf16* v_cache;
-  int cache_head_stride;
-  float* h;                // fp32 residual stream [d]
-  float* q;                // [hq*hd]
-  float* attn;             // [hq*hd]
-  float* mlp;              // [ffn]
-  float* ws;               // stream-K partials
-  int* counters;
-  int max_contrib;
-  float* attn_ws;          // [hq][n_split][hd+2]
-  int* attn_cnt;           // [hkv]
-  int n_split;
-  float scale;
-  unsigned* barrier;       // grid barrier {count, generation}, zero-initialised once
-};
-int decode_layer_stages(int max_kb);
-cudaError_t launch_decode_layer(const DecodeLayerArgs& a, int num_sms, cudaStream_t st);
-
 // ---------------- tcgen05 GEMM: Y[T x N] = X[T x K] * W^T ---------------------
 enum GemmEpi : int {
   GEMM_BF16 = 0,       // out_bf16 = acc (+bias)
