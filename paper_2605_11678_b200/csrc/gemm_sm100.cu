@@ -28,11 +28,16 @@ struct GemmCfg {
   static constexpr int kABytes = kTileBytes;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kAccCols = BN < 32 ? 32 : BN;     // one accumulator
+  static constexpr int kTmemCols = 2 * kAccCols;         // double-buffered (<= 512)
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes +
-                                  128 * 17 * 4 + (2 * kStages + 2) * 8 + 16;
+                                  128 * 17 * 4 + (2 * kStages + 4) * 8 + 16;
 };
 
+// Persistent: grid = min(#tiles, #SMs); CTA c takes tiles c, c+grid, ...  Tiles
+// are ordered token-tile fastest, so the CTAs working on one weight m-tile at
+// the same time share it through L2 (each weight byte read from HBM ~once).
+// Two TMEM accumulators: the epilogue of tile i overlaps the MMAs of tile i+1.
 template <int BN, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmArgs a) {
@@ -45,22 +50,25 @@ __global__ void __launch_bounds__(192, 1)
   float* stage_f = reinterpret_cast<float*>(sb + Cfg::kStages * Cfg::kBBytes);  // [128][17]
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_f + 128 * 17);
   uint64_t* empty = full + Cfg::kStages;
-  uint64_t* accf = empty + Cfg::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 2);
+  uint64_t* acc_full = empty + Cfg::kStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // token tiles vary fastest: the CTAs sharing one weight m-tile are co-resident,
-  // so each weight byte comes from HBM once and from L2 for the other token tiles
-  const int mt = blockIdx.y, n0 = blockIdx.x * BN;
   const int n_kb = a.n_kb;
+  const int n_nt = (a.T + BN - 1) / BN;
+  const int n_tiles = a.n_mt * n_nt;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+    }
     fence_barrier_init();
     prefetch_tmap(&xmap);
   }
@@ -73,79 +81,108 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
       pdl_wait();  // activations of the previous kernel
-      const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kTileBytes;
-      for (int kb = 0; kb < n_kb; ++kb) {
-        const int s = kb % Cfg::kStages;
-        if (kb >= Cfg::kStages) mbar_wait(&empty[s], ((kb / Cfg::kStages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-        bulk_g2s(sa + s * Cfg::kABytes, wt + static_cast<long>(kb) * kTileBytes, kTileBytes, &full[s]);
-        tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &full[s]);
+      int s = 0;
+      uint32_t round = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int mt = t / n_nt, n0 = (t % n_nt) * BN;
+        const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kTileBytes;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          if (round) mbar_wait(&empty[s], (round - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+          bulk_g2s(sa + s * Cfg::kABytes, wt + static_cast<long>(kb) * kTileBytes, kTileBytes,
+                   &full[s]);
+          tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &full[s]);
+          if (++s == Cfg::kStages) {
+            s = 0;
+            ++round;
+          }
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // ---- single-thread MMA issuer ----
       constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
-      for (int kb = 0; kb < n_kb; ++kb) {
-        const int s = kb % Cfg::kStages;
-        mbar_wait(&full[s], (kb / Cfg::kStages) & 1);
+      int s = 0;
+      uint32_t round = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        if (i >= 2) mbar_wait(&acc_empty[b], ((i >> 1) - 1) & 1);  // epilogue drained buffer b
         tc_fence_after();
-        const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
-        const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
+        const uint32_t acc = tmem + b * Cfg::kAccCols;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[s], round & 1);
+          tc_fence_after();
+          const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
+          const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
 #pragma unroll
-        for (int k = 0; k < kTileCols / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-          umma_bf16(tmem, da + 2ull * k, db + 2ull * k, idesc, (kb | k) ? 1u : 0u);
-        umma_commit(&empty[s]);
+          for (int k = 0; k < kTileCols / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+            umma_bf16(acc, da + 2ull * k, db + 2ull * k, idesc, (kb | k) ? 1u : 0u);
+          umma_commit(&empty[s]);
+          if (++s == Cfg::kStages) {
+            s = 0;
+            ++round;
+          }
+        }
+        umma_commit(&acc_full[b]);
       }
-      umma_commit(accf);
     }
     __syncwarp();
   } else {  // ---- epilogue warps 2..5 ----
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int m = q * 32 + lane;
-    const int f = mt * kTileRows + m;
-    mbar_wait(accf, 0);
-    tc_fence_after();
-    float bias = 0.f;
-    if (f < a.n_valid) {
-      if (a.bias) bias = a.bias[f];
-      else if (a.bias_bf16) bias = bf2f(a.bias_bf16[f]);
-    }
-    const int etid = threadIdx.x - 64;  // 0..127
+    int i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int mt = t / n_nt, n0 = (t % n_nt) * BN;
+      const int f = mt * kTileRows + m;
+      mbar_wait(&acc_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      float bias = 0.f;
+      if (f < a.n_valid) {
+        if (a.bias) bias = a.bias[f];
+        else if (a.bias_bf16) bias = bf2f(a.bias_bf16[f]);
+      }
+      const uint32_t acc = tmem + b * Cfg::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
-      if constexpr (EPI == GEMM_SILU_BF16) {
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(acc + c0, v);
+        if constexpr (EPI == GEMM_SILU_BF16) {
+          named_bar(2, 128);  // previous chunk's readers are done with stage_f
 #pragma unroll
-        for (int i = 0; i < 16; ++i) stage_f[m * 17 + i] = v[i];
-        named_bar(2, 128);
-        if (m < 64) {
-          const int g = mt * 64 + m;
-          bf16* out = static_cast<bf16*>(a.out);
+          for (int j = 0; j < 16; ++j) stage_f[m * 17 + j] = v[j];
+          named_bar(2, 128);
+          if (m < 64) {
+            const int g = mt * 64 + m;
+            bf16* out = static_cast<bf16*>(a.out);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int t = n0 + c0 + i;
-            if (t < a.T && g < a.n_valid)
-              out[static_cast<long>(t) * a.ldo + g] = f2bf(silu(stage_f[m * 17 + i]) * stage_f[(m + 64) * 17 + i]);
+            for (int j = 0; j < 16; ++j) {
+              const int tok = n0 + c0 + j;
+              if (tok < a.T && g < a.n_valid)
+                out[static_cast<long>(tok) * a.ldo + g] =
+                    f2bf(silu(stage_f[m * 17 + j]) * stage_f[(m + 64) * 17 + j]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int tok = n0 + c0 + j;
+            if (tok >= a.T) break;
+            const long o = static_cast<long>(tok) * a.ldo + f;
+            const float y = v[j] + bias;
+            if constexpr (EPI == GEMM_BF16) static_cast<bf16*>(a.out)[o] = f2bf(y);
+            else if constexpr (EPI == GEMM_BF16_GELU) static_cast<bf16*>(a.out)[o] = f2bf(gelu_tanh(y));
+            else if constexpr (EPI == GEMM_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] = y; }
+            else if constexpr (EPI == GEMM_RESID_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] += y; }
           }
         }
-        named_bar(2, 128);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int t = n0 + c0 + i;
-          if (t >= a.T) break;
-          const long o = static_cast<long>(t) * a.ldo + f;
-          const float y = v[i] + bias;
-          if constexpr (EPI == GEMM_BF16) static_cast<bf16*>(a.out)[o] = f2bf(y);
-          else if constexpr (EPI == GEMM_BF16_GELU) static_cast<bf16*>(a.out)[o] = f2bf(gelu_tanh(y));
-          else if constexpr (EPI == GEMM_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] = y; }
-          else if constexpr (EPI == GEMM_RESID_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] += y; }
-        }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
-    (void)etid;
   }
   tc_fence_before();
   __syncthreads();
@@ -168,7 +205,10 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.T + BN - 1) / BN, a.n_mt);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int tiles = a.n_mt * ((a.T + BN - 1) / BN);
+  dim3 grid(tiles < nsm ? tiles : nsm);
   return launch_k(gemm_kernel<BN, EPI>, grid, dim3(192), Cfg::kSmem, st, map, a);
 }
 
