@@ -170,6 +170,16 @@ def gemm_microbench(torch, device, T, n, k, reps=20):
     return {"flops": flops, "ms": ms, "tflops": flops / (ms * 1e9)}
 
 
+def ncu_traffic(kernel_key):
+    """dram read+write bytes per launch of `kernel_key` from the committed ncu
+    capture (profiles/ncu_traffic.json, written from tools/gpu_verify.sh)."""
+    try:
+        ent = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).get(kernel_key)
+        return None if ent is None else ent["bytes"]
+    except Exception:
+        return None
+
+
 def run_reference(args, cfg):
     """Reference arm: the path on the box's host cores (oracle/cpu_baseline.py)."""
     from oracle import cpu_baseline
@@ -375,7 +385,8 @@ def main():
         "lower_bound": {"dfbsim_total_s": sim_bound_s, "measured_over_bound": (ms / 1e3) / sim_bound_s,
                         "note": "dfbsim total of the chosen placement on the measured profile"},
         "roofline": {"bound": "hbm", "achieved": gv["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": gv["gbs"] / peaks["hbm_gbs"], "traffic": None,
+                     "frac": gv["gbs"] / peaks["hbm_gbs"],
+                     "traffic": ncu_traffic(f"gemv_kernel<SILU> gate|up {2 * cfg.lm_ffn}x{cfg.lm_d}"),
                      "kernel": f"gemv_kernel<SILU> gate|up {2 * cfg.lm_ffn}x{cfg.lm_d} bf16 "
                                f"({gv['bytes']} B/launch, {gv['ms'] * 1e3:.1f} us)",
                      "peak_source": peaks_src,
