@@ -380,6 +380,7 @@ def main():
                 "frac": (h2d_streamed / h2d_peak) if h2d_streamed else None,
                 "effective_weight_gbs": statistics.fmean(eff_rates) if eff_rates else None,
                 "ecf_modules": [M.MODULE_NAMES[k] for k in eng.ecf_kinds],
+                "compact_modules": [M.MODULE_NAMES[k] for k in eng.ct_kinds],
                 "peak_source": "measured on this box: pinned 1 GiB cudaMemcpyAsync, best of 5"},
         "predictor": pred,
         "lower_bound": {"dfbsim_total_s": sim_bound_s, "measured_over_bound": (ms / 1e3) / sim_bound_s,

@@ -244,6 +244,13 @@ int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_pt
  * unchanged (slots = slot_count x largest layer, dfbsim.py:266). */
 int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* host_ptrs,
                                 const uint64_t* bytes, int32_t n);
+/* ECT-compressed host blobs (exponent-coded tiles, ect.py) of one module: the
+   module is then stored compact everywhere -- DFB slots and resident blocks
+   hold blobs (resident footprint = largest blob, 256-aligned), and every EXE
+   decodes the blob before the layer's kernels.  Re-lays out the slot ring and
+   drops resident layers (call ls_exec_set_placement afterwards). */
+int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host_ptrs,
+                               const uint64_t* bytes, int32_t n);
 /* Upload resident layers for a placement mask (module order vit, lm, expert). */
 int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n);
 /* out: cap, used, high_water, slots, always_resident, overhead, resident (bytes) */
@@ -286,9 +293,21 @@ int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream);
 int ls_k_gemm(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, const void* x,
               int32_t T, int64_t ldx, void* out, int64_t ldo, const float* bias,
               const void* bias_bf16, int32_t n_valid, void* stream);
+/* Same with a split-K workspace (fp32 partials + self-cleaning tile counters):
+   skinny GEMMs (few 128-feature tiles) split K across CTAs, deterministic
+   reduction in split order.  ls_gemm_splits: the split factor it will use. */
+int ls_k_gemm_ws(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, const void* x,
+                 int32_t T, int64_t ldx, void* out, int64_t ldo, const float* bias,
+                 const void* bias_bf16, int32_t n_valid, float* sk_ws, int64_t sk_ws_floats,
+                 int32_t* sk_cnt, int32_t sk_cnt_n, void* stream);
+int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64_t ws_floats,
+                   int32_t cnt_n);
 int ls_k_decode_attention(const void* args, void* stream);
 /* Lossless exponent-coded BF16 (ECF) blob -> BF16 words (decode + exception patch). */
 int ls_k_ecf_decode(const void* blob, void* out, void* stream);
+/* Exponent-coded-tiles (ECT) blob -> plain packed layer (tiles + vectors).
+   out must hold the plain size rounded up to 16 bytes. */
+int ls_k_ect_decode(const void* blob, void* out, void* stream);
 int ls_k_flash_attention(const void* args, void* stream);
 int ls_k_rmsnorm_rows(const float* x, const void* w, void* out, int32_t T, int32_t D, float eps,
                       void* stream);

@@ -66,20 +66,26 @@ def build(verbose: bool = False) -> Path:
     nvcc = _nvcc()
     cuda_inc = str(_cuda_home() / "include")
     objs: list[Path] = []
+    jobs: list[tuple[str, list[str]]] = []
     for src in sorted(CSRC.glob("*.cpp")):
         obj = OBJ_DIR / (src.stem + ".cpp.o")
         if _stale(obj, [src] + headers):
-            if verbose:
-                print("[build] g++", src.name)
-            _run(["g++", *CXXFLAGS, "-I", str(INCLUDE), "-I", cuda_inc, "-c", str(src), "-o", str(obj)])
+            jobs.append((f"g++ {src.name}", ["g++", *CXXFLAGS, "-I", str(INCLUDE), "-I", cuda_inc,
+                                              "-c", str(src), "-o", str(obj)]))
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cu")):
         obj = OBJ_DIR / (src.stem + ".cu.o")
         if _stale(obj, [src] + headers):
-            if verbose:
-                print("[build] nvcc", src.name)
-            _run([nvcc, *NVCCFLAGS, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(src), "-o", str(obj)])
+            jobs.append((f"nvcc {src.name}", [nvcc, *NVCCFLAGS, "-I", str(INCLUDE), "-I", str(CSRC),
+                                               "-c", str(src), "-o", str(obj)]))
         objs.append(obj)
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+        if verbose:
+            for name, _ in jobs:
+                print("[build]", name)
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
+            list(pool.map(lambda j: _run(j[1]), jobs))
     if _stale(LIB, objs):
         if verbose:
             print("[build] link", LIB.name)

@@ -20,20 +20,25 @@ namespace lsb {
 // positions of one KV head: its K and V rows are contiguous in the cache, so
 // two 1-D bulk copies (TMA engine) land them in shared memory with a single
 // mbarrier wait -- one memory latency per CTA instead of one per position.
-// The GQA group's G query heads stay in registers; per-CTA partials
-// (max, sum, O) are merged by the last CTA of the head in split order.
+// Scores: one thread per (query head, position) dot product, K rows read with
+// a per-lane rotation (conflict-free); softmax per head by one warp; P.V: one
+// thread per (head, dim pair).  No cross-lane reductions in the inner loops.
+// Per-CTA partials (max, sum, O) are merged by the last CTA of the head in
+// split order (deterministic).
 
 constexpr int kDecChunk = 64;
 
 template <int HD, int G>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a) {
-  constexpr int E = HD / 32;  // elements per lane
+  constexpr int HP = HD / 2;  // bf16 pairs per row
   extern __shared__ __align__(16) uint8_t dsm[];
   bf16* ks = reinterpret_cast<bf16*>(dsm);
   bf16* vs = ks + kDecChunk * HD;
-  float* comb = reinterpret_cast<float*>(vs + kDecChunk * HD);  // combine scratch
+  float* qs = reinterpret_cast<float*>(vs + kDecChunk * HD);  // [G][HD], pre-scaled
+  float* ps = qs + G * HD;                                     // [G][kDecChunk] scores -> probs
+  float* comb = ps + G * kDecChunk;                            // combine scratch
   __shared__ __align__(8) uint64_t bar;
-  __shared__ float sm_m[4][G], sm_l[4][G];
+  __shared__ float sm_m[G], sm_l[G];
   __shared__ int s_last;
   pdl_trigger();
   const int kh = blockIdx.x, split = blockIdx.y;
@@ -55,75 +60,75 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
     bulk_g2s(vs, a.v_cache + off, bytes, &bar);
   }
   const float sl2 = a.scale * 1.4426950408889634f;
-  float qv[G][E];
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int e = 0; e < E; ++e) qv[g][e] = a.q[(kh * G + g) * HD + lane * E + e] * sl2;
-  float m[G], l[G], acc[G][E];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m[g] = -INFINITY;
-    l[g] = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[g][e] = 0.f;
-  }
-  if (np > 0) mbar_wait(&bar, 0);
-  for (int j = warp; j < np; j += 4) {
-    float kv[E], vv[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      kv[e] = bf2f(ks[j * HD + lane * E + e]);
-      vv[e] = bf2f(vs[j * HD + lane * E + e]);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float sc = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) sc = fmaf(qv[g][e], kv[e], sc);
-      sc = warp_sum(sc);
-      const float mn = fmaxf(m[g], sc);
-      const float corr = exp2f(m[g] - mn), pe = exp2f(sc - mn);
-      l[g] = l[g] * corr + pe;
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[g][e] = acc[g][e] * corr + pe * vv[e];
-      m[g] = mn;
-    }
-  }
-  // ---- merge the 4 warps (shared memory) ----
-  float* sm_o = comb;  // [4][G][HD]
-  if (lane == 0)
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      sm_m[warp][g] = m[g];
-      sm_l[warp][g] = l[g];
-    }
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int e = 0; e < E; ++e) sm_o[(warp * G + g) * HD + lane * E + e] = acc[g][e];
+  for (int i = threadIdx.x; i < G * HD; i += 128) qs[i] = a.q[kh * G * HD + i] * sl2;
   __syncthreads();
-  const int W = HD + 2;  // workspace record: M, L, O[HD]
-  for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-    const int g = idx / HD, d = idx % HD;
-    float M = -INFINITY;
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][g]);
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY)
-      for (int w = 0; w < 4; ++w) {
-        const float f = exp2f(sm_m[w][g] - M);
-        L += sm_l[w][g] * f;
-        O += sm_o[(w * G + g) * HD + d] * f;
+  if (np > 0) mbar_wait(&bar, 0);
+  // ---- scores (log2 domain) ----
+  for (int idx = threadIdx.x; idx < G * kDecChunk; idx += 128) {
+    const int g = idx / kDecChunk, p = idx % kDecChunk;
+    float sc = -INFINITY;
+    if (p < np) {
+      const uint32_t* kr = reinterpret_cast<const uint32_t*>(ks + p * HD);
+      const float2* qg = reinterpret_cast<const float2*>(qs + g * HD);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+      for (int j = 0; j < HP; ++j) {
+        const int jj = (j + p) & (HP - 1);  // rotate: lanes hit distinct banks
+        const uint32_t kv = kr[jj];
+        const float2 qv = qg[jj];
+        s0 = fmaf(bf16_lo(kv), qv.x, s0);
+        s1 = fmaf(bf16_hi(kv), qv.y, s1);
       }
+      sc = s0 + s1;
+    }
+    ps[idx] = sc;
+  }
+  __syncthreads();
+  // ---- softmax per head: warp g (g < G, strided) ----
+  for (int g = warp; g < G; g += 4) {
+    float mx = -INFINITY;
+    for (int p = lane; p < kDecChunk; p += 32) mx = fmaxf(mx, ps[g * kDecChunk + p]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int p = lane; p < kDecChunk; p += 32) {
+      const float v = ps[g * kDecChunk + p];
+      const float e = v == -INFINITY ? 0.f : exp2f(v - mx);
+      ps[g * kDecChunk + p] = e;
+      sum += e;
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) {
+      sm_m[g] = mx;
+      sm_l[g] = sum;
+    }
+  }
+  __syncthreads();
+  // ---- O = P V: one thread per (head, dim pair) ----
+  const int W = HD + 2;  // workspace record: M, L, O[HD]
+  for (int idx = threadIdx.x; idx < G * HP; idx += 128) {
+    const int g = idx / HP, dp = idx % HP;
+    const uint32_t* vc = reinterpret_cast<const uint32_t*>(vs) + dp;
+    const float* pg = ps + g * kDecChunk;
+    float o0 = 0.f, o1 = 0.f;
+#pragma unroll 8
+    for (int p = 0; p < np; ++p) {
+      const uint32_t v = vc[p * HP];
+      const float w = pg[p];
+      o0 = fmaf(w, bf16_lo(v), o0);
+      o1 = fmaf(w, bf16_hi(v), o1);
+    }
     const int h = kh * G + g;
     if (a.n_split == 1) {
-      a.out[h * HD + d] = O / L;
+      const float inv = sm_l[g] > 0.f ? 1.0f / sm_l[g] : 0.f;
+      a.out[h * HD + 2 * dp] = o0 * inv;
+      a.out[h * HD + 2 * dp + 1] = o1 * inv;
     } else {
       float* rec = a.ws + (static_cast<long>(h) * a.n_split + split) * W;
-      rec[2 + d] = O;
-      if (d == 0) {
-        rec[0] = M;
-        rec[1] = L;
+      rec[2 + 2 * dp] = o0;
+      rec[3 + 2 * dp] = o1;
+      if (dp == 0) {
+        rec[0] = sm_m[g];
+        rec[1] = sm_l[g];
       }
     }
   }
@@ -162,8 +167,8 @@ int decode_attn_splits(int n_ctx) { return (n_ctx + kDecChunk - 1) / kDecChunk; 
 
 template <int HD, int G>
 static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
-  const size_t kv = 2ull * kDecChunk * HD * 2;
-  const size_t comb = 4ull * std::max<size_t>(4ull * G * HD, static_cast<size_t>(G) * a.n_split * (HD + 2));
+  const size_t kv = 2ull * kDecChunk * HD * 2 + 4ull * G * (HD + kDecChunk);
+  const size_t comb = 4ull * static_cast<size_t>(G) * a.n_split * (HD + 2);
   const size_t smem = kv + comb;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   static bool attr = false;
@@ -198,21 +203,6 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------- flash ----------------------------------------
-
-__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                               uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ void ldsm_x2_trans(uint32_t& r0, uint32_t& r1, const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
-               : "=r"(r0), "=r"(r1)
-               : "r"(smem_u32(p)));
-}
 
 template <int HD>
 struct FlashCfg {
@@ -275,6 +265,14 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
     k_end = min(n_keys, k_begin + a.seg_len);
   }
   if (a.causal) k_end = min(k_end, q0 + BM + a.q_offset);
+  const int splits = a.kv_splits > 1 ? a.kv_splits : 1;
+  if (splits > 1) {  // this CTA's contiguous share of the key blocks
+    const int nblk = (k_end - k_begin + BN - 1) / BN;
+    const int per = (nblk + splits - 1) / splits;
+    const int b0 = k_begin + static_cast<int>(blockIdx.z) * per * BN;
+    k_end = min(k_end, b0 + per * BN);
+    k_begin = b0;
+  }
 
   for (int j0 = k_begin; j0 < k_end; j0 += BN) {
     __syncthreads();
@@ -369,6 +367,65 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
       }
     }
   }
+  if (splits > 1) {
+    // ---- partial (o unnormalised, m, l) -> workspace; last CTA merges ----
+    constexpr int W = HD + 2;
+    const int unit = blockIdx.x * a.hq + h;
+    float* rec = a.ws + (static_cast<long>(unit) * splits + blockIdx.z) * BM * W;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = warp * 16 + g + 8 * r;
+#pragma unroll
+      for (int dt = 0; dt < ND; ++dt) {
+        rec[row * W + dt * 8 + 2 * t4] = o[dt][2 * r];
+        rec[row * W + dt * 8 + 2 * t4 + 1] = o[dt][2 * r + 1];
+      }
+      if (t4 == 0) {
+        rec[row * W + HD] = mrow[r];
+        rec[row * W + HD + 1] = lrow[r];
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[unit], 1) == splits - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    float* mscale = reinterpret_cast<float*>(fsm);  // [BM][splits] weights, then [BM] 1/L
+    const float* base = a.ws + static_cast<long>(unit) * splits * BM * W;
+    for (int row = threadIdx.x; row < BM; row += 128) {
+      float M = -INFINITY;
+      for (int z = 0; z < splits; ++z) M = fmaxf(M, __ldcg(base + (static_cast<long>(z) * BM + row) * W + HD));
+      float L = 0.f;
+      for (int z = 0; z < splits; ++z) {
+        const float* rz = base + (static_cast<long>(z) * BM + row) * W;
+        const float mz = __ldcg(rz + HD);
+        const float wz = mz == -INFINITY ? 0.f : exp2f(mz - M);
+        mscale[row * splits + z] = wz;
+        L = fmaf(__ldcg(rz + HD + 1), wz, L);
+      }
+      mscale[BM * splits + row] = L > 0.f ? 1.0f / L : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < BM * (HD / 2); i += 128) {
+      const int row = i / (HD / 2), d = 2 * (i % (HD / 2));
+      const int qrow = q0 + row;
+      if (qrow >= a.Tq) continue;
+      float v0 = 0.f, v1 = 0.f;
+      for (int z = 0; z < splits; ++z) {
+        const float* rz = base + (static_cast<long>(z) * BM + row) * W + d;
+        const float wz = mscale[row * splits + z];
+        v0 = fmaf(__ldcg(rz), wz, v0);
+        v1 = fmaf(__ldcg(rz + 1), wz, v1);
+      }
+      const float inv = mscale[BM * splits + row];
+      bf16* op = a.out + static_cast<long>(qrow) * a.o_tok_stride + static_cast<long>(h) * a.o_head_stride;
+      *reinterpret_cast<uint32_t*>(op + d) = pack_bf16x2(v0 * inv, v1 * inv);
+    }
+    if (threadIdx.x == 0) a.counters[unit] = 0;
+    return;
+  }
   // normalise + store
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -393,8 +450,24 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq);
+  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq, a.kv_splits > 1 ? a.kv_splits : 1);
+  if (a.kv_splits > 1 && (!a.ws || !a.counters || a.seg_len > 0 ||
+                          static_cast<size_t>(Cfg::kBM) * (a.kv_splits + 1) * 4 > smem))
+    return cudaErrorInvalidValue;
   return launch_k(flash_kernel<HD>, grid, dim3(128), smem, st, a);
+}
+
+int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms) {
+  const int units = (Tq + 63) / 64 * hq;
+  const int nblk = (n_keys + 63) / 64;
+  if (units * 2 > num_sms || nblk < 4) return 1;
+  int s = (2 * num_sms + units - 1) / units;  // ~2 CTAs per SM
+  s = s < nblk / 2 ? s : nblk / 2;            // >= 2 key blocks per split
+  return s < 1 ? 1 : s;
+}
+
+long flash_ws_floats(int Tq, int hq, int hd, int kv_splits) {
+  return static_cast<long>((Tq + 63) / 64) * hq * kv_splits * 64 * (hd + 2);
 }
 
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {

@@ -79,12 +79,50 @@ int ls_k_gemm(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void
   return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm");
 }
 
+int ls_k_gemm_ws(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void* x, int32_t T,
+                 int64_t ldx, void* out, int64_t ldo, const float* bias, const void* bias_bf16,
+                 int32_t n_valid, float* sk_ws, int64_t sk_ws_floats, int32_t* sk_cnt,
+                 int32_t sk_cnt_n, void* stream) {
+  CUtensorMap map;
+  int rc = make_tmap_bf16(&map, x, static_cast<uint64_t>(T), static_cast<uint64_t>(n_kb) * 64,
+                          static_cast<uint64_t>(ldx), static_cast<uint32_t>(gemm_block_n(T)));
+  if (rc) return set_error(LS_ERR_CUDA, "ls_k_gemm_ws: cuTensorMapEncodeTiled failed (%d)", rc);
+  GemmArgs a{};
+  a.w = static_cast<const uint8_t*>(w);
+  a.n_mt = n_mt;
+  a.n_kb = n_kb;
+  a.T = T;
+  a.out = out;
+  a.ldo = ldo;
+  a.bias = bias;
+  a.bias_bf16 = static_cast<const bf16*>(bias_bf16);
+  a.n_valid = n_valid;
+  a.sk_ws = sk_ws;
+  a.sk_ws_floats = sk_ws_floats;
+  a.sk_cnt = sk_cnt;
+  a.sk_cnt_n = sk_cnt_n;
+  return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm_ws");
+}
+
+int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64_t ws_floats,
+                   int32_t cnt_n) {
+  return gemm_splits(n_mt, n_kb, T, num_sms, ws_floats, cnt_n);
+}
+
 int ls_k_ecf_decode(const void* blob, void* out, void* stream) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   return cuda_rc(launch_ecf_decode(static_cast<const uint8_t*>(blob), out, nsm,
                                    static_cast<cudaStream_t>(stream)),
                  "ls_k_ecf_decode");
+}
+
+int ls_k_ect_decode(const void* blob, void* out, void* stream) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  return cuda_rc(launch_ect_decode(static_cast<const uint8_t*>(blob), out, nsm,
+                                   static_cast<cudaStream_t>(stream)),
+                 "ls_k_ect_decode");
 }
 
 int ls_k_decode_attention(const void* args, void* stream) {

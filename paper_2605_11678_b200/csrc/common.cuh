@@ -30,6 +30,99 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&t);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- warp-level tensor-core helpers (mma.sync m16n8k16 bf16 -> fp32) -----------
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t& r0, uint32_t& r1, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(p)));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
+// ---- ECT page decode (kernels.h EctHeader) -------------------------------------
+// 8 consecutive words of a page: sm = their sign+mantissa bytes, nib = their
+// 4-bit exponent codes (word k in bits 4k..4k+3), e0p = (e0 << 7) | (e0 << 23).
+// Returns the 8 BF16 words exactly as the plain tile stores them (escapes --
+// code 15 -- get exponent e0 + 15 and must be patched with ect_patch8).
+// Per word pair: PRMT places both sm bytes with their sign bit replicated into
+// the byte above (sign lands on bit 15 / 31), one LOP3 keeps sign + mantissa
+// and ORs the window base, one PRMT lines up the pair's codes, one IMAD adds
+// them into the exponent fields: ~2.4 integer ops per word.
+// prmt.b32 in its default mode: bit 3 of a selector nibble replicates the sign
+// of the selected byte (__byte_perm ignores that bit)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ uint32_t ect_pair(uint32_t sbytes, uint32_t sel_s, uint32_t lo,
+                                             uint32_t hi, uint32_t sel_c, uint32_t e0p) {
+  const uint32_t x = (prmt(sbytes, 0u, sel_s) & 0x807F807Fu) | e0p;
+  return prmt(lo, hi, sel_c) * 128u + x;
+}
+__device__ __forceinline__ uint4 ect_decode8(uint2 sm, uint32_t nib, uint32_t e0p) {
+  const uint32_t lo = nib & 0x0F0F0F0Fu, hi = (nib >> 4) & 0x0F0F0F0Fu;
+  uint4 w;
+  w.x = ect_pair(sm.x, 0x9180u, lo, hi, 0xC480u, e0p);
+  w.y = ect_pair(sm.x, 0xB3A2u, lo, hi, 0xD591u, e0p);
+  w.z = ect_pair(sm.y, 0x9180u, lo, hi, 0xE6A2u, e0p);
+  w.w = ect_pair(sm.y, 0xB3A2u, lo, hi, 0xF7B3u, e0p);
+  return w;
+}
+// ECT pages store words in mma.sync A-fragment order: fragment f = (warp * 4 +
+// kstep) * 32 + lane holds the 8 words lane (g = lane / 4, t4 = lane % 4) of
+// warp `warp` needs for k-step `kstep` of m16n8k16 (rows 16 warp + g [+8],
+// k = 16 kstep + 2 t4 [+1] [+8]), i.e. registers a0..a3 in order.  Page word q
+// -> plain (swizzled) tile word:
+__device__ __forceinline__ uint32_t ect_plain_word(uint32_t q) {
+  const uint32_t f = q >> 3, j = q & 7, w = f >> 7, ks = (f >> 5) & 3, lane = f & 31;
+  const uint32_t r = 16 * w + (lane >> 2) + 8 * ((j >> 1) & 1);
+  const uint32_t k = 16 * ks + 8 * (j >> 2) + 2 * (lane & 3) + (j & 1);
+  return r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7);
+}
+// bit 4k set iff word k's code is 15 (escape)
+__device__ __forceinline__ uint32_t ect_escapes(uint32_t nib) {
+  return nib & (nib >> 1) & (nib >> 2) & (nib >> 3) & 0x11111111u;
+}
+// Slow path: t = ect_escapes(nib) of the chunk starting at page word `word0`;
+// true exponents come from the page's exception list.
+static __device__ __noinline__ uint4 ect_patch8(uint4 w, uint32_t t, uint32_t page, uint32_t word0,
+                                                const uint32_t* exc_off, const uint32_t* exc) {
+  const uint32_t b = exc_off[page], e = exc_off[page + 1];
+  uint32_t v[4] = {w.x, w.y, w.z, w.w};
+  for (int k = 0; k < 8; ++k) {
+    if (!((t >> (4 * k)) & 1u)) continue;
+    uint32_t ex = 0;
+    for (uint32_t i = b; i < e; ++i) {
+      const uint32_t x = exc[i];
+      if ((x >> 8) == word0 + k) {
+        ex = x & 0xFFu;
+        break;
+      }
+    }
+    const int sh = 16 * (k & 1);
+    v[k >> 1] = (v[k >> 1] & ~(0x7F80u << sh)) | ((ex << 7) << sh);
+  }
+  return make_uint4(v[0], v[1], v[2], v[3]);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -55,9 +148,6 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, uint32_t idx) 
   return (static_cast<unsigned long long>(b) << 32) | (0xffffffffu - idx);
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

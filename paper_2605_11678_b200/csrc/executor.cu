@@ -200,6 +200,14 @@ struct Module {
   bool ecf = false;                 // stream ECF-compressed blobs
   std::vector<const char*> host_ecf;
   std::vector<uint64_t> ecf_bytes;
+  // ECT (exponent-coded tiles): the module lives in compact form everywhere --
+  // host arena, DFB slots and resident blocks hold ECT blobs; EXE decodes
+  // (or the decode GEMV reads pages directly)
+  bool ct = false;
+  std::vector<const char*> host_ct;
+  std::vector<uint64_t> ct_bytes;
+  uint64_t ct_stride = 0;  // resident footprint per layer (largest blob, 256-aligned)
+  const char* host_of(int l) const { return ct ? host_ct[l] : host[l]; }
 };
 
 }  // namespace
@@ -219,6 +227,10 @@ struct ls_exec {
   std::vector<Module> mods;
   char* g[LS_N_GLOBAL] = {};
   uint64_t bytes_slots = 0, bytes_always = 0, bytes_overhead = 0, mark = 0;
+  uint64_t mark0 = 0;            // arena offset where the slot ring starts (after overhead)
+  char* scratch = nullptr;       // decoded ECT layer (counted as overhead)
+  bool ct_fused_decode = true;   // LM decode GEMVs read ECT pages (else decode to scratch)
+  uint64_t scratch_bytes = 0;
   int S = 0, ctx = 0, Tv = 0, Te = 0, vit_ffn_pad = 0, n_split = 1;
   // activations
   float *vit_h = nullptr, *lm_h = nullptr, *dec_h = nullptr, *dec_q = nullptr, *dec_attn = nullptr,
@@ -230,7 +242,13 @@ struct ls_exec {
        *lm_q = nullptr, *lm_attn = nullptr, *lm_mlp = nullptr, *kv = nullptr, *ex_norm = nullptr,
        *ex_qkv = nullptr, *ex_q = nullptr, *ex_kv = nullptr, *ex_attn = nullptr, *ex_mlp = nullptr;
   int *text_ids = nullptr, *token = nullptr, *hist = nullptr, *attn_cnt = nullptr,
-      *gemv_cnt = nullptr;
+      *gemv_cnt = nullptr, *flash_cnt = nullptr;
+  float* flash_ws = nullptr;  // split-KV partials of the expert's joint attention
+  float* gemm_ws = nullptr;   // split-K partials of skinny GEMMs (expert, T = 64)
+  int* gemm_cnt = nullptr;
+  long gemm_ws_floats = 0;
+  int gemm_cnt_n = 0;
+  int ex_kv_splits = 1;
   unsigned long long* amax = nullptr;
   CUtensorMap m_patches, m_vit_ln, m_vit_attn, m_vit_fc1, m_merge_in, m_merger_mid, m_lm_norm,
       m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
@@ -300,14 +318,38 @@ int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensor
   a.ldo = ldo;
   a.bias_bf16 = static_cast<const bf16*>(bias_bf16);
   a.n_valid = n_valid < 0 ? n : n_valid;
+  a.sk_ws = e->gemm_ws;
+  a.sk_ws_floats = e->gemm_ws_floats;
+  a.sk_cnt = e->gemm_cnt;
+  a.sk_cnt_n = e->gemm_cnt_n;
   KL(launch_gemm(epi, a, map, e->ss));
   return LS_OK;
 }
 
+// Compact (ECT) view of a layer blob: where part i of the plain layout lives.
+struct CtView {
+  const char* blob = nullptr;  // nullptr: plain layer
+  uint64_t mat = 0, tail = 0;
+  CtView() = default;
+  CtView(const char* b, const ls_layer_layout& L) : blob(b) {
+    mat = L.offset[3] + L.bytes[3];
+    tail = align_up(sizeof(EctHeader) + mat / 16384 * kEctPageBytes, 16);
+  }
+  // matrices (parts 0..3): first page; vectors: raw tail
+  const char* part(const ls_layer_layout& L, int i) const {
+    return i < 4 ? blob + sizeof(EctHeader) + L.offset[i] / 16384 * kEctPageBytes
+                 : blob + tail + (L.offset[i] - mat);
+  }
+  int page0(const ls_layer_layout& L, int i) const { return static_cast<int>(L.offset[i] / 16384); }
+};
+
 int gemv(ls_exec* e, int epi, const GemvPlan& p, const char* w, const float* x, float* out,
-         const void* norm_w, const float* bias = nullptr, int n_valid = -1, GemvArgs* extra = nullptr) {
+         const void* norm_w, const float* bias = nullptr, int n_valid = -1, GemvArgs* extra = nullptr,
+         const char* ct_blob = nullptr, int ct_page0 = 0) {
   GemvArgs a = extra ? *extra : GemvArgs{};
   a.w = reinterpret_cast<const uint8_t*>(w);
+  a.ct_blob = reinterpret_cast<const uint8_t*>(ct_blob);
+  a.ct_page0 = ct_page0;
   a.n_mt = n_mt(p.n);
   a.n_kb = n_kb(p.k);
   a.x = x;
@@ -361,18 +403,17 @@ int resid_gemm(ls_exec* e, const char* w, int n, int k, int T, const CUtensorMap
   return tp_reduce_add(e, dst, static_cast<long>(T) * n);
 }
 
-int resid_gemv(ls_exec* e, const GemvPlan& p, const char* w, const float* x, float* dst) {
-  if (!e->tp_on) return gemv(e, GEMV_RESID, p, w, x, dst, nullptr);
-  RC(gemv(e, GEMV_F32, p, w, x, e->tp_buf, nullptr));
+int resid_gemv(ls_exec* e, const GemvPlan& p, const char* w, const float* x, float* dst,
+               const char* ct_blob = nullptr, int ct_page0 = 0) {
+  if (!e->tp_on) return gemv(e, GEMV_RESID, p, w, x, dst, nullptr, nullptr, -1, nullptr, ct_blob, ct_page0);
+  RC(gemv(e, GEMV_F32, p, w, x, e->tp_buf, nullptr, nullptr, -1, nullptr, ct_blob, ct_page0));
   return tp_reduce_add(e, dst, p.n);
 }
 
 int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L) {
   const ls_dims& d = e->d;
   const int T = e->Tv, D = d.vit_d, H = d.vit_heads * d.vit_hd, F = d.vit_ffn;
-  const bf16* P = reinterpret_cast<const bf16*>(w);
   auto part = [&](int i) { return w + L.offset[i]; };
-  (void)P;
   KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(8), (const bf16*)part(9), e->vit_ln, T, D, D,
                            d.vit_eps, e->ss));
   RC(gemm(e, GEMM_BF16, part(0), 3 * H, D, T, e->m_vit_ln, e->vit_qkv, 3 * H, part(4)));
@@ -429,9 +470,14 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l)
   return LS_OK;
 }
 
-int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, int pos) {
+// ct.blob != nullptr: the layer is an ECT blob and the four GEMVs decode its
+// pages in registers (no decoded copy of the layer is ever written).
+int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, int pos,
+                    const CtView& ct = CtView()) {
   const ls_dims& d = e->d;
-  auto part = [&](int i) { return w + L.offset[i]; };
+  auto part = [&](int i) { return ct.blob ? ct.part(L, i) : w + L.offset[i]; };
+  const char* cb = ct.blob;
+  auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
   GemvArgs q{};
   q.hq = d.lm_hq;
   q.hkv = d.lm_hkv;
@@ -444,7 +490,7 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   q.k_cache = e->kc(l);
   q.v_cache = e->vc(l);
   q.cache_head_stride = e->cache_stride();
-  RC(gemv(e, GEMV_QKV, e->gp_qkv, part(0), e->dec_h, e->dec_q, part(4), nullptr, -1, &q));
+  RC(gemv(e, GEMV_QKV, e->gp_qkv, part(0), e->dec_h, e->dec_q, part(4), nullptr, -1, &q, cb, pg(0)));
   DecodeAttnArgs a{};
   a.q = e->dec_q;
   a.k_cache = e->kc(l);
@@ -460,9 +506,10 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.counters = e->attn_cnt;
   a.n_split = decode_attn_splits(pos + 1);  // <= 64 positions per CTA
   KL(launch_decode_attention(a, e->ss));
-  RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h));
-  RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn));
-  RC(resid_gemv(e, e->gp_down, part(3), e->dec_mlp, e->dec_h));
+  RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h, cb, pg(1)));
+  RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn, nullptr,
+          cb, pg(2)));
+  RC(resid_gemv(e, e->gp_down, part(3), e->dec_mlp, e->dec_h, cb, pg(3)));
   return LS_OK;
 }
 
@@ -495,6 +542,9 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
   f.out = e->ex_attn;
   f.o_tok_stride = AH;
   f.o_head_stride = d.ex_hd;
+  f.kv_splits = e->ex_kv_splits;
+  f.ws = e->flash_ws;
+  f.counters = e->flash_cnt;
   KL(launch_flash_attention(f, e->ss));
   RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h));
   KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
@@ -563,13 +613,54 @@ int post_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* i
   return LS_OK;
 }
 
-int run_layer(ls_exec* e, const Module& m, int phase, int inv, int l, const char* w) {
+int run_layer(ls_exec* e, const Module& m, int phase, int inv, int l, const char* w,
+              const CtView& ct = CtView()) {
   switch (m.kind) {
     case LS_KIND_VIT: return vit_layer(e, w, m.lay);
     case LS_KIND_LM:
-      return phase == 0 ? lm_prefill_layer(e, w, m.lay, l) : lm_decode_layer(e, w, m.lay, l, e->S + inv);
+      return phase == 0 ? lm_prefill_layer(e, w, m.lay, l)
+                        : lm_decode_layer(e, w, m.lay, l, e->S + inv, ct);
     default: return expert_layer(e, w, m.lay, l);
   }
+}
+
+// Slot ring + ECT decode scratch after the fixed allocations.  Slot = the
+// largest staged layer (plain bytes, or the largest ECT blob of a compact
+// module), so the reference's buffer term slots x max(layer_mem) holds with
+// layer_mem = what a resident layer occupies.  Drops resident layers (the
+// next ls_exec_set_placement re-creates them).
+int finalize_layout(ls_exec* e) {
+  e->ar.used = e->mark0;
+  e->bytes_slots = 0;
+  e->slot_bytes = 0;
+  uint64_t scratch = 0;
+  for (auto& m : e->mods) {
+    e->slot_bytes = std::max(e->slot_bytes, m.ct ? m.ct_stride : m.lay.total);
+    if (m.ct) scratch = std::max(scratch, align_up(m.lay.total, 256) + 256);
+    std::fill(m.resident.begin(), m.resident.end(), nullptr);
+  }
+  for (auto& m : e->mods) {
+    if (!m.ecf || m.ct) continue;
+    uint64_t worst = 0;
+    for (uint64_t b : m.ecf_bytes) worst = std::max(worst, b);
+    // the ECF decoder writes whole 1024-word units: up to 2046 bytes past the layer
+    if (align_up(m.lay.total + 2048, 256) + worst + 256 > e->slot_bytes)
+      return set_error(LS_ERR_VALUE,
+                       "compressed staging does not fit in a DFB slot (layer %llu + blob %llu > "
+                       "slot %llu bytes)",
+                       static_cast<unsigned long long>(m.lay.total),
+                       static_cast<unsigned long long>(worst),
+                       static_cast<unsigned long long>(e->slot_bytes));
+  }
+  for (int s = 0; s < e->n_slots; ++s)
+    if (int rc = alloc_into(e, &e->slots[s], e->slot_bytes, &e->bytes_slots)) return rc;
+  e->scratch = nullptr;
+  e->scratch_bytes = 0;
+  if (scratch) {
+    if (int rc = alloc_into(e, &e->scratch, scratch, &e->scratch_bytes)) return rc;
+  }
+  e->mark = e->ar.used;
+  return LS_OK;
 }
 
 }  // namespace
@@ -638,11 +729,10 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
   if (cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&e->ss, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_error(LS_ERR_CUDA, "stream creation failed"));
-  // 1. DFB slot ring
+  // 1. DFB slot ring: events now, buffers in finalize_layout (slot size depends
+  //    on which modules are stored compact)
+  e->slots.assign(static_cast<size_t>(e->n_slots), nullptr);
   for (int s = 0; s < e->n_slots; ++s) {
-    char* p = nullptr;
-    if (int rc = alloc_into(e, &p, e->slot_bytes, &e->bytes_slots)) return fail(rc);
-    e->slots.push_back(p);
     cudaEvent_t a, b;
     cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
@@ -731,6 +821,16 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       OV(actions, 4ull * Te * d.action_dim);
       OV(velocity, 4ull * Te * d.action_dim);
       OV(noise, 4ull * Te * d.action_dim);
+      // split-K partials: one wave of 128 x 64 fp32 units
+      e->gemm_ws_floats = static_cast<long>(e->nsm) * 128 * 64;
+      e->gemm_cnt_n = e->nsm;
+      OV(gemm_ws, 4ull * e->gemm_ws_floats);
+      OV(gemm_cnt, 4ull * e->gemm_cnt_n);
+      e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq, e->ctx + Te, e->nsm);
+      if (e->ex_kv_splits > 1) {
+        OV(flash_ws, 4ull * flash_ws_floats(Te, d.ex_hq, d.ex_hd, e->ex_kv_splits));
+        OV(flash_cnt, 4ull * ((Te + 63) / 64) * d.ex_hq);
+      }
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
     e->tp_world = std::max(1, d.tp_world);
@@ -794,7 +894,8 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
         return fail(rc);
     }
   }
-  e->mark = e->ar.used;
+  e->mark0 = e->ar.used;
+  if (int rc = finalize_layout(e)) return fail(rc);
   cudaEvent_t* evs[] = {&e->inv_done, &e->exe_done};
   for (auto p : evs) cudaEventCreateWithFlags(p, cudaEventDisableTiming);
   cudaEvent_t* tevs[] = {&e->ev_begin, &e->ev_t0, &e->ev_t1, &e->ev_end};
@@ -877,16 +978,7 @@ int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* hos
   for (auto& m : e->mods) {
     if (m.kind != kind) continue;
     if (n != m.layers) return set_error(LS_ERR_VALUE, "expected %d host layers, got %d", m.layers, n);
-    uint64_t worst = 0;
-    for (int i = 0; i < n; ++i) worst = std::max<uint64_t>(worst, bytes[i]);
-    // the decoder writes whole 1024-word units: up to 2046 bytes past the layer
-    if (align_up(m.lay.total + 2048, 256) + worst + 256 > e->slot_bytes)
-      return set_error(LS_ERR_VALUE,
-                       "compressed staging does not fit in a DFB slot (layer %llu + blob %llu > "
-                       "slot %llu bytes)",
-                       static_cast<unsigned long long>(m.lay.total),
-                       static_cast<unsigned long long>(worst),
-                       static_cast<unsigned long long>(e->slot_bytes));
+    if (m.ct) return set_error(LS_ERR_VALUE, "module kind %d is stored as ECT; ECF staging does not apply", kind);
     m.host_ecf.assign(n, nullptr);
     m.ecf_bytes.assign(n, 0);
     for (int i = 0; i < n; ++i) {
@@ -894,7 +986,41 @@ int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* hos
       m.ecf_bytes[i] = bytes[i];
     }
     m.ecf = true;
+    if (int rc = finalize_layout(e)) {
+      m.ecf = false;
+      finalize_layout(e);
+      return rc;
+    }
     return LS_OK;
+  }
+  return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
+}
+
+int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host_ptrs,
+                               const uint64_t* bytes, int32_t n) {
+  for (auto& m : e->mods) {
+    if (m.kind != kind) continue;
+    if (n != m.layers) return set_error(LS_ERR_VALUE, "expected %d host layers, got %d", m.layers, n);
+    CK(cudaStreamSynchronize(e->ss));
+    CK(cudaStreamSynchronize(e->cs));
+    uint64_t worst = 0;
+    for (int i = 0; i < n; ++i) {
+      if (!host_ptrs[i] || bytes[i] < sizeof(EctHeader))
+        return set_error(LS_ERR_VALUE, "ECT blob %d of module kind %d is missing or truncated", i, kind);
+      const EctHeader* h = static_cast<const EctHeader*>(host_ptrs[i]);
+      if (h->magic != 0x31544345u || h->total != m.lay.total ||
+          h->mat_bytes != static_cast<uint64_t>(h->n_pages) * 16384ull)
+        return set_error(LS_ERR_VALUE, "ECT blob %d of module kind %d does not match the layer layout",
+                         i, kind);
+      worst = std::max<uint64_t>(worst, bytes[i]);
+    }
+    m.host_ct.assign(n, nullptr);
+    for (int i = 0; i < n; ++i) m.host_ct[i] = static_cast<const char*>(host_ptrs[i]);
+    m.ct_bytes.assign(bytes, bytes + n);
+    m.ct_stride = align_up(worst, 256);
+    m.ct = true;
+    m.ecf = false;
+    return finalize_layout(e);
   }
   return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
 }
@@ -912,14 +1038,16 @@ int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n) {
     for (int l = 0; l < m.layers; ++l) {
       m.resident[l] = nullptr;
       if (!mask[off + l]) continue;
-      if (!m.host[l]) return set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind);
-      char* p = e->ar.alloc(m.lay.total, 256);
+      if (!m.host_of(l)) return set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind);
+      const uint64_t foot = m.ct ? m.ct_stride : m.lay.total;
+      char* p = e->ar.alloc(foot, 256);
       if (!p)
         return set_error(LS_ERR_CAP,
                          "resident layers exceed the emulated VRAM cap (%llu bytes used of %llu)",
                          static_cast<unsigned long long>(e->ar.used),
                          static_cast<unsigned long long>(e->ar.cap));
-      CK(cudaMemcpyAsync(p, m.host[l], m.lay.total, cudaMemcpyHostToDevice, e->cs));
+      CK(cudaMemcpyAsync(p, m.host_of(l), m.ct ? m.ct_bytes[l] : m.lay.total, cudaMemcpyHostToDevice,
+                         e->cs));
       m.resident[l] = p;
     }
     off += m.layers;
@@ -934,7 +1062,7 @@ int ls_exec_memory(ls_exec* e, uint64_t out[7]) {
   out[2] = e->ar.high;
   out[3] = e->bytes_slots;
   out[4] = e->bytes_always;
-  out[5] = e->bytes_overhead;
+  out[5] = e->bytes_overhead + e->scratch_bytes;
   out[6] = e->ar.used - e->mark;
   return LS_OK;
 }
@@ -963,7 +1091,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
     return set_error(LS_ERR_VALUE, "tensor-parallel executor has no communicator (ls_exec_set_tp)");
   for (auto& m : e->mods)
     for (int l = 0; l < m.layers; ++l)
-      if (!m.resident[l] && !m.host[l])
+      if (!m.resident[l] && !m.host_of(l))
         return set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind);
   // timing event pool
   int64_t need = 0;
@@ -1025,11 +1153,11 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
               pending_barrier = false;
             }
             // ECF: blob lands in the slot's tail, decoded into its head on the compute stream
-            const uint64_t nbytes = m.ecf ? m.ecf_bytes[l] : m.lay.total;
+            const uint64_t nbytes = m.ct ? m.ct_bytes[l] : m.ecf ? m.ecf_bytes[l] : m.lay.total;
             char* dst = m.ecf ? e->slots[slot] + ((e->slot_bytes - nbytes) & ~uint64_t(255))
                               : e->slots[slot];
             if (timing) dma0 = tick(e->cs);
-            CK(cudaMemcpyAsync(dst, m.ecf ? m.host_ecf[l] : m.host[l], nbytes,
+            CK(cudaMemcpyAsync(dst, m.ct ? m.host_ct[l] : m.ecf ? m.host_ecf[l] : m.host[l], nbytes,
                                cudaMemcpyHostToDevice, e->cs));
             ++e->h2d_copies;
             e->h2d_bytes += nbytes;
@@ -1044,7 +1172,18 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             KL(launch_ecf_decode(ecf_src, const_cast<char*>(w), e->nsm, e->ss));
             ++e->launches;  // decode + exception patch
           }
-          RC(run_layer(e, m, ph, inv, l, w));
+          CtView ct;
+          if (m.ct && m.kind == LS_KIND_LM && ph == 1 && e->ct_fused_decode) {
+            ct = CtView(w, m.lay);  // decode GEMVs read the blob's pages directly
+          } else if (m.ct) {
+            // compact layer (slot or resident block) -> plain layer in the scratch;
+            // the next kernel must not start early: its weight producer reads the scratch
+            KL(launch_ect_decode(reinterpret_cast<const uint8_t*>(w), e->scratch, e->nsm, e->ss));
+            ++e->launches;  // decode + exception scatter
+            e->pdl_ok = false;
+            w = e->scratch;
+          }
+          RC(run_layer(e, m, ph, inv, l, w, ct));
           int x1 = timing ? tick(e->ss) : -1;
           if (slot >= 0) {
             SSOP(cudaEventRecord(e->comp_done[slot], e->ss));

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kb = a.n_kb;
   const int n_nt = (a.T + BN - 1) / BN;
-  const int n_tiles = a.n_mt * n_nt;
+  const int ks = a.ks > 1 ? a.ks : 1;
+  const int n_tiles = a.n_mt * n_nt * ks;  // work units: (tile, k-split)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
@@ -84,9 +85,11 @@ __global__ void __launch_bounds__(192, 1)
       int s = 0;
       uint32_t round = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int mt = t / n_nt, n0 = (t % n_nt) * BN;
+        const int tile = t / ks, sp = t % ks;
+        const int mt = tile / n_nt, n0 = (tile % n_nt) * BN;
         const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kTileBytes;
-        for (int kb = 0; kb < n_kb; ++kb) {
+        const int kb1 = (sp + 1) * n_kb / ks;
+        for (int kb = sp * n_kb / ks; kb < kb1; ++kb) {
           if (round) mbar_wait(&empty[s], (round - 1) & 1);
           mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
           bulk_g2s(sa + s * Cfg::kABytes, wt + static_cast<long>(kb) * kTileBytes, kTileBytes,
@@ -111,14 +114,15 @@ __global__ void __launch_bounds__(192, 1)
         if (i >= 2) mbar_wait(&acc_empty[b], ((i >> 1) - 1) & 1);  // epilogue drained buffer b
         tc_fence_after();
         const uint32_t acc = tmem + b * Cfg::kAccCols;
-        for (int kb = 0; kb < n_kb; ++kb) {
+        const int sp = t % ks, kb0 = sp * n_kb / ks, kb1 = (sp + 1) * n_kb / ks;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], round & 1);
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
           const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
 #pragma unroll
           for (int k = 0; k < kTileCols / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-            umma_bf16(acc, da + 2ull * k, db + 2ull * k, idesc, (kb | k) ? 1u : 0u);
+            umma_bf16(acc, da + 2ull * k, db + 2ull * k, idesc, (kb > kb0 || k) ? 1u : 0u);
           umma_commit(&empty[s]);
           if (++s == Cfg::kStages) {
             s = 0;
@@ -133,9 +137,11 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int m = q * 32 + lane;
     int i = 0;
+    __shared__ int sk_last;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int b = i & 1;
-      const int mt = t / n_nt, n0 = (t % n_nt) * BN;
+      const int tile = t / ks, sp = t % ks;
+      const int mt = tile / n_nt, n0 = (tile % n_nt) * BN;
       const int f = mt * kTileRows + m;
       mbar_wait(&acc_full[b], (i >> 1) & 1);
       tc_fence_after();
@@ -144,11 +150,8 @@ __global__ void __launch_bounds__(192, 1)
         if (a.bias) bias = a.bias[f];
         else if (a.bias_bf16) bias = bf2f(a.bias_bf16[f]);
       }
-      const uint32_t acc = tmem + b * Cfg::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(acc + c0, v);
+      // fused epilogue of 16 consecutive tokens n0 + c0 .. (all 128 epilogue threads call it)
+      auto emit = [&](int c0, const float (&v)[16]) {
         if constexpr (EPI == GEMM_SILU_BF16) {
           named_bar(2, 128);  // previous chunk's readers are done with stage_f
 #pragma unroll
@@ -178,10 +181,54 @@ __global__ void __launch_bounds__(192, 1)
             else if constexpr (EPI == GEMM_RESID_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] += y; }
           }
         }
+      };
+      const uint32_t acc = tmem + b * Cfg::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+      if (ks == 1) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(acc + c0, v);
+          emit(c0, v);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        continue;
+      }
+      // ---- split-K: partial -> workspace (token-major, coalesced), last unit reduces ----
+      float* part = a.sk_ws + static_cast<long>(t) * BN * kTileRows;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(acc + c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) part[(c0 + j) * kTileRows + m] = v[j];
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      if (lane == 0) mbar_arrive(&acc_empty[b]);  // TMEM buffer free for the next unit
+      __threadfence();
+      named_bar(3, 128);
+      if (m == 0) sk_last = atomicAdd(&a.sk_cnt[tile], 1) == ks - 1;
+      named_bar(3, 128);
+      const bool last = sk_last;
+      named_bar(3, 128);  // everyone has read sk_last before it is reused
+      if (!last) continue;
+      __threadfence();
+      const float* base = a.sk_ws + static_cast<long>(tile) * ks * BN * kTileRows;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int z = 0; z < ks; ++z) {
+          const float* pz = base + static_cast<long>(z) * BN * kTileRows + c0 * kTileRows + m;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += __ldcg(pz + j * kTileRows);
+        }
+        emit(c0, v);
+      }
+      if (m == 0) a.sk_cnt[tile] = 0;
     }
   }
   tc_fence_before();
@@ -193,6 +240,16 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 int gemm_block_n(int T) { return T <= 64 ? 64 : (T <= 256 ? 128 : 256); }
+
+int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n) {
+  const int bn = gemm_block_n(T);
+  const int tiles = n_mt * ((T + bn - 1) / bn);
+  if (tiles * 2 > num_sms || tiles > cnt_n) return 1;
+  int ks = num_sms / tiles;                 // one wave of units
+  if (ks > n_kb / 4) ks = n_kb / 4;         // >= 4 k-blocks (256 of K) per unit
+  while (ks > 1 && static_cast<long>(tiles) * ks * bn * 128 > ws_floats) --ks;
+  return ks < 1 ? 1 : ks;
+}
 
 template <int BN, int EPI>
 static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
@@ -207,9 +264,11 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  const int tiles = a.n_mt * ((a.T + BN - 1) / BN);
-  dim3 grid(tiles < nsm ? tiles : nsm);
-  return launch_k(gemm_kernel<BN, EPI>, grid, dim3(192), Cfg::kSmem, st, map, a);
+  GemmArgs b = a;
+  b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n) : 1;
+  const int units = a.n_mt * ((a.T + BN - 1) / BN) * b.ks;
+  dim3 grid(units < nsm ? units : nsm);
+  return launch_k(gemm_kernel<BN, EPI>, grid, dim3(192), Cfg::kSmem, st, map, b);
 }
 
 template <int BN>

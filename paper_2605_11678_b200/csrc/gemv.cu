@@ -21,30 +21,42 @@
 
 namespace lsb {
 
-constexpr int kGemvMaxStages = 12;
+constexpr int kGemvMaxStages = 16;
 
-// Ring depth from the shared-memory left after x (fp32, K floats): 12 stages
-// (192 KiB in flight per SM) for K = 4096, 11 for K = 12288.
+// Ring depth from the shared-memory left after x (fp32, K floats): 12 x 16 KiB
+// plain tiles or 16 x 12 KiB ECT pages (192 KiB in flight per SM) for K = 4096.
+template <bool CT>
 __host__ __device__ inline int gemv_stages(int n_kb) {
-  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 1024) / kTileBytes;
-  return avail > kGemvMaxStages ? kGemvMaxStages : avail;
+  constexpr int stage = CT ? kEctPageBytes : kTileBytes;
+  constexpr int cap = CT ? 16 : 12;
+  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 1024) / stage;
+  return avail > cap ? cap : avail;
 }
-constexpr int kGemvConsumers = 256;  // 8 warps
+constexpr int kGemvConsumers = 256;  // 8 warps, 16 rows of every tile each
 constexpr int kGemvThreads = kGemvConsumers + 32;
 
 __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
   return static_cast<int>(((t + 1) * G - 1) / T);
 }
 
-template <int EPI>
+// Consumers run the dot products on the tensor cores: mma.sync m16n8k16 with
+// the weight tile as A (16 rows x 16 k per warp and k-step, fetched by one
+// ldmatrix.x4 from the swizzled tile -- conflict-free -- or decoded straight
+// from an ECT page, which stores words in A-fragment order) and x as B with
+// two live columns, bf16(x) and bf16(x - bf16(x)) (x to ~16 mantissa bits).
+// Per 8 weight words a thread spends ~0.25 instructions instead of 16 FMA +
+// convert ops, which is what lets the ECT decode (~2.5 ops/word) fit under
+// the HBM stream.  Plain and ECT tiles give bit-identical results.
+template <int EPI, bool CT>
 __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int kStage = CT ? kEctPageBytes : kTileBytes;
   const int K = a.n_kb * kTileCols;
   uint8_t* stages = smem;
-  const int NS = gemv_stages(a.n_kb);
-  float* xs = reinterpret_cast<float*>(smem + NS * kTileBytes);
-  float* red = xs + K;
-  float* scratch = red + kTileRows;  // 8 floats for block reductions
+  const int NS = gemv_stages<CT>(a.n_kb);
+  uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NS * kStage);  // [K/2][hi, lo] bf16x2
+  float* red = reinterpret_cast<float*>(xq + K);
+  float* scratch = red + kTileRows;  // 16 floats for block reductions
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
   uint64_t* empty = full + kGemvMaxStages;
   int* flag = reinterpret_cast<int*>(empty + kGemvMaxStages);
@@ -68,14 +80,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       // stage / round counters advance incrementally: no 64-bit div or mod per tile
-      const uint8_t* src = a.w + t0 * kTileBytes;
+      const uint8_t* src = a.w + t0 * kStage;
       int s = 0;
       uint32_t round = 0;
       for (int n = static_cast<int>(t1 - t0); n > 0; --n) {
         if (round) mbar_wait(&empty[s], (round - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], kTileBytes);
-        bulk_g2s_evict_first(stages + s * kTileBytes, src, kTileBytes, &full[s], pol);
-        src += kTileBytes;
+        mbar_arrive_expect_tx(&full[s], kStage);
+        bulk_g2s_evict_first(stages + s * kStage, src, kStage, &full[s], pol);
+        src += kStage;
         if (++s == NS) {
           s = 0;
           ++round;
@@ -86,40 +98,59 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   }
 
   // ---- consumers: x -> shared (fp32), optional fused RMSNorm ----
-  pdl_wait();  // x, workspace and outputs belong to the previous kernel until here
   const int tid = threadIdx.x;
-  float ss = 0.f;
-  for (int k = tid; k < K; k += kGemvConsumers) {
-    float v = a.x[k];
-    xs[k] = v;
-    ss = fmaf(v, v, ss);
+  const uint32_t* exc_off = nullptr;
+  const uint32_t* exc = nullptr;
+  uint32_t e0p = 0;
+  if constexpr (CT) {  // weights are not produced by the previous kernel
+    const EctHeader* h = reinterpret_cast<const EctHeader*>(a.ct_blob);
+    e0p = (h->e0 << 7) | (h->e0 << 23);
+    exc_off = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_excoff) + a.ct_page0;
+    exc = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_exc);
   }
+  pdl_wait();  // x, workspace and outputs belong to the previous kernel until here
+  // fused RMSNorm: sum of squares in a fixed order (threads < 256, stride 256)
+  float rstd = 1.f;
   if (a.norm_w) {
+    float ss = 0.f;
+    for (int k = tid; k < K; k += kGemvConsumers) {
+      const float v = a.x[k];
+      ss = fmaf(v, v, ss);
+    }
     ss = warp_sum(ss);
     if (lane == 0) scratch[warp] = ss;
     named_bar(1, kGemvConsumers);
     float tot = 0.f;
 #pragma unroll
     for (int w = 0; w < kGemvConsumers / 32; ++w) tot += scratch[w];
-    const float rstd = rsqrtf(tot / K + a.eps);
-    for (int k = tid; k < K; k += kGemvConsumers) xs[k] = xs[k] * rstd * bf2f(a.norm_w[k]);
+    rstd = rsqrtf(tot / K + a.eps);
+  }
+  // x -> (hi, lo) bf16 pairs: xq[2i] = {hi[2i], hi[2i+1]}, xq[2i+1] = {lo[2i], lo[2i+1]}
+  for (int i = tid; i < K / 2; i += kGemvConsumers) {
+    float v0 = a.x[2 * i], v1 = a.x[2 * i + 1];
+    if (a.norm_w) {
+      v0 = v0 * rstd * bf2f(a.norm_w[2 * i]);
+      v1 = v1 * rstd * bf2f(a.norm_w[2 * i + 1]);
+    }
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+    const float2 hf = __bfloat1622float2(hi);
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+    xq[2 * i] = *reinterpret_cast<const uint32_t*>(&hi);
+    xq[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&lo);
   }
   named_bar(1, kGemvConsumers);
 
-  const int rr = lane >> 3, ch = lane & 7;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int g = lane >> 2, t4 = lane & 3;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};  // mma C: rows g, g+8 x columns (hi, lo) in lanes t4 == 0
   int cur_mt = t0 < t1 ? static_cast<int>(t0 / a.n_kb) : -1;
 
   auto flush = [&](int mt) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float v = acc[j];
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      if (ch == 0) red[warp * 16 + rr + 4 * j] = v;
-      acc[j] = 0.f;
+    if (t4 == 0) {
+      red[warp * 16 + g] = acc[0] + acc[1];
+      red[warp * 16 + g + 8] = acc[2] + acc[3];
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = 0.f;
     named_bar(1, kGemvConsumers);
     const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
     const int c_first = cta_of_tile(first, G, T);
@@ -154,10 +185,17 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     named_bar(1, kGemvConsumers);
   };
 
+  // B fragment source: column g = 0 -> hi, g = 1 -> lo, other columns zero
+  const uint32_t* xb = xq + (g & 1);
+  const bool bcol = g < 2;
+  // ldmatrix.x4 row address of this lane inside a plain tile (k-step added per use)
+  const int lr = warp * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+  const int lc = lane >> 4;  // 0: k 0-7 of the step, 1: k 8-15
   int kb = t0 < t1 ? static_cast<int>(t0 - static_cast<long>(cur_mt) * a.n_kb) : 0;
   int s = 0;
   uint32_t round = 0;
-  for (int n = static_cast<int>(t1 - t0), mt = cur_mt; n > 0; --n) {
+  uint32_t tile = static_cast<uint32_t>(t0);
+  for (int n = static_cast<int>(t1 - t0), mt = cur_mt; n > 0; --n, ++tile) {
     if (kb == a.n_kb) {
       kb = 0;
       ++mt;
@@ -165,16 +203,28 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       cur_mt = mt;
     }
     mbar_wait(&full[s], round & 1);
-    const uint8_t* st = stages + s * kTileBytes;
-    const float* xk = xs + kb * kTileCols;
-    const float4* xa = reinterpret_cast<const float4*>(xk + ((ch ^ rr) << 3));
-    const float4* xb = reinterpret_cast<const float4*>(xk + ((ch ^ (rr + 4)) << 3));
-    const float4 a0 = xa[0], a1 = xa[1], b0 = xb[0], b1 = xb[1];
+    const uint8_t* st = stages + s * kStage;
+    const uint32_t* xk = xb + kb * kTileCols;  // pair index kb*32 (x2 for hi/lo interleave)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int row = warp * 16 + rr + 4 * j;
-      const uint4 wv = *reinterpret_cast<const uint4*>(st + row * 128 + ch * 16);
-      acc[j] += (j & 1) ? dot8(wv, b0, b1) : dot8(wv, a0, a1);
+    for (int ks = 0; ks < kTileCols / 16; ++ks) {
+      uint32_t af[4];
+      if constexpr (CT) {
+        const int f = (warp * 4 + ks) * 32 + lane;  // this lane's A fragment in the page
+        const uint2 sm = *reinterpret_cast<const uint2*>(st + f * 8);
+        const uint32_t nib = *reinterpret_cast<const uint32_t*>(st + kEctPageWords + f * 4);
+        uint4 wv = ect_decode8(sm, nib, e0p);
+        const uint32_t t = ect_escapes(nib);
+        if (t) wv = ect_patch8(wv, t, tile, f * 8, exc_off, exc);
+        af[0] = wv.x;
+        af[1] = wv.y;
+        af[2] = wv.z;
+        af[3] = wv.w;
+      } else {
+        ldsm_x4(af, st + lr * 128 + (((2 * ks + lc) ^ (lr & 7)) << 4));
+      }
+      const uint32_t b0 = bcol ? xk[2 * (8 * ks + t4)] : 0u;
+      const uint32_t b1 = bcol ? xk[2 * (8 * ks + 4 + t4)] : 0u;
+      mma_bf16_16816(acc, af, b0, b1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -204,33 +254,40 @@ int gemv_max_contrib(int n_mt, int n_kb, int grid) {
   return best;
 }
 
+template <bool CT>
 static size_t gemv_smem(int n_kb) {
-  return static_cast<size_t>(gemv_stages(n_kb)) * kTileBytes + static_cast<size_t>(n_kb) * kTileCols * 4 +
-         kTileRows * 4 + 16 * 4 + 2 * kGemvMaxStages * 8 + 16;
+  return static_cast<size_t>(gemv_stages<CT>(n_kb)) * (CT ? kEctPageBytes : kTileBytes) +
+         static_cast<size_t>(n_kb) * kTileCols * 4 + kTileRows * 4 + 16 * 4 + 2 * kGemvMaxStages * 8 +
+         16;
 }
 
-template <int EPI>
+template <int EPI, bool CT>
 static cudaError_t launch_t(const GemvArgs& a, int grid, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<EPI, CT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_k(gemv_kernel<EPI>, dim3(grid), dim3(kGemvThreads), gemv_smem(a.n_kb), st, a);
+  return launch_k(gemv_kernel<EPI, CT>, dim3(grid), dim3(kGemvThreads), gemv_smem<CT>(a.n_kb), st, a);
+}
+
+template <bool CT>
+static cudaError_t launch_ct(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
+  if (gemv_smem<CT>(a.n_kb) > 227 * 1024) return cudaErrorInvalidValue;
+  switch (epi) {
+    case GEMV_F32: return launch_t<GEMV_F32, CT>(a, grid, st);
+    case GEMV_RESID: return launch_t<GEMV_RESID, CT>(a, grid, st);
+    case GEMV_SILU: return launch_t<GEMV_SILU, CT>(a, grid, st);
+    case GEMV_QKV: return launch_t<GEMV_QKV, CT>(a, grid, st);
+    case GEMV_ARGMAX: return launch_t<GEMV_ARGMAX, CT>(a, grid, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
-  if (gemv_smem(a.n_kb) > 227 * 1024) return cudaErrorInvalidValue;
-  switch (epi) {
-    case GEMV_F32: return launch_t<GEMV_F32>(a, grid, st);
-    case GEMV_RESID: return launch_t<GEMV_RESID>(a, grid, st);
-    case GEMV_SILU: return launch_t<GEMV_SILU>(a, grid, st);
-    case GEMV_QKV: return launch_t<GEMV_QKV>(a, grid, st);
-    case GEMV_ARGMAX: return launch_t<GEMV_ARGMAX>(a, grid, st);
-  }
-  return cudaErrorInvalidValue;
+  return a.ct_blob ? launch_ct<true>(epi, a, grid, st) : launch_ct<false>(epi, a, grid, st);
 }
 
 }  // namespace lsb

@@ -45,6 +45,11 @@ struct GemvArgs {
   bf16* v_cache;
   int cache_head_stride;   // max_ctx * hd
   unsigned long long* amax;  // ARGMAX packed key
+  // ECT (compact) weights: w points at this matrix's first 12 KiB page inside
+  // the blob whose header is ct_blob; tile t of the matrix is page ct_page0 + t.
+  // nullptr: plain 16 KiB tiles.
+  const uint8_t* ct_blob;
+  int ct_page0;
 };
 
 int gemv_max_contrib(int n_mt, int n_kb, int grid);
@@ -70,9 +75,19 @@ struct GemmArgs {
   const float* bias;  // per output feature (optional)
   const bf16* bias_bf16;  // alternative bf16 bias (optional)
   int n_valid;        // features < n_valid are real (bias / store guard)
+  // split-K for skinny GEMMs (few output tiles, e.g. the 64-token expert):
+  // each (tile, k-range) unit stores fp32 partials; the last unit of a tile
+  // sums them in split order and runs the epilogue.  sk_ws == nullptr: off.
+  float* sk_ws;       // partials [tiles * ks][BN tokens][128 features]
+  long sk_ws_floats;  // capacity
+  int* sk_cnt;        // [tiles] arrival counters, zero between launches
+  int sk_cnt_n;
+  int ks;             // set by launch_gemm (callers leave 0)
 };
 
 int gemm_block_n(int T);
+// split factor launch_gemm picks for a shape (1 = no split)
+int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n);
 cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st);
 // Encode a row-major bf16 [rows x cols] tensor map with box {64, box_rows}, SWIZZLE_128B.
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -105,8 +120,18 @@ struct FlashArgs {
   int q_offset;
   int seg_len;     // >0: block-diagonal attention over segments of seg_len tokens (ViT images)
   float scale;
+  // split-KV (few query tiles, long KV: the 64-token expert over the LM cache):
+  // grid.z = kv_splits CTAs per (q tile, head) each reduce a contiguous key
+  // range; the last to finish merges the partials in split order.
+  int kv_splits;   // <= 1: off
+  float* ws;       // [q_tiles * hq * kv_splits][64][hd + 2]
+  int* counters;   // [q_tiles * hq], zero between launches (self-cleaning)
 };
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st);
+// kv_splits the launcher will use for (Tq, hq, keys) given num_sms, and the
+// workspace floats / counters it then needs
+int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms);
+long flash_ws_floats(int Tq, int hq, int hd, int kv_splits);
 
 // ---------------- elementwise / norms ------------------------------------------
 cudaError_t launch_rmsnorm_rows(const float* x, const bf16* w, bf16* out, int T, int D, float eps,
@@ -156,5 +181,28 @@ struct EcfHeader {
 static_assert(sizeof(EcfHeader) == 128, "ECF header is 128 bytes");
 // decode + exception patch (two kernels) from a device blob into `out`
 cudaError_t launch_ecf_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st);
+
+// ---------------- ECT: exponent-coded tiles (compact resident / streamed layers) --
+// Fixed-rate: every 16 KiB weight tile (page) is 12 KiB = 8192 sign+mantissa
+// bytes then 4096 bytes of 4-bit exponent codes (word 2i in the low nibble of
+// byte i).  Code c < 15 is exponent e0 + c (codebook[c] = e0 + c); 15 = escape,
+// whose exponent is the low byte of the page's exc entry with (word index <<
+// 8).  ect.py has the format.
+constexpr int kEctPageBytes = 12288;
+constexpr int kEctPageWords = 8192;
+struct EctHeader {
+  uint32_t magic;  // 'ECT1'
+  uint32_t n_pages;
+  uint64_t total;      // plain layer bytes
+  uint64_t mat_bytes;  // = n_pages * 16 KiB (the layer's tiled matrices)
+  uint64_t off_pages, off_tail, off_excoff, off_exc;
+  uint32_t n_exc, e0;
+  uint8_t codebook[16];
+  uint8_t _pad[48];
+};
+static_assert(sizeof(EctHeader) == 128, "ECT header is 128 bytes");
+// blob -> plain layer bytes (whole 16-byte chunks: out needs a16(total) bytes);
+// a decode kernel then an exception scatter (PDL-chained)
+cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st);
 
 }  // namespace lsb

@@ -21,6 +21,7 @@ import torch
 
 from . import _native
 from . import ecf
+from . import ect
 from . import model as M
 from .dfbsim import Engine as EngineKind
 from .dfbsim import Mode, Placement, SimConfig, SimEvent, Timeline
@@ -52,6 +53,8 @@ def _bind():
         "ls_exec_set_host_layers": [vp, C.c_int32, C.POINTER(vp), C.c_int32],
         "ls_exec_set_host_layers_ecf": [vp, C.c_int32, C.POINTER(vp), C.POINTER(C.c_uint64),
                                         C.c_int32],
+        "ls_exec_set_host_layers_ct": [vp, C.c_int32, C.POINTER(vp), C.POINTER(C.c_uint64),
+                                       C.c_int32],
         "ls_exec_set_placement": [vp, C.POINTER(C.c_uint8), C.c_int64],
         "ls_exec_memory": [vp, C.POINTER(C.c_uint64)],
         "ls_exec_streams": [vp, C.POINTER(vp), C.POINTER(vp)],
@@ -107,12 +110,20 @@ class DemandLayeringEngine:
 
     def __init__(self, cfg: M.ModelConfig = M.ALPAMAYO, *, device: int = 0,
                  vram_cap_mb: float = 16000.0, n_slots: int = 2, seed: int = 0,
-                 keep_logical: bool = False, ecf: bool = True, tp_world: int = 1,
+                 keep_logical: bool = False, ecf: bool = True, compact: bool = True,
+                 tp_world: int = 1,
                  tp_rank: int = 0, tp_id: bytes | None = None, tp_force: bool = False) -> None:
         """tp_world > 1: this engine is rank `tp_rank` of a tensor-parallel group;
         it holds and streams only its shard of every layer (model.tp_config /
         shard_layer_tensors) and all-reduces row-parallel outputs with NCCL
-        (`tp_id` = the 128-byte id from `nccl_unique_id()` on rank 0)."""
+        (`tp_id` = the 128-byte id from `nccl_unique_id()` on rank 0).
+
+        compact=True stores every module as ECT blobs (ect.py: exponent-coded
+        tiles, lossless, 75 % of the bytes) in the host arena, the DFB slots
+        and the resident blocks; the profile then reports the compact resident
+        footprint, so the unchanged planner fits ~1/3 more layers under the
+        cap.  compact=False keeps plain layers (ECF-compressed streaming where
+        layer + blob fit a slot, ecf=True)."""
         if not torch.cuda.is_available():
             raise RuntimeError("DemandLayeringEngine needs a CUDA device (B200, sm_100a)")
         self.lib = _bind()
@@ -131,6 +142,7 @@ class DemandLayeringEngine:
         self.n_slots = n_slots
         self.seed = seed
         self.use_ecf = ecf
+        self.use_compact = compact
         torch.cuda.set_device(device)
         self._dims = cfg.dims()
         self.handle = C.c_void_p()
@@ -174,9 +186,16 @@ class DemandLayeringEngine:
         torch.cuda.synchronize()
 
     def _init_layers(self) -> None:
-        slot = max(self.layouts[k].total for k in self.kinds)
         self.stream_bytes = {}
+        self.resident_bytes = {}
         self.ecf_kinds = []
+        self.ct_kinds = []
+        if self.use_compact:
+            for kind in self.kinds:
+                self._init_compact(kind)
+            torch.cuda.synchronize()
+            return
+        slot = max(self.layouts[k].total for k in self.kinds)
         for kind in self.kinds:
             lay = self.layouts[kind]
             n = self.cfg.layers_of(kind)
@@ -188,37 +207,62 @@ class DemandLayeringEngine:
             want_ecf = self.use_ecf and _a256(lay.total + 2048) + int(0.75 * lay.total) + 256 <= slot
             blobs = []
             for layer in range(n):
-                t = M.layer_tensors(self.full_cfg, kind, layer, self.seed, self.dev)
-                shard = M.shard_layer_tensors(self.full_cfg, kind, t, self.tp_world, self.tp_rank)
-                buf = M.pack_layer(self.cfg, kind, shard)
-                del shard
+                buf = self._packed_layer(kind, layer)
                 arena.tensor[layer * stride:layer * stride + lay.total].copy_(buf)
                 ptrs[layer] = arena.ptr.value + layer * stride
                 if want_ecf:
                     blobs.append(ecf.compress(buf))
-                if self.logical is not None:
-                    self.logical["layers"][(kind, layer)] = {k: v.float().cpu() for k, v in t.items()}
-                del t, buf
+                del buf
             _native.check(self.lib.ls_exec_set_host_layers(self.handle, kind, ptrs, n), RuntimeError)
             self.stream_bytes[kind] = [lay.total] * n
+            self.resident_bytes[kind] = _a256(lay.total)
             if blobs and _a256(lay.total + 2048) + max(b.numel() for b in blobs) + 256 <= slot:
                 sizes = [b.numel() for b in blobs]
-                strides = [(s + 4095) // 4096 * 4096 for s in sizes]
-                earena = HostArena(sum(strides))
-                self.arenas[("ecf", kind)] = earena
-                eptrs = (C.c_void_p * n)()
-                nbytes = (C.c_uint64 * n)(*sizes)
-                off = 0
-                for i, b in enumerate(blobs):
-                    earena.tensor[off:off + sizes[i]].copy_(b)
-                    eptrs[i] = earena.ptr.value + off
-                    off += strides[i]
-                _native.check(self.lib.ls_exec_set_host_layers_ecf(self.handle, kind, eptrs, nbytes, n),
-                              RuntimeError)
+                self._blob_arena(("ecf", kind), blobs, self.lib.ls_exec_set_host_layers_ecf, kind)
                 self.stream_bytes[kind] = sizes
                 self.ecf_kinds.append(kind)
             del blobs
         torch.cuda.synchronize()
+
+    def _packed_layer(self, kind: int, layer: int) -> torch.Tensor:
+        """This rank's packed (tiled, flat) bytes of one layer, on the GPU."""
+        t = M.layer_tensors(self.full_cfg, kind, layer, self.seed, self.dev)
+        shard = M.shard_layer_tensors(self.full_cfg, kind, t, self.tp_world, self.tp_rank)
+        buf = M.pack_layer(self.cfg, kind, shard)
+        if self.logical is not None:
+            self.logical["layers"][(kind, layer)] = {k: v.float().cpu() for k, v in t.items()}
+        return buf
+
+    def _blob_arena(self, key, blobs: list, setter, kind: int) -> None:
+        n = len(blobs)
+        sizes = [b.numel() for b in blobs]
+        strides = [(sz + 4095) // 4096 * 4096 for sz in sizes]
+        arena = HostArena(sum(strides))
+        self.arenas[key] = arena
+        ptrs = (C.c_void_p * n)()
+        nbytes = (C.c_uint64 * n)(*sizes)
+        off = 0
+        for i, b in enumerate(blobs):
+            arena.tensor[off:off + sizes[i]].copy_(b)
+            ptrs[i] = arena.ptr.value + off
+            off += strides[i]
+        _native.check(setter(self.handle, kind, ptrs, nbytes, n), RuntimeError)
+
+    def _init_compact(self, kind: int) -> None:
+        lay = self.layouts[kind]
+        mat = lay.offset[3] + lay.bytes[3]  # parts 0..3 are the layer's tiled matrices
+        assert mat % ect.PAGE_PLAIN == 0 and lay.offset[4] >= mat, (kind, mat)
+        blobs = []
+        for layer in range(self.cfg.layers_of(kind)):
+            buf = self._packed_layer(kind, layer)
+            blobs.append(ect.compress(buf, mat))
+            del buf
+        self._blob_arena(("ect", kind), blobs, self.lib.ls_exec_set_host_layers_ct, kind)
+        sizes = [b.numel() for b in blobs]
+        self.stream_bytes[kind] = sizes
+        self.resident_bytes[kind] = _a256(max(sizes))
+        self.ct_kinds.append(kind)
+        del blobs
 
     def close(self) -> None:
         if self.handle:
@@ -383,7 +427,7 @@ class DemandLayeringEngine:
                               * len(samples[(name, ph, "copy")]))
                 dma_ms += sum(samples[(name, ph, "copy")])
             modules.append(ModuleProfile(name=name, layers=self.cfg.layers_of(kind),
-                                         layer_mem_mb=M.layer_mem_mb(self.cfg, kind),
+                                         layer_mem_mb=self.resident_bytes[kind] / MIB,
                                          phases=tuple(phases)))
         calibration = None
         if calibrate:

@@ -22,7 +22,8 @@ class GemvArgs(C.Structure):
                 ("out", _vp), ("bias", _vp), ("n_valid", C.c_int32), ("hq", C.c_int32),
                 ("hkv", C.c_int32), ("hd", C.c_int32), ("pos", C.c_int32), ("qn_w", _vp),
                 ("kn_w", _vp), ("rope", _vp), ("q_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
-                ("cache_head_stride", C.c_int32), ("amax", _vp)]
+                ("cache_head_stride", C.c_int32), ("amax", _vp), ("ct_blob", _vp),
+                ("ct_page0", C.c_int32)]
 
 
 class DecodeAttnArgs(C.Structure):
@@ -41,7 +42,7 @@ class FlashArgs(C.Structure):
                 ("out", _vp), ("o_tok_stride", C.c_int64), ("o_head_stride", C.c_int64),
                 ("Tq", C.c_int32), ("hq", C.c_int32), ("hkv", C.c_int32), ("hd", C.c_int32),
                 ("causal", C.c_int32), ("q_offset", C.c_int32), ("seg_len", C.c_int32),
-                ("scale", C.c_float)]
+                ("scale", C.c_float), ("kv_splits", C.c_int32), ("ws", _vp), ("counters", _vp)]
 
 
 GEMV_F32, GEMV_RESID, GEMV_SILU, GEMV_QKV, GEMV_ARGMAX = range(5)
@@ -61,6 +62,9 @@ def _lib():
             "ls_k_gemv": [C.c_int32, _vp, C.c_int32, _vp],
             "ls_k_gemm": [C.c_int32, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int64, _vp,
                           C.c_int64, _vp, _vp, C.c_int32, _vp],
+            "ls_k_gemm_ws": [C.c_int32, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int64, _vp,
+                             C.c_int64, _vp, _vp, C.c_int32, _vp, C.c_int64, _vp, C.c_int32, _vp],
+            "ls_gemm_splits": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32],
             "ls_k_decode_attention": [_vp, _vp],
             "ls_k_flash_attention": [_vp, _vp],
             "ls_k_rmsnorm_rows": [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_float, _vp],
@@ -149,7 +153,9 @@ class GemvWorkspace:
 
 def gemv(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: torch.Tensor,
          ws: GemvWorkspace, *, norm_w=None, eps=1e-6, bias=None, n_valid=None, qkv=None,
-         amax=None, grid=None, stream=None):
+         amax=None, grid=None, stream=None, ct_blob=None, ct_page0=0):
+    """w_tiled: plain tiles, or (ct_blob given) an ECT blob whose pages
+    ct_page0.. hold this matrix -- the GEMV then decodes pages in registers."""
     n_mt, n_kb = tile_dims(n, k)
     lib = _lib()
     g, mc = C.c_int32(), C.c_int32()
@@ -158,22 +164,46 @@ def gemv(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: 
     a = GemvArgs(w=_p(w_tiled), n_mt=n_mt, n_kb=n_kb, x=_p(x), norm_w=_p(norm_w), eps=eps,
                  ws=_p(ws.ws), counters=_p(ws.counters), max_contrib=mc.value, out=_p(out),
                  bias=_p(bias), n_valid=n if n_valid is None else n_valid, amax=_p(amax))
+    if ct_blob is not None:
+        a.ct_blob = ct_blob.data_ptr()
+        a.ct_page0 = ct_page0
+        a.w = ct_blob.data_ptr() + 128 + 12288 * ct_page0
     if qkv is not None:
         for key, val in qkv.items():
             setattr(a, key, _p(val) if isinstance(val, torch.Tensor) else val)
     _native.check(lib.ls_k_gemv(epi, C.byref(a), g.value, _stream(stream)), RuntimeError)
 
 
+_SPLITK_WS: dict = {}
+
+
 def gemm(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: torch.Tensor,
-         *, bias=None, n_valid=None, ldo=None, stream=None):
+         *, bias=None, n_valid=None, ldo=None, stream=None, splitk: bool = False):
+    """splitk=True passes a split-K workspace (skinny shapes then split K)."""
     n_mt, n_kb = tile_dims(n, k)
     T = x.shape[0]
     bias_f = bias if bias is not None and bias.dtype == torch.float32 else None
     bias_b = bias if bias is not None and bias.dtype == torch.bfloat16 else None
-    _native.check(_lib().ls_k_gemm(epi, _p(w_tiled), n_mt, n_kb, _p(x), T, x.stride(0), _p(out),
-                                   ldo if ldo is not None else out.stride(0), _p(bias_f),
-                                   _p(bias_b), n if n_valid is None else n_valid,
-                                   _stream(stream)), RuntimeError)
+    common = (epi, _p(w_tiled), n_mt, n_kb, _p(x), T, x.stride(0), _p(out),
+              ldo if ldo is not None else out.stride(0), _p(bias_f), _p(bias_b),
+              n if n_valid is None else n_valid)
+    if not splitk:
+        _native.check(_lib().ls_k_gemm(*common, _stream(stream)), RuntimeError)
+        return
+    nsm = num_sms(x.device.index or 0)
+    key = str(x.device)
+    if key not in _SPLITK_WS:  # counters are self-cleaning, so one workspace per device
+        _SPLITK_WS[key] = (torch.empty(nsm * 128 * 64, dtype=torch.float32, device=x.device),
+                           torch.zeros(nsm, dtype=torch.int32, device=x.device))
+    ws, cnt = _SPLITK_WS[key]
+    _native.check(_lib().ls_k_gemm_ws(*common, ws.data_ptr(), ws.numel(), cnt.data_ptr(), nsm,
+                                      _stream(stream)), RuntimeError)
+
+
+def gemm_splits(n: int, k: int, T: int, device=0) -> int:
+    n_mt, n_kb = tile_dims(n, k)
+    nsm = num_sms(device)
+    return _lib().ls_gemm_splits(n_mt, n_kb, T, nsm, nsm * 128 * 64, nsm)
 
 
 def decode_attention(q, k_cache, v_cache, n_ctx, out, hq, hkv, hd, scale, ws, counters,

@@ -1,0 +1,50 @@
+"""Exponent-coded tiles (ECT), the compact resident/streamed layer form:
+encoder + CPU reference decoder (no GPU), the sm_100a page decoder (bit-exact),
+and the executor running compact layers bit-identically to plain ones."""
+import pytest
+import torch
+
+from conftest import cuda_available
+from paper_2605_11678_b200 import ect
+
+
+def _layer(n_pages, tail_elems, seed=0, device="cpu"):
+    g = torch.Generator().manual_seed(seed)
+    w = torch.randn(n_pages * ect.PAGE_WORDS, generator=g) * 0.02
+    w[:64] = 0.0                                   # zero padding rows
+    w[100:104] = torch.tensor([3e-30, -1e20, float("inf"), 65504.0])  # rare exponents
+    w[min(ect.PAGE_WORDS + 7, w.numel() - 1)] = 1e-12
+    tail = 1 + 0.05 * torch.randn(tail_elems, generator=g)
+    buf = torch.cat([w.to(torch.bfloat16).view(torch.uint8), tail.to(torch.bfloat16).view(torch.uint8)])
+    return buf.to(device), n_pages * ect.PAGE_PLAIN
+
+
+def test_cpu_roundtrip_ratio_and_escapes():
+    buf, mat = _layer(24, 4104)
+    blob = ect.compress(buf, mat)
+    h = ect.header(blob)
+    assert h["n_pages"] == 24 and h["total"] == buf.numel() and h["n_exc"] >= 5
+    assert torch.equal(ect.decompress_cpu(blob), buf)
+    assert blob.numel() / buf.numel() < 0.76
+
+
+def test_cpu_roundtrip_no_tail_and_single_page():
+    buf, mat = _layer(1, 0, seed=2)
+    assert torch.equal(ect.decompress_cpu(ect.compress(buf, mat)), buf)
+
+
+def test_rejects_unaligned_matrix_region():
+    buf, _ = _layer(2, 8)
+    with pytest.raises(AssertionError):
+        ect.compress(buf, 1000)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")
+def test_gpu_decoder_bit_exact():
+    buf, mat = _layer(300, 2 * 4096 + 136, seed=3, device="cuda")
+    blob = ect.compress(buf, mat)
+    out = ect.decompress_gpu(blob)
+    torch.cuda.synchronize()
+    assert torch.equal(out, buf)
+    assert torch.equal(ect.decompress_cpu(blob), buf.cpu())

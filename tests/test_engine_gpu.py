@@ -185,7 +185,7 @@ def test_vram_cap_is_enforced():
     try:
         mem = eng.memory()
         room = mem["cap"] - mem["used"]
-        per_layer = eng.layer_bytes(M.KIND_LM)
+        per_layer = eng.resident_bytes[M.KIND_LM]  # compact (ECT) resident footprint
         fit = room // per_layer
         assert fit < M.TINY_LM.lm_layers
         eng.set_placement(ls.Placement.of({"vlm": range(fit)}))
@@ -211,3 +211,24 @@ def test_tensor_parallel_path_bit_exact_at_world_1():
     finally:
         base.close()
         tp.close()
+
+
+def test_compact_layers_bit_identical_to_plain():
+    """ECT storage is lossless: a compact engine (blobs in host arena, slots and
+    resident blocks) must reproduce the plain engine bit for bit, streamed and
+    resident, and its resident footprint must be the smaller blob size."""
+    plain = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=2, compact=False)
+    comp = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=2, compact=True)
+    try:
+        inputs = M.synthetic_inputs(M.TINY_ALPAMAYO, seed=6)
+        for pl in (ls.Placement.empty(), ls.Placement.of({"vit": [0], "vlm": [0, 2], "expert": [1]})):
+            a = plain.execute(pl, inputs=inputs, want_logits=True, record_timeline=False)
+            b = comp.execute(pl, inputs=inputs, want_logits=True, record_timeline=False)
+            assert torch.equal(a.logits, b.logits) and torch.equal(a.tokens, b.tokens)
+            assert torch.equal(a.actions, b.actions)
+        for kind in M.TINY_ALPAMAYO.kinds:
+            assert comp.resident_bytes[kind] < plain.resident_bytes[kind]
+        assert comp.memory()["slots"] < plain.memory()["slots"]
+    finally:
+        plain.close()
+        comp.close()

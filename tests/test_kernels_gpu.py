@@ -215,7 +215,7 @@ def _attn_ref(q, k, v, mask, scale):
     return (torch.softmax(s, -1) @ vv).permute(1, 0, 2)
 
 
-def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0):
+def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0, kv_splits=0):
     a = K.FlashArgs(q=q.data_ptr(), q_tok_stride=q.stride(0), q_head_stride=q.stride(1),
                     k1=k1.data_ptr(), v1=v1.data_ptr(), k1_tok_stride=k1.stride(0),
                     k1_head_stride=k1.stride(1), len1=k1.shape[0],
@@ -227,6 +227,15 @@ def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0)
                     out=out.data_ptr(), o_tok_stride=out.stride(0), o_head_stride=out.stride(1),
                     Tq=q.shape[0], hq=hq, hkv=hkv, hd=hd, causal=causal, q_offset=q_offset,
                     seg_len=seg_len, scale=1 / math.sqrt(hd))
+    if kv_splits > 1:
+        units = (q.shape[0] + 63) // 64 * hq
+        ws = torch.empty(units * kv_splits * 64 * (hd + 2), device=q.device)
+        cnt = torch.zeros(units, dtype=torch.int32, device=q.device)
+        a.kv_splits, a.ws, a.counters = kv_splits, ws.data_ptr(), cnt.data_ptr()
+        K.flash_attention(a)
+        torch.cuda.synchronize()
+        assert int(cnt.abs().sum()) == 0  # self-cleaning
+        return
     K.flash_attention(a)
 
 
@@ -255,7 +264,8 @@ def test_flash_vit_block_diagonal_hd72():
     _close(out, _attn_ref(q, k, v, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
 
 
-def test_flash_two_segments_expert():
+@pytest.mark.parametrize("kv_splits", [0, 3, 9, 40])
+def test_flash_two_segments_expert(kv_splits):
     torch.manual_seed(10)
     Tq, L1, hq, hkv, hd = 64, 530, 32, 8, 128
     q = torch.randn(Tq, hq, hd, device=DEV).to(torch.bfloat16)
@@ -266,7 +276,7 @@ def test_flash_two_segments_expert():
     out = torch.empty(Tq, hq, hd, dtype=torch.bfloat16, device=DEV)
     k1v = cache_k.permute(1, 0, 2)  # strided view [pos][head][d]
     v1v = cache_v.permute(1, 0, 2)
-    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd)
+    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd, kv_splits=kv_splits)
     kk = torch.cat([k1v[:L1], k2], 0)
     vv = torch.cat([v1v[:L1], v2], 0)
     mask = torch.ones(Tq, L1 + Tq, dtype=torch.bool, device=DEV)
@@ -293,3 +303,53 @@ def test_qk_norm_rope_prefill_kernel():
     _close(kc[:, 5:5 + T].permute(1, 0, 2), _rope_ref(hn(x[:, hq:hq + hkv], kn), cs), rel=1.5e-2,
            abs_=1e-2)
     assert torch.equal(vc[:, 5:5 + T].permute(1, 0, 2), qkv.view(T, -1, hd)[:, hq + hkv:])
+
+
+@pytest.mark.parametrize("n,k,page0", [(384, 256, 0), (6144, 4096, 0), (4096, 12288, 3)])
+def test_gemv_ect_pages_bit_identical(n, k, page0):
+    """Decode GEMV over ECT pages (decoded in registers) == plain-tile GEMV, bit
+    for bit, including escaped exponents; pages may start mid-blob (page0)."""
+    from paper_2605_11678_b200 import ect
+    torch.manual_seed(7)
+    w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
+    w[0, :5] = torch.tensor([1e-9, -3e-12, 0.0, 5.0, -1e-30], device=DEV).to(torch.bfloat16)
+    tiled = K.pack_tiled(w)
+    lead = torch.zeros(page0 * ect.PAGE_PLAIN, dtype=torch.uint8, device=DEV)
+    layer = torch.cat([lead, tiled.view(torch.uint8).reshape(-1), torch.ones(48, dtype=torch.uint8, device=DEV)])
+    blob = ect.compress(layer, layer.numel() - 48)
+    assert ect.header(blob)["n_exc"] > 0
+    x = torch.randn(k, device=DEV)
+    nw = (1 + 0.1 * torch.randn(k, device=DEV)).to(torch.bfloat16)
+    ws = K.GemvWorkspace(DEV)
+    a = torch.empty(n, device=DEV)
+    b = torch.empty(n, device=DEV)
+    K.gemv(K.GEMV_F32, tiled, n, k, x, a, ws, norm_w=nw)
+    K.gemv(K.GEMV_F32, None, n, k, x, b, ws, norm_w=nw, ct_blob=blob, ct_page0=page0)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+# epi: 0 BF16, 2 RESID_F32, 3 SILU_BF16, 4 F32 (kernels.GEMM_*)
+@pytest.mark.parametrize("epi,T,n,k", [(2, 64, 2048, 4096), (2, 64, 2048, 6912), (0, 64, 6144, 2048),
+                                       (3, 64, 1024, 2048), (4, 40, 256, 1536)])
+def test_gemm_split_k(epi, T, n, k):
+    """Skinny GEMMs split K across CTAs (deterministic reduction in split order):
+    matches the unsplit kernel to fp32 rounding and is run-to-run bit-stable."""
+    torch.manual_seed(11)
+    assert K.gemm_splits(n, k, T) > 1
+    w = K.pack_tiled((torch.randn(n, k, device=DEV) * 0.05).to(torch.bfloat16))
+    x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
+    ncol = n // 2 if epi == K.GEMM_SILU_BF16 else n
+    odt = torch.float32 if epi in (K.GEMM_RESID_F32, K.GEMM_F32) else torch.bfloat16
+    base = torch.randn(T, ncol, device=DEV).to(odt)
+    outs = []
+    for splitk in (False, True, True):
+        out = base.clone()
+        K.gemm(epi, w, n, k, x, out, n_valid=ncol, splitk=splitk)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[1], outs[2])
+    if odt == torch.float32:
+        _close(outs[1], outs[0], rel=1e-3, abs_=2e-3)
+    else:  # bf16 outputs: split and unsplit sums may round to adjacent bf16 values
+        _close(outs[1].float(), outs[0].float(), rel=8e-3, abs_=8e-3)

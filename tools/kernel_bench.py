@@ -19,13 +19,24 @@ from paper_2605_11678_b200 import kernels as K  # noqa: E402
 
 
 def timed(fn, reps=20, warm=5):
-    s = torch.cuda.current_stream()
+    """Mean device time per call: `reps` calls captured in one CUDA graph (no
+    host launch overhead in the measurement), replayed after warm-up."""
     for _ in range(warm):
         fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    for _ in range(reps):
-        fn()
+    g.replay()
     e1.record(s)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
@@ -49,16 +60,73 @@ def bench_gemv(n, k, epi=K.GEMV_F32, copies=3):
     return {"kernel": f"gemv epi={epi} {n}x{k}", "us": ms * 1e3, "GBps": b / (ms * 1e6)}
 
 
-def bench_gemm(T, n, k, epi=K.GEMM_BF16):
+def bench_gemv_ect(n, k, epi=K.GEMV_F32, copies=4):
+    """Decode GEMV reading ECT pages (12 KiB per 16 KiB tile), decoded in registers."""
+    from paper_2605_11678_b200 import ect
     dev = "cuda"
-    w = K.pack_tiled((torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16))
+    blobs = []
+    for _ in range(copies):
+        t = K.pack_tiled((torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)).view(torch.uint8).reshape(-1)
+        blobs.append(ect.compress(t, t.numel()))
+    x = torch.randn(k, device=dev)
+    nw = torch.ones(k, dtype=torch.bfloat16, device=dev)
+    out = torch.zeros(n, device=dev)
+    ws = K.GemvWorkspace(dev)
+    it = [0]
+
+    def run():
+        b = blobs[it[0] % copies]
+        it[0] += 1
+        K.gemv(epi, None, n, k, x, out, ws, norm_w=nw, n_valid=n // 2 if epi == K.GEMV_SILU else n,
+               ct_blob=b)
+    ms = timed(run)
+    plain = n * k * 2
+    moved = plain * 3 // 4 + k * 6 + n * 4
+    return {"kernel": f"gemv_ect epi={epi} {n}x{k}", "us": ms * 1e3, "GBps_moved": moved / (ms * 1e6),
+            "plain_equiv_GBps": plain / (ms * 1e6)}
+
+
+def bench_ect_decode(nbytes=385_892_352, copies=2):
+    from paper_2605_11678_b200 import ect
+    dev = "cuda"
+    blobs = []
+    for _ in range(copies):
+        w = (torch.randn(nbytes // 2, device=dev) * 0.02).to(torch.bfloat16).view(torch.uint8)
+        blobs.append(ect.compress(w, nbytes // 16384 * 16384))
+    out = torch.empty(nbytes + 4096, dtype=torch.uint8, device=dev)
+    it = [0]
+
+    import ctypes as C
+    from paper_2605_11678_b200 import _native
+    fn = _native.lib().ls_k_ect_decode
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+
+    def run():
+        fn(blobs[it[0] % copies].data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        it[0] += 1
+    ms = timed(run, reps=10, warm=3)
+    moved = nbytes * 7 // 4
+    return {"kernel": f"ect_decode {nbytes} B", "us": ms * 1e3, "GBps_moved": moved / (ms * 1e6)}
+
+
+def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False):
+    dev = "cuda"
+    # rotate weight copies so skinny (weight-bound) shapes stream from HBM, not L2
+    copies = max(1, min(12, (256 << 20) // (n * k * 2)))
+    ws_ = [K.pack_tiled((torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)) for _ in range(copies)]
     x = torch.randn(T, k, device=dev).to(torch.bfloat16)
     ncol = n // 2 if epi == K.GEMM_SILU_BF16 else n
     out = torch.zeros(T, ncol, dtype=torch.bfloat16 if epi != K.GEMM_RESID_F32 else torch.float32,
                       device=dev)
-    ms = timed(lambda: K.gemm(epi, w, n, k, x, out, n_valid=ncol))
+    it = [0]
+
+    def run():
+        K.gemm(epi, ws_[it[0] % copies], n, k, x, out, n_valid=ncol, splitk=splitk)
+        it[0] += 1
+    ms = timed(run)
     f = 2.0 * T * n * k
-    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}", "us": ms * 1e3, "TFLOPs": f / (ms * 1e9)}
+    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}" + (" splitk" if splitk else ""), "us": ms * 1e3,
+            "TFLOPs": f / (ms * 1e9), "weight_GBps": n * k * 2 / (ms * 1e6)}
 
 
 def bench_decode_attn(ctx=1045, hq=32, hkv=8, hd=128, n_split=18):
@@ -86,6 +154,16 @@ def main():
         res.append(bench_gemv(4096, 12288, K.GEMV_RESID))
         res.append(bench_gemv(6144, 4096, K.GEMV_F32))
         res.append(bench_gemv(4096, 4096, K.GEMV_RESID))
+    if args.only in ("all", "splitk"):
+        for T, n, k, epi in ((64, 2048, 4096, K.GEMM_RESID_F32), (64, 2048, 6912, K.GEMM_RESID_F32),
+                             (64, 6144, 2048, K.GEMM_BF16), (64, 13824, 2048, K.GEMM_SILU_BF16)):
+            res.append(bench_gemm(T, n, k, epi))
+            res.append(bench_gemm(T, n, k, epi, splitk=True))
+    if args.only in ("all", "ect"):
+        res.append(bench_gemv_ect(24576, 4096, K.GEMV_SILU))
+        res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
+        res.append(bench_gemv_ect(6144, 4096, K.GEMV_F32))
+        res.append(bench_ect_decode())
     if args.only in ("all", "attn"):
         for s in (18, 66):
             res.append(bench_decode_attn(n_split=s))
