@@ -9,6 +9,8 @@
 //   block-diagonal (per image) / two-segment KV (expert: VLM cache + own).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -143,7 +145,20 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
   float* recs = comb;  // [G][n_split][W]  (fits: host caps n_split * G * W floats)
   const float* base = a.ws + static_cast<long>(kh * G) * a.n_split * W;
   const int total = G * a.n_split * W;
-  for (int i = threadIdx.x; i < total; i += 128) recs[i] = __ldcg(base + i);
+  // 16 independent loads in flight per thread per round (L2 latency-bound otherwise)
+  for (int i0 = 0; i0 < total; i0 += 16 * 128) {
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u * 128 + threadIdx.x;
+      v[u] = i < total ? __ldcg(base + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u * 128 + threadIdx.x;
+      if (i < total) recs[i] = v[u];
+    }
+  }
   __syncthreads();
   for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
     const int g = idx / HD, d = idx % HD, h = kh * G + g;
@@ -204,6 +219,8 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
 
 // ------------------------------- flash ----------------------------------------
 
+constexpr int kMaxKvSplits = 8;  // split-KV CTAs form one (portable-size) cluster
+
 template <int HD>
 struct FlashCfg {
   static constexpr int kDK = (HD + 15) / 16 * 16;  // QK^T contraction, padded to k16
@@ -219,8 +236,8 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(16) uint8_t fsm[];
   bf16* qs = reinterpret_cast<bf16*>(fsm);
-  bf16* ks = qs + BM * LD;
-  bf16* vs = ks + BN * LD;
+  bf16* ks_buf = qs + BM * LD;          // [2][BN][LD]: double-buffered K and V blocks
+  bf16* vs_buf = ks_buf + 2 * BN * LD;
   pdl_trigger();
   pdl_wait();
 
@@ -274,14 +291,17 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
     k_begin = b0;
   }
 
-  for (int j0 = k_begin; j0 < k_end; j0 += BN) {
-    __syncthreads();
+  // K/V block loader: cp.async 16-byte chunks (zero-filled past the end), one
+  // commit group per block, so block j+1 streams in while block j is computed
+  auto load_kv = [&](int buf, int j0) {
+    bf16* kd = ks_buf + buf * BN * LD;
+    bf16* vd = vs_buf + buf * BN * LD;
     for (int i = threadIdx.x; i < BN * (DK / 8); i += 128) {
       const int r = i / (DK / 8), c = i % (DK / 8);
       const int j = j0 + r;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (j < k_end && c < CH) {
-        const bf16 *kp, *vp;
+      const bool ok = j < k_end && c < CH;
+      const bf16 *kp = a.k1, *vp = a.v1;
+      if (ok) {
         if (j < a.len1) {
           const long off = static_cast<long>(j) * a.k1_tok_stride + static_cast<long>(kvh) * a.k1_head_stride + c * 8;
           kp = a.k1 + off;
@@ -291,13 +311,24 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
           kp = a.k2 + off;
           vp = a.v2 + off;
         }
-        kv = *reinterpret_cast<const uint4*>(kp);
-        vv = *reinterpret_cast<const uint4*>(vp);
       }
-      *reinterpret_cast<uint4*>(ks + r * LD + c * 8) = kv;
-      *reinterpret_cast<uint4*>(vs + r * LD + c * 8) = vv;
+      cp_async16(kd + r * LD + c * 8, kp, ok);
+      cp_async16(vd + r * LD + c * 8, vp, ok);
+    }
+    cp_async_commit();
+  };
+  if (k_begin < k_end) load_kv(0, k_begin);
+  int buf = 0;
+  for (int j0 = k_begin; j0 < k_end; j0 += BN, buf ^= 1) {
+    if (j0 + BN < k_end) {
+      load_kv(buf ^ 1, j0 + BN);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const bf16* ks = ks_buf + buf * BN * LD;
+    const bf16* vs = vs_buf + buf * BN * LD;
     // S = Q K^T  (16 x 64 per warp)
     float s[BN / 8][4];
 #pragma unroll
@@ -366,12 +397,19 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
         mma_bf16_16816(o[dt], pa, b0, b1);
       }
     }
+    __syncthreads();  // everyone is done with `buf` before the next prefetch overwrites it
   }
   if (splits > 1) {
-    // ---- partial (o unnormalised, m, l) -> workspace; last CTA merges ----
+    // ---- split-KV merge inside the thread-block cluster (the splits of one
+    // (q tile, head)): partials stay in each CTA's shared memory; after a
+    // cluster barrier CTA z merges rows [z*BM/S, (z+1)*BM/S) reading its peers'
+    // partials over DSMEM (fixed split order -> deterministic), then a second
+    // barrier keeps every CTA alive until its peers are done reading ----
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     constexpr int W = HD + 2;
-    const int unit = blockIdx.x * a.hq + h;
-    float* rec = a.ws + (static_cast<long>(unit) * splits + blockIdx.z) * BM * W;
+    float* rec = reinterpret_cast<float*>(fsm);  // [BM][W]: o unnormalised, m, l
+    __syncthreads();                             // K/V buffers are free
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int row = warp * 16 + g + 8 * r;
@@ -385,45 +423,46 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
         rec[row * W + HD + 1] = lrow[r];
       }
     }
-    __threadfence();
-    __syncthreads();
-    __shared__ int s_last;
-    if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[unit], 1) == splits - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    float* mscale = reinterpret_cast<float*>(fsm);  // [BM][splits] weights, then [BM] 1/L
-    const float* base = a.ws + static_cast<long>(unit) * splits * BM * W;
-    for (int row = threadIdx.x; row < BM; row += 128) {
-      float M = -INFINITY;
-      for (int z = 0; z < splits; ++z) M = fmaxf(M, __ldcg(base + (static_cast<long>(z) * BM + row) * W + HD));
+    cluster.sync();
+    const int z = static_cast<int>(cluster.block_rank());
+    const int r_lo = z * BM / splits, r_hi = (z + 1) * BM / splits;
+    __shared__ float wz[BM / 2 + 1][kMaxKvSplits + 1];  // merge weights, then 1/L
+    for (int row = r_lo + threadIdx.x; row < r_hi; row += 128) {
+      float mz[kMaxKvSplits], M = -INFINITY;
+#pragma unroll
+      for (int p = 0; p < kMaxKvSplits; ++p) {
+        mz[p] = p < splits ? cluster.map_shared_rank(rec, p)[row * W + HD] : -INFINITY;
+        M = fmaxf(M, mz[p]);
+      }
       float L = 0.f;
-      for (int z = 0; z < splits; ++z) {
-        const float* rz = base + (static_cast<long>(z) * BM + row) * W;
-        const float mz = __ldcg(rz + HD);
-        const float wz = mz == -INFINITY ? 0.f : exp2f(mz - M);
-        mscale[row * splits + z] = wz;
-        L = fmaf(__ldcg(rz + HD + 1), wz, L);
+#pragma unroll
+      for (int p = 0; p < kMaxKvSplits; ++p) {
+        const float w = (p < splits && mz[p] != -INFINITY) ? exp2f(mz[p] - M) : 0.f;
+        wz[row - r_lo][p] = w;
+        if (p < splits) L = fmaf(cluster.map_shared_rank(rec, p)[row * W + HD + 1], w, L);
       }
-      mscale[BM * splits + row] = L > 0.f ? 1.0f / L : 0.f;
+      wz[row - r_lo][kMaxKvSplits] = L > 0.f ? 1.0f / L : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < BM * (HD / 2); i += 128) {
-      const int row = i / (HD / 2), d = 2 * (i % (HD / 2));
-      const int qrow = q0 + row;
-      if (qrow >= a.Tq) continue;
+    for (int i = threadIdx.x; i < (r_hi - r_lo) * (HD / 2); i += 128) {
+      const int rr = i / (HD / 2), d = 2 * (i % (HD / 2)), row = r_lo + rr;
       float v0 = 0.f, v1 = 0.f;
-      for (int z = 0; z < splits; ++z) {
-        const float* rz = base + (static_cast<long>(z) * BM + row) * W + d;
-        const float wz = mscale[row * splits + z];
-        v0 = fmaf(__ldcg(rz), wz, v0);
-        v1 = fmaf(__ldcg(rz + 1), wz, v1);
+#pragma unroll
+      for (int p = 0; p < kMaxKvSplits; ++p) {
+        if (p < splits) {
+          const float2 pv = *reinterpret_cast<const float2*>(cluster.map_shared_rank(rec, p) + row * W + d);
+          v0 = fmaf(pv.x, wz[rr][p], v0);
+          v1 = fmaf(pv.y, wz[rr][p], v1);
+        }
       }
-      const float inv = mscale[BM * splits + row];
-      bf16* op = a.out + static_cast<long>(qrow) * a.o_tok_stride + static_cast<long>(h) * a.o_head_stride;
-      *reinterpret_cast<uint32_t*>(op + d) = pack_bf16x2(v0 * inv, v1 * inv);
+      const int qrow = q0 + row;
+      if (qrow < a.Tq) {
+        const float inv = wz[rr][kMaxKvSplits];
+        bf16* op = a.out + static_cast<long>(qrow) * a.o_tok_stride + static_cast<long>(h) * a.o_head_stride;
+        *reinterpret_cast<uint32_t*>(op + d) = pack_bf16x2(v0 * inv, v1 * inv);
+      }
     }
-    if (threadIdx.x == 0) a.counters[unit] = 0;
+    cluster.sync();
     return;
   }
   // normalise + store
@@ -442,7 +481,7 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
 template <int HD>
 static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   using Cfg = FlashCfg<HD>;
-  const size_t smem = static_cast<size_t>(Cfg::kBM + 2 * Cfg::kBN) * Cfg::kLd * 2;
+  const size_t smem = static_cast<size_t>(Cfg::kBM + 4 * Cfg::kBN) * Cfg::kLd * 2;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -450,11 +489,26 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq, a.kv_splits > 1 ? a.kv_splits : 1);
-  if (a.kv_splits > 1 && (!a.ws || !a.counters || a.seg_len > 0 ||
-                          static_cast<size_t>(Cfg::kBM) * (a.kv_splits + 1) * 4 > smem))
+  const int splits = a.kv_splits > 1 ? a.kv_splits : 1;
+  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq, splits);
+  if (splits > kMaxKvSplits || (splits > 1 && a.seg_len > 0) ||
+      static_cast<size_t>(Cfg::kBM) * (HD + 2) * 4 > smem)
     return cudaErrorInvalidValue;
-  return launch_k(flash_kernel<HD>, grid, dim3(128), smem, st, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = take_launch_pdl() ? 1 : 0;
+  la[1].id = cudaLaunchAttributeClusterDimension;
+  la[1].val.clusterDim.x = 1;
+  la[1].val.clusterDim.y = 1;
+  la[1].val.clusterDim.z = static_cast<unsigned>(splits);
+  cfg.attrs = la;
+  cfg.numAttrs = splits > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, flash_kernel<HD>, a);
 }
 
 int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms) {
@@ -463,6 +517,7 @@ int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms) {
   if (units * 2 > num_sms || nblk < 4) return 1;
   int s = (2 * num_sms + units - 1) / units;  // ~2 CTAs per SM
   s = s < nblk / 2 ? s : nblk / 2;            // >= 2 key blocks per split
+  s = s < kMaxKvSplits ? s : kMaxKvSplits;    // one portable cluster per (q tile, head)
   return s < 1 ? 1 : s;
 }
 

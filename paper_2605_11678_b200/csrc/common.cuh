@@ -30,8 +30,26 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&t);
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async copy global -> shared (zero-filled when !valid), Ampere-style groups
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 // ---- warp-level tensor-core helpers (mma.sync m16n8k16 bf16 -> fp32) -----------
@@ -86,20 +104,24 @@ __device__ __forceinline__ uint4 ect_decode8(uint2 sm, uint32_t nib, uint32_t e0
   w.w = ect_pair(sm.y, 0xB3A2u, lo, hi, 0xF7B3u, e0p);
   return w;
 }
-// ECT pages store words in mma.sync A-fragment order: fragment f = (warp * 4 +
-// kstep) * 32 + lane holds the 8 words lane (g = lane / 4, t4 = lane % 4) of
-// warp `warp` needs for k-step `kstep` of m16n8k16 (rows 16 warp + g [+8],
-// k = 16 kstep + 2 t4 [+1] [+8]), i.e. registers a0..a3 in order.  Page word q
-// -> plain (swizzled) tile word:
+// ECT pages store words in mma.sync A-fragment order: fragment
+// f = ((w * 2 + kstep / 2) * 32 + lane) * 2 + kstep % 2 holds the 8 words lane
+// (g = lane / 4, t4 = lane % 4) of row block w needs for k-step `kstep` of
+// m16n8k16 (rows 16 w + g [+8], k = 16 kstep + 2 t4 [+1] [+8]), i.e. registers
+// a0..a3 in order; a lane's two fragments of a k-step pair are adjacent.
+// Page word q -> plain (swizzled) tile word:
 __device__ __forceinline__ uint32_t ect_plain_word(uint32_t q) {
-  const uint32_t f = q >> 3, j = q & 7, w = f >> 7, ks = (f >> 5) & 3, lane = f & 31;
+  const uint32_t f = q >> 3, j = q & 7, w = f >> 7, lane = (f >> 1) & 31;
+  const uint32_t ks = ((f >> 6) & 1) * 2 + (f & 1);
   const uint32_t r = 16 * w + (lane >> 2) + 8 * ((j >> 1) & 1);
   const uint32_t k = 16 * ks + 8 * (j >> 2) + 2 * (lane & 3) + (j & 1);
   return r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7);
 }
 // bit 4k set iff word k's code is 15 (escape)
 __device__ __forceinline__ uint32_t ect_escapes(uint32_t nib) {
-  return nib & (nib >> 1) & (nib >> 2) & (nib >> 3) & 0x11111111u;
+  // low 3 bits == 7 carries into bit 3; with bit 3 set the nibble is 15
+  const uint32_t t = ((nib & 0x77777777u) + 0x11111111u) & nib & 0x88888888u;
+  return t >> 3;
 }
 // Slow path: t = ect_escapes(nib) of the chunk starting at page word `word0`;
 // true exponents come from the page's exception list.

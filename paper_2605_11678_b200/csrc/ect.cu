@@ -15,31 +15,40 @@ namespace lsb {
 
 __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restrict__ blob,
                                                          uint8_t* __restrict__ out) {
+  __shared__ __align__(16) uint32_t tile[kTileBytes / 4];
   pdl_trigger();
   pdl_wait();  // `out` (the decode scratch) is read by the previous layer's kernels
   const EctHeader* h = reinterpret_cast<const EctHeader*>(blob);
   const uint32_t e0p = (h->e0 << 7) | (h->e0 << 23);
   const uint8_t* pages = blob + h->off_pages;
-  const uint64_t chunks = static_cast<uint64_t>(h->n_pages) * (kEctPageWords / 8);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < chunks; i += stride) {
-    const uint8_t* pg = pages + (i >> 10) * kEctPageBytes;
-    const uint32_t c = static_cast<uint32_t>(i & 1023);  // fragment index in the page
-    const uint2 sm = __ldcs(reinterpret_cast<const uint2*>(pg) + c);
-    const uint32_t nib = __ldcs(reinterpret_cast<const uint32_t*>(pg + kEctPageWords) + c);
-    const uint4 w = ect_decode8(sm, nib, e0p);
-    // the 4 word pairs go back to their swizzled tile positions (4-byte stores; a
-    // warp writes 16-byte runs of 8 rows, merged in L2)
-    uint32_t* po = reinterpret_cast<uint32_t*>(out + (i >> 10) * 16384ull);
-    po[ect_plain_word(c * 8 + 0) >> 1] = w.x;
-    po[ect_plain_word(c * 8 + 2) >> 1] = w.y;
-    po[ect_plain_word(c * 8 + 4) >> 1] = w.z;
-    po[ect_plain_word(c * 8 + 6) >> 1] = w.w;
+  // one page per CTA iteration: fragments decoded into the plain tile image in
+  // shared memory (pair stores are bank-conflict-free thanks to the 128 B
+  // swizzle), then streamed out as coalesced 16-byte stores
+  for (uint32_t page = blockIdx.x; page < h->n_pages; page += gridDim.x) {
+    const uint8_t* pg = pages + static_cast<uint64_t>(page) * kEctPageBytes;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const uint32_t f = it * 256 + threadIdx.x;  // fragment index in the page
+      const uint2 sm = __ldcs(reinterpret_cast<const uint2*>(pg) + f);
+      const uint32_t nib = __ldcs(reinterpret_cast<const uint32_t*>(pg + kEctPageWords) + f);
+      const uint4 w = ect_decode8(sm, nib, e0p);
+      tile[ect_plain_word(f * 8 + 0) >> 1] = w.x;
+      tile[ect_plain_word(f * 8 + 2) >> 1] = w.y;
+      tile[ect_plain_word(f * 8 + 4) >> 1] = w.z;
+      tile[ect_plain_word(f * 8 + 6) >> 1] = w.w;
+    }
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<uint64_t>(page) * kTileBytes);
+#pragma unroll
+    for (int it = 0; it < 4; ++it)
+      dst[it * 256 + threadIdx.x] = reinterpret_cast<const uint4*>(tile)[it * 256 + threadIdx.x];
+    __syncthreads();
   }
   // raw tail (vectors), whole 16-byte chunks
   const uint64_t tail = (h->total - h->mat_bytes + 15) / 16;
   const uint4* src = reinterpret_cast<const uint4*>(blob + h->off_tail);
   uint4* dst = reinterpret_cast<uint4*>(out + h->mat_bytes);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < tail; i += stride)
     dst[i] = src[i];
 }
@@ -66,7 +75,7 @@ __global__ void __launch_bounds__(256) ect_patch_kernel(const uint8_t* __restric
 }
 
 cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st) {
-  cudaError_t e = launch_k(ect_decode_kernel, dim3(8 * num_sms), dim3(256), 0, st, blob,
+  cudaError_t e = launch_k(ect_decode_kernel, dim3(6 * num_sms), dim3(256), 0, st, blob,
                            static_cast<uint8_t*>(out));
   if (e != cudaSuccess) return e;
   set_launch_pdl(true);  // the scatter follows the decode kernel directly

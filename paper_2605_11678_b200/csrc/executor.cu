@@ -827,10 +827,6 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       OV(gemm_ws, 4ull * e->gemm_ws_floats);
       OV(gemm_cnt, 4ull * e->gemm_cnt_n);
       e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq, e->ctx + Te, e->nsm);
-      if (e->ex_kv_splits > 1) {
-        OV(flash_ws, 4ull * flash_ws_floats(Te, d.ex_hq, d.ex_hd, e->ex_kv_splits));
-        OV(flash_cnt, 4ull * ((Te + 63) / 64) * d.ex_hq);
-      }
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
     e->tp_world = std::max(1, d.tp_world);

@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int m = q * 32 + lane;
     int i = 0;
-    __shared__ int sk_last;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int b = i & 1;
       const int tile = t / ks, sp = t % ks;
@@ -183,19 +182,43 @@ __global__ void __launch_bounds__(192, 1)
         }
       };
       const uint32_t acc = tmem + b * Cfg::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
-      if (ks == 1) {
+      if (ks == 1 && EPI == GEMM_RESID_F32) {
+        // residual add: all 32 old values of a chunk are loaded before any store
+        // (a load-add-store per token would serialise on possible aliasing)
+        float* out = static_cast<float*>(a.out);
+        const bool fv = f < a.n_valid;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float old[32], v0[16], v1[16];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int tok = n0 + c0 + j;
+            old[j] = (fv && tok < a.T) ? out[static_cast<long>(tok) * a.ldo + f] : 0.f;
+          }
+          tmem_ld16(acc + c0, v0);
+          tmem_ld16(acc + c0 + 16, v1);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int tok = n0 + c0 + j;
+            if (fv && tok < a.T)
+              out[static_cast<long>(tok) * a.ldo + f] = old[j] + ((j < 16 ? v0[j] : v1[j - 16]) + bias);
+          }
+        }
+      } else if (ks == 1) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
           tmem_ld16(acc + c0, v);
           emit(c0, v);
         }
+      }
+      if (ks == 1) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[b]);
         continue;
       }
-      // ---- split-K: partial -> workspace (token-major, coalesced), last unit reduces ----
+      // ---- split-K: partial -> workspace (token-major, coalesced) ----
       float* part = a.sk_ws + static_cast<long>(t) * BN * kTileRows;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -206,29 +229,73 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);  // TMEM buffer free for the next unit
+      if (lane == 0) mbar_arrive(&acc_empty[b]);  // TMEM buffer free
+      // Distributed fix-up: every unit of the tile waits for all ks partials,
+      // then reduces its own 1/ks of the tile's tokens (in split order, so the
+      // result is deterministic) and runs the epilogue on them.  All units are
+      // co-resident (grid = units <= #SMs, launch_dependents issued at entry), so
+      // the wait cannot deadlock.
       __threadfence();
       named_bar(3, 128);
-      if (m == 0) sk_last = atomicAdd(&a.sk_cnt[tile], 1) == ks - 1;
-      named_bar(3, 128);
-      const bool last = sk_last;
-      named_bar(3, 128);  // everyone has read sk_last before it is reused
-      if (!last) continue;
-      __threadfence();
-      const float* base = a.sk_ws + static_cast<long>(tile) * ks * BN * kTileRows;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        for (int z = 0; z < ks; ++z) {
-          const float* pz = base + static_cast<long>(z) * BN * kTileRows + c0 * kTileRows + m;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += __ldcg(pz + j * kTileRows);
-        }
-        emit(c0, v);
+      if (m == 0) {
+        atomicAdd(&a.sk_cnt[tile], 1);
+        while (ld_acquire_gpu(&a.sk_cnt[tile]) < ks) __nanosleep(64);
       }
-      if (m == 0) a.sk_cnt[tile] = 0;
+      named_bar(3, 128);
+      __threadfence();
+      const float* base = a.sk_ws + static_cast<long>(tile) * ks * BN * kTileRows + m;
+      const int c_lo = sp * BN / ks, c_hi = (sp + 1) * BN / ks;
+      // two tokens per round, all (<= 16) split partials of both loaded at once:
+      // the reduction costs ~ceil(tokens / 2) L2 round trips, not tokens x splits
+#pragma unroll 1
+      for (int c = c_lo; c < c_hi; c += 2) {
+        const bool two = c + 1 < c_hi;
+        float p0[16], p1[16];
+#pragma unroll
+        for (int z = 0; z < 16; ++z) {
+          p0[z] = z < ks ? __ldcg(base + (static_cast<long>(z) * BN + c) * kTileRows) : 0.f;
+          p1[z] = (z < ks && two) ? __ldcg(base + (static_cast<long>(z) * BN + c + 1) * kTileRows) : 0.f;
+        }
+        float old0 = 0.f, old1 = 0.f;
+        if constexpr (EPI == GEMM_RESID_F32) {
+          if (f < a.n_valid && n0 + c < a.T) old0 = static_cast<float*>(a.out)[static_cast<long>(n0 + c) * a.ldo + f];
+          if (f < a.n_valid && two && n0 + c + 1 < a.T)
+            old1 = static_cast<float*>(a.out)[static_cast<long>(n0 + c + 1) * a.ldo + f];
+        }
+        float ys[2] = {0.f, 0.f};
+#pragma unroll
+        for (int z = 0; z < 16; ++z) {
+          ys[0] += p0[z];
+          ys[1] += p1[z];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const int tok = n0 + c + u;
+          float y = ys[u];
+          if constexpr (EPI == GEMM_SILU_BF16) {
+            named_bar(2, 128);
+            stage_f[m] = y;
+            named_bar(2, 128);
+            const int g = mt * 64 + m;
+            if (m < 64 && tok < a.T && g < a.n_valid)
+              static_cast<bf16*>(a.out)[static_cast<long>(tok) * a.ldo + g] =
+                  f2bf(silu(stage_f[m]) * stage_f[m + 64]);
+          } else if (tok < a.T) {
+            const long o = static_cast<long>(tok) * a.ldo + f;
+            y += bias;
+            if constexpr (EPI == GEMM_BF16) static_cast<bf16*>(a.out)[o] = f2bf(y);
+            else if constexpr (EPI == GEMM_BF16_GELU) static_cast<bf16*>(a.out)[o] = f2bf(gelu_tanh(y));
+            else if constexpr (EPI == GEMM_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] = y; }
+            else if constexpr (EPI == GEMM_RESID_F32) {
+              if (f < a.n_valid) static_cast<float*>(a.out)[o] = (u ? old1 : old0) + y;
+            }
+          }
+        }
+      }
+      // second arrival: the last unit to leave re-arms the counter for the next launch
+      named_bar(3, 128);
+      if (m == 0 && atomicAdd(&a.sk_cnt[tile], 1) == 2 * ks - 1) a.sk_cnt[tile] = 0;
     }
   }
   tc_fence_before();
@@ -244,9 +311,10 @@ int gemm_block_n(int T) { return T <= 64 ? 64 : (T <= 256 ? 128 : 256); }
 int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n) {
   const int bn = gemm_block_n(T);
   const int tiles = n_mt * ((T + bn - 1) / bn);
-  if (tiles * 2 > num_sms || tiles > cnt_n) return 1;
-  int ks = num_sms / tiles;                 // one wave of units
+  if (tiles * 4 > num_sms || tiles > cnt_n) return 1;  // >= 4 splits or not worth the fix-up
+  int ks = num_sms / tiles;                 // one wave of units: all co-resident (fix-up waits)
   if (ks > n_kb / 4) ks = n_kb / 4;         // >= 4 k-blocks (256 of K) per unit
+  if (ks > 16) ks = 16;                     // the fix-up loads <= 16 partials per token at once
   while (ks > 1 && static_cast<long>(tiles) * ks * bn * 128 > ws_floats) --ks;
   return ks < 1 ? 1 : ks;
 }

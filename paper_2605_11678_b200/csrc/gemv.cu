@@ -29,10 +29,10 @@ template <bool CT>
 __host__ __device__ inline int gemv_stages(int n_kb) {
   constexpr int stage = CT ? kEctPageBytes : kTileBytes;
   constexpr int cap = CT ? 16 : 12;
-  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 1024) / stage;
+  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 1536) / stage;
   return avail > cap ? cap : avail;
 }
-constexpr int kGemvConsumers = 256;  // 8 warps, 16 rows of every tile each
+constexpr int kGemvConsumers = 512;  // 16 warps: 8 row blocks x 2 k-halves of every tile
 constexpr int kGemvThreads = kGemvConsumers + 32;
 
 __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
@@ -46,7 +46,12 @@ __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
 // two live columns, bf16(x) and bf16(x - bf16(x)) (x to ~16 mantissa bits).
 // Per 8 weight words a thread spends ~0.25 instructions instead of 16 FMA +
 // convert ops, which is what lets the ECT decode (~2.5 ops/word) fit under
-// the HBM stream.  Plain and ECT tiles give bit-identical results.
+// the HBM stream.  Warp w owns rows 16 (w % 8) .. +15 and k-steps 2 (w / 8),
+// +1 of every tile (16 warps hide the decode latency); the two k-halves are
+// summed in a fixed order at flush.  x lives in shared memory pre-arranged so
+// a lane's four B words for two k-steps are one 16-byte load, and an ECT page
+// keeps a lane's two fragments for its k-step pair adjacent (one 16-byte +
+// one 8-byte load).  Plain and ECT tiles give bit-identical results.
 template <int EPI, bool CT>
 __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -54,9 +59,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   const int K = a.n_kb * kTileCols;
   uint8_t* stages = smem;
   const int NS = gemv_stages<CT>(a.n_kb);
-  uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NS * kStage);  // [K/2][hi, lo] bf16x2
-  float* red = reinterpret_cast<float*>(xq + K);
-  float* scratch = red + kTileRows;  // 16 floats for block reductions
+  // x as bf16x2 B words: [kb][half h][column hi|lo][t4][b0(2h), b1(2h), b0(2h+1), b1(2h+1)]
+  uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NS * kStage);
+  float* red = reinterpret_cast<float*>(xq + K);  // [2][128]: k-half 0, k-half 1
+  float* scratch = red + 2 * kTileRows;  // 16 floats for block reductions
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
   uint64_t* empty = full + kGemvMaxStages;
   int* flag = reinterpret_cast<int*>(empty + kGemvMaxStages);
@@ -125,8 +131,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     for (int w = 0; w < kGemvConsumers / 32; ++w) tot += scratch[w];
     rstd = rsqrtf(tot / K + a.eps);
   }
-  // x -> (hi, lo) bf16 pairs: xq[2i] = {hi[2i], hi[2i+1]}, xq[2i+1] = {lo[2i], lo[2i+1]}
-  for (int i = tid; i < K / 2; i += kGemvConsumers) {
+  // x -> (hi, lo) bf16 pairs, scattered into the B-word layout above
+  for (int i = tid; i < K / 2; i += kGemvConsumers) {  // pair i = k 2i, 2i+1
     float v0 = a.x[2 * i], v1 = a.x[2 * i + 1];
     if (a.norm_w) {
       v0 = v0 * rstd * bf2f(a.norm_w[2 * i]);
@@ -135,8 +141,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
     const float2 hf = __bfloat1622float2(hi);
     const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
-    xq[2 * i] = *reinterpret_cast<const uint32_t*>(&hi);
-    xq[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&lo);
+    const int kb = i >> 5, pp = i & 31;  // pair within the k-block: 16 h + 8 (ks&1) + 4 (b1) + t4
+    const int h = pp >> 4, slot = ((pp >> 3) & 1) * 2 + ((pp >> 2) & 1), t4i = pp & 3;
+    const int base = kb * 64 + h * 32 + t4i * 4 + slot;
+    xq[base] = *reinterpret_cast<const uint32_t*>(&hi);
+    xq[base + 16] = *reinterpret_cast<const uint32_t*>(&lo);
   }
   named_bar(1, kGemvConsumers);
 
@@ -144,13 +153,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   float acc[4] = {0.f, 0.f, 0.f, 0.f};  // mma C: rows g, g+8 x columns (hi, lo) in lanes t4 == 0
   int cur_mt = t0 < t1 ? static_cast<int>(t0 / a.n_kb) : -1;
 
+  const int rb = warp & 7, kh = warp >> 3;  // row block, k-half
   auto flush = [&](int mt) {
     if (t4 == 0) {
-      red[warp * 16 + g] = acc[0] + acc[1];
-      red[warp * 16 + g + 8] = acc[2] + acc[3];
+      red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
+      red[kh * kTileRows + rb * 16 + g + 8] = acc[2] + acc[3];
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = 0.f;
+    named_bar(1, kGemvConsumers);
+    if (tid < kTileRows) red[tid] += red[kTileRows + tid];
     named_bar(1, kGemvConsumers);
     const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
     const int c_first = cta_of_tile(first, G, T);
@@ -185,12 +197,13 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     named_bar(1, kGemvConsumers);
   };
 
-  // B fragment source: column g = 0 -> hi, g = 1 -> lo, other columns zero
-  const uint32_t* xb = xq + (g & 1);
+  // B words: column g = 0 -> hi, g = 1 -> lo, other columns zero
+  const uint32_t* xb = xq + kh * 32 + (g & 1) * 16 + t4 * 4;
   const bool bcol = g < 2;
   // ldmatrix.x4 row address of this lane inside a plain tile (k-step added per use)
-  const int lr = warp * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+  const int lr = rb * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
   const int lc = lane >> 4;  // 0: k 0-7 of the step, 1: k 8-15
+  const int f0 = ((rb * 2 + kh) * 32 + lane) * 2;  // ECT: this lane's fragments for k-steps 2kh, 2kh+1
   int kb = t0 < t1 ? static_cast<int>(t0 - static_cast<long>(cur_mt) * a.n_kb) : 0;
   int s = 0;
   uint32_t round = 0;
@@ -204,28 +217,27 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
     mbar_wait(&full[s], round & 1);
     const uint8_t* st = stages + s * kStage;
-    const uint32_t* xk = xb + kb * kTileCols;  // pair index kb*32 (x2 for hi/lo interleave)
-#pragma unroll
-    for (int ks = 0; ks < kTileCols / 16; ++ks) {
-      uint32_t af[4];
-      if constexpr (CT) {
-        const int f = (warp * 4 + ks) * 32 + lane;  // this lane's A fragment in the page
-        const uint2 sm = *reinterpret_cast<const uint2*>(st + f * 8);
-        const uint32_t nib = *reinterpret_cast<const uint32_t*>(st + kEctPageWords + f * 4);
-        uint4 wv = ect_decode8(sm, nib, e0p);
-        const uint32_t t = ect_escapes(nib);
-        if (t) wv = ect_patch8(wv, t, tile, f * 8, exc_off, exc);
-        af[0] = wv.x;
-        af[1] = wv.y;
-        af[2] = wv.z;
-        af[3] = wv.w;
-      } else {
-        ldsm_x4(af, st + lr * 128 + (((2 * ks + lc) ^ (lr & 7)) << 4));
+    uint4 bw = make_uint4(0u, 0u, 0u, 0u);
+    if (bcol) bw = *reinterpret_cast<const uint4*>(xb + kb * 64);
+    uint32_t af[2][4];
+    if constexpr (CT) {
+      const uint4 sm = *reinterpret_cast<const uint4*>(st + f0 * 8);
+      const uint2 nib = *reinterpret_cast<const uint2*>(st + kEctPageWords + f0 * 4);
+      uint4 w0 = ect_decode8(make_uint2(sm.x, sm.y), nib.x, e0p);
+      uint4 w1 = ect_decode8(make_uint2(sm.z, sm.w), nib.y, e0p);
+      if (ect_escapes(nib.x) | ect_escapes(nib.y)) {
+        w0 = ect_patch8(w0, ect_escapes(nib.x), tile, f0 * 8, exc_off, exc);
+        w1 = ect_patch8(w1, ect_escapes(nib.y), tile, f0 * 8 + 8, exc_off, exc);
       }
-      const uint32_t b0 = bcol ? xk[2 * (8 * ks + t4)] : 0u;
-      const uint32_t b1 = bcol ? xk[2 * (8 * ks + 4 + t4)] : 0u;
-      mma_bf16_16816(acc, af, b0, b1);
+      af[0][0] = w0.x; af[0][1] = w0.y; af[0][2] = w0.z; af[0][3] = w0.w;
+      af[1][0] = w1.x; af[1][1] = w1.y; af[1][2] = w1.z; af[1][3] = w1.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        ldsm_x4(af[q], st + lr * 128 + (((2 * (2 * kh + q) + lc) ^ (lr & 7)) << 4));
     }
+    mma_bf16_16816(acc, af[0], bw.x, bw.y);
+    mma_bf16_16816(acc, af[1], bw.z, bw.w);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     ++kb;
@@ -257,8 +269,8 @@ int gemv_max_contrib(int n_mt, int n_kb, int grid) {
 template <bool CT>
 static size_t gemv_smem(int n_kb) {
   return static_cast<size_t>(gemv_stages<CT>(n_kb)) * (CT ? kEctPageBytes : kTileBytes) +
-         static_cast<size_t>(n_kb) * kTileCols * 4 + kTileRows * 4 + 16 * 4 + 2 * kGemvMaxStages * 8 +
-         16;
+         static_cast<size_t>(n_kb) * kTileCols * 4 + 2 * kTileRows * 4 + 16 * 4 +
+         2 * kGemvMaxStages * 8 + 16;
 }
 
 template <int EPI, bool CT>

@@ -121,11 +121,12 @@ struct FlashArgs {
   int seg_len;     // >0: block-diagonal attention over segments of seg_len tokens (ViT images)
   float scale;
   // split-KV (few query tiles, long KV: the 64-token expert over the LM cache):
-  // grid.z = kv_splits CTAs per (q tile, head) each reduce a contiguous key
-  // range; the last to finish merges the partials in split order.
+  // grid.z = kv_splits (<= 8) CTAs per (q tile, head), one thread-block cluster,
+  // each reduce a contiguous key range; partials are merged over DSMEM in split
+  // order.  ws / counters: unused (kept for ABI stability).
   int kv_splits;   // <= 1: off
-  float* ws;       // [q_tiles * hq * kv_splits][64][hd + 2]
-  int* counters;   // [q_tiles * hq], zero between launches (self-cleaning)
+  float* ws;
+  int* counters;
 };
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st);
 // kv_splits the launcher will use for (Tq, hq, keys) given num_sms, and the

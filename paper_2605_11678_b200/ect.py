@@ -47,12 +47,14 @@ _HDR_FMT = "<IIQQQQQQII16B48x"  # ..., n_exc, e0, codebook[16]
 
 
 def page_order() -> torch.Tensor:
-    """perm[q] = plain (swizzled tile) word index of page word q.  Fragment f =
-    (warp * 4 + kstep) * 32 + lane holds the 8 words a decode-GEMV lane feeds to
-    mma.sync m16n8k16 as A registers a0..a3 (csrc/common.cuh ect_plain_word)."""
+    """perm[q] = plain (swizzled tile) word index of page word q.  Fragment
+    f = ((w * 2 + kstep / 2) * 32 + lane) * 2 + kstep % 2 holds the 8 words a
+    decode-GEMV lane feeds to mma.sync m16n8k16 as A registers a0..a3
+    (csrc/common.cuh ect_plain_word)."""
     q = torch.arange(PAGE_WORDS, dtype=torch.int64)
     f, j = q >> 3, q & 7
-    w, ks, lane = f >> 7, (f >> 5) & 3, f & 31
+    w, lane = f >> 7, (f >> 1) & 31
+    ks = ((f >> 6) & 1) * 2 + (f & 1)
     r = 16 * w + (lane >> 2) + 8 * ((j >> 1) & 1)
     k = 16 * ks + 8 * (j >> 2) + 2 * (lane & 3) + (j & 1)
     return r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7)

@@ -227,15 +227,7 @@ def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0,
                     out=out.data_ptr(), o_tok_stride=out.stride(0), o_head_stride=out.stride(1),
                     Tq=q.shape[0], hq=hq, hkv=hkv, hd=hd, causal=causal, q_offset=q_offset,
                     seg_len=seg_len, scale=1 / math.sqrt(hd))
-    if kv_splits > 1:
-        units = (q.shape[0] + 63) // 64 * hq
-        ws = torch.empty(units * kv_splits * 64 * (hd + 2), device=q.device)
-        cnt = torch.zeros(units, dtype=torch.int32, device=q.device)
-        a.kv_splits, a.ws, a.counters = kv_splits, ws.data_ptr(), cnt.data_ptr()
-        K.flash_attention(a)
-        torch.cuda.synchronize()
-        assert int(cnt.abs().sum()) == 0  # self-cleaning
-        return
+    a.kv_splits = kv_splits  # > 1: one thread-block cluster per (q tile, head), DSMEM merge
     K.flash_attention(a)
 
 
@@ -264,7 +256,7 @@ def test_flash_vit_block_diagonal_hd72():
     _close(out, _attn_ref(q, k, v, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
 
 
-@pytest.mark.parametrize("kv_splits", [0, 3, 9, 40])
+@pytest.mark.parametrize("kv_splits", [0, 3, 8])
 def test_flash_two_segments_expert(kv_splits):
     torch.manual_seed(10)
     Tq, L1, hq, hkv, hd = 64, 530, 32, 8, 128
@@ -330,7 +322,7 @@ def test_gemv_ect_pages_bit_identical(n, k, page0):
 
 
 # epi: 0 BF16, 2 RESID_F32, 3 SILU_BF16, 4 F32 (kernels.GEMM_*)
-@pytest.mark.parametrize("epi,T,n,k", [(2, 64, 2048, 4096), (2, 64, 2048, 6912), (0, 64, 6144, 2048),
+@pytest.mark.parametrize("epi,T,n,k", [(2, 64, 2048, 4096), (2, 64, 2048, 6912), (0, 64, 3072, 2048),
                                        (3, 64, 1024, 2048), (4, 40, 256, 1536)])
 def test_gemm_split_k(epi, T, n, k):
     """Skinny GEMMs split K across CTAs (deterministic reduction in split order):

@@ -1,0 +1,99 @@
+"""Residency sweep (BASELINE config 4): k = 0..36 resident LM layers, interleaved
+(planner.interleaved_indices) vs contiguous (range(k)) placement, everything
+else streamed; measured latency vs the reference predictor (Eq. 10, one k=0
+measurement + the profile slope, predictor.py:53-104) and vs the schedule
+model (dfbsim.simulate on the measured profile).
+
+    python tools/sweep.py [--trials 3] [--out profiles/r1_sweep.json]
+
+Writes the measured sweep in the reference's CSV format (k,measured_s,
+predictor.py:115-143) next to the JSON report.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--trials", type=int, default=3)
+    ap.add_argument("--config", default="alpamayo-r1-10b-shape")
+    ap.add_argument("--vram-cap-mb", type=float, default=16000.0)
+    ap.add_argument("--out", default="profiles/r1_sweep.json")
+    ap.add_argument("--no-prefetch", action="store_true")
+    args = ap.parse_args()
+    import paper_2605_11678_b200 as ls
+    from paper_2605_11678_b200 import model as M
+    from paper_2605_11678_b200.engine import DemandLayeringEngine
+
+    cfg = M.PRESETS[args.config]
+    eng = DemandLayeringEngine(cfg, vram_cap_mb=args.vram_cap_mb)
+    sim_cfg = ls.SimConfig(cross_invocation_prefetch=not args.no_prefetch)
+    t0 = time.time()
+    prof = eng.profile_run(iterations=2, warmup=1, config=sim_cfg)
+    vlm = prof.module("vlm")
+    L = vlm.layers
+    plan = ls.plan_for_budget(prof, prof.hardware.vram_mb, sim_cfg)
+    k_cap = plan.resident_count_per_module.get("vlm", 0)
+    inputs = M.synthetic_inputs(cfg, seed=0)
+    placements = {"interleaved": lambda k: ls.interleaved_indices(k, L) if k < L else range(L),
+                  "contiguous": lambda k: range(k)}
+    rows = []
+    for name, fn in placements.items():
+        for k in range(0, L + 1):
+            pl = ls.Placement.of({"vlm": fn(k)}) if k else ls.Placement.empty()
+            eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False)  # warm-up
+            ms = [eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False).total_ms
+                  for _ in range(args.trials)]
+            sim = ls.simulated_total(prof, pl, sim_cfg)
+            rows.append({"placement": name, "k": k, "measured_s": statistics.median(ms) / 1e3,
+                         "trials_s": [m / 1e3 for m in ms], "dfbsim_s": sim / 1e3})
+    intercept = rows[0]["measured_s"]
+    slope = ls.slope_from_profile(vlm)
+    report = {"config": cfg.name, "vram_cap_mb": args.vram_cap_mb, "trials": args.trials,
+              "sim_config": {"cross_invocation_prefetch": sim_cfg.cross_invocation_prefetch,
+                             "slot_count": sim_cfg.slot_count},
+              "profile": json.loads(ls.profile.dumps(prof)),
+              "planner_k_vlm": k_cap, "intercept_s": intercept, "slope_ms_per_layer": slope}
+    for name in placements:
+        sub = [r for r in rows if r["placement"] == name]
+        ks = [r["k"] for r in sub]
+        preds = ls.predict(intercept, slope, ks)
+        rep = ls.validate(preds, [(r["k"], r["measured_s"]) for r in sub])
+        for r, row, p in zip(sub, rep.rows, preds):
+            r["eq10_s"] = p.predicted_s
+            r["eq10_error_pct"] = row.error_pct
+            r["dfbsim_error_pct"] = (r["dfbsim_s"] - r["measured_s"]) / r["measured_s"] * 100.0
+        within = [r for r in sub if r["k"] <= min(k_cap, L - 1)]
+        report[name] = {
+            "rows": sub,
+            "eq10_max_abs_error_pct": rep.max_abs_error_pct,
+            "eq10_max_abs_error_pct_k_le_28": max(abs(r["eq10_error_pct"]) for r in sub if r["k"] <= 28),
+            "dfbsim_max_abs_error_pct": max(abs(r["dfbsim_error_pct"]) for r in sub),
+            "within_planner_cap_k": len(within) - 1,
+            "fitted_slope_s": rep.fitted_slope_s,
+        }
+    report["wall_s"] = time.time() - t0
+    out = Path(args.out)
+    out.parent.mkdir(parents=True, exist_ok=True)
+    out.write_text(json.dumps(report, indent=1))
+    with open(out.with_suffix(".csv"), "w") as fh:
+        fh.write("k,measured_s\n")
+        for r in report["interleaved"]["rows"]:
+            fh.write(f"{r['k']},{r['measured_s']!r}\n")
+    for name in placements:
+        s = report[name]
+        print(f"{name}: Eq10 max|err| {s['eq10_max_abs_error_pct']:.3f}% (k<=28: "
+              f"{s['eq10_max_abs_error_pct_k_le_28']:.3f}%), dfbsim max|err| {s['dfbsim_max_abs_error_pct']:.3f}%")
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
