@@ -295,11 +295,14 @@ int ls_k_gemm(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, cons
               const void* bias_bf16, int32_t n_valid, void* stream);
 /* Same with a split-K workspace (fp32 partials + self-cleaning tile counters):
    skinny GEMMs (few 128-feature tiles) split K across CTAs, deterministic
-   reduction in split order.  ls_gemm_splits: the split factor it will use. */
+   reduction in split order.  ls_gemm_splits: the split factor it will use.
+   ct_blob != NULL: the weights are pages ct_page0.. of that ECT blob (w_tiled
+   ignored), decoded into shared memory inside the kernel. */
 int ls_k_gemm_ws(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, const void* x,
                  int32_t T, int64_t ldx, void* out, int64_t ldo, const float* bias,
                  const void* bias_bf16, int32_t n_valid, float* sk_ws, int64_t sk_ws_floats,
-                 int32_t* sk_cnt, int32_t sk_cnt_n, void* stream);
+                 int32_t* sk_cnt, int32_t sk_cnt_n, const void* ct_blob, int32_t ct_page0,
+                 void* stream);
 int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64_t ws_floats,
                    int32_t cnt_n);
 int ls_k_decode_attention(const void* args, void* stream);

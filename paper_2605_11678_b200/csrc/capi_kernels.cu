@@ -82,7 +82,7 @@ int ls_k_gemm(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void
 int ls_k_gemm_ws(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void* x, int32_t T,
                  int64_t ldx, void* out, int64_t ldo, const float* bias, const void* bias_bf16,
                  int32_t n_valid, float* sk_ws, int64_t sk_ws_floats, int32_t* sk_cnt,
-                 int32_t sk_cnt_n, void* stream) {
+                 int32_t sk_cnt_n, const void* ct_blob, int32_t ct_page0, void* stream) {
   CUtensorMap map;
   int rc = make_tmap_bf16(&map, x, static_cast<uint64_t>(T), static_cast<uint64_t>(n_kb) * 64,
                           static_cast<uint64_t>(ldx), static_cast<uint32_t>(gemm_block_n(T)));
@@ -101,6 +101,9 @@ int ls_k_gemm_ws(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const v
   a.sk_ws_floats = sk_ws_floats;
   a.sk_cnt = sk_cnt;
   a.sk_cnt_n = sk_cnt_n;
+  a.ct_blob = static_cast<const uint8_t*>(ct_blob);
+  a.ct_page0 = ct_page0;
+  if (ct_blob) a.w = static_cast<const uint8_t*>(ct_blob) + sizeof(EctHeader) + static_cast<long>(ct_page0) * kEctPageBytes;
   return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm_ws");
 }
 

@@ -229,7 +229,7 @@ struct ls_exec {
   uint64_t bytes_slots = 0, bytes_always = 0, bytes_overhead = 0, mark = 0;
   uint64_t mark0 = 0;            // arena offset where the slot ring starts (after overhead)
   char* scratch = nullptr;       // decoded ECT layer (counted as overhead)
-  bool ct_fused_decode = true;   // LM decode GEMVs read ECT pages (else decode to scratch)
+  bool ct_fused = true;          // kernels read ECT pages (else decode each layer to the scratch)
   uint64_t scratch_bytes = 0;
   int S = 0, ctx = 0, Tv = 0, Te = 0, vit_ffn_pad = 0, n_split = 1;
   // activations
@@ -307,25 +307,6 @@ int tmap(CUtensorMap* m, const void* base, int rows, int cols, int ld) {
 
 // ---------------------------- launch helpers -----------------------------------
 
-int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensorMap& map, void* out,
-         long ldo, const void* bias_bf16 = nullptr, int n_valid = -1) {
-  GemmArgs a{};
-  a.w = reinterpret_cast<const uint8_t*>(w);
-  a.n_mt = n_mt(n);
-  a.n_kb = n_kb(k);
-  a.T = T;
-  a.out = out;
-  a.ldo = ldo;
-  a.bias_bf16 = static_cast<const bf16*>(bias_bf16);
-  a.n_valid = n_valid < 0 ? n : n_valid;
-  a.sk_ws = e->gemm_ws;
-  a.sk_ws_floats = e->gemm_ws_floats;
-  a.sk_cnt = e->gemm_cnt;
-  a.sk_cnt_n = e->gemm_cnt_n;
-  KL(launch_gemm(epi, a, map, e->ss));
-  return LS_OK;
-}
-
 // Compact (ECT) view of a layer blob: where part i of the plain layout lives.
 struct CtView {
   const char* blob = nullptr;  // nullptr: plain layer
@@ -342,6 +323,28 @@ struct CtView {
   }
   int page0(const ls_layer_layout& L, int i) const { return static_cast<int>(L.offset[i] / 16384); }
 };
+
+int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensorMap& map, void* out,
+         long ldo, const void* bias_bf16 = nullptr, int n_valid = -1, const char* ct_blob = nullptr,
+         int ct_page0 = 0) {
+  GemmArgs a{};
+  a.w = reinterpret_cast<const uint8_t*>(w);
+  a.ct_blob = reinterpret_cast<const uint8_t*>(ct_blob);
+  a.ct_page0 = ct_page0;
+  a.n_mt = n_mt(n);
+  a.n_kb = n_kb(k);
+  a.T = T;
+  a.out = out;
+  a.ldo = ldo;
+  a.bias_bf16 = static_cast<const bf16*>(bias_bf16);
+  a.n_valid = n_valid < 0 ? n : n_valid;
+  a.sk_ws = e->gemm_ws;
+  a.sk_ws_floats = e->gemm_ws_floats;
+  a.sk_cnt = e->gemm_cnt;
+  a.sk_cnt_n = e->gemm_cnt_n;
+  KL(launch_gemm(epi, a, map, e->ss));
+  return LS_OK;
+}
 
 int gemv(ls_exec* e, int epi, const GemvPlan& p, const char* w, const float* x, float* out,
          const void* norm_w, const float* bias = nullptr, int n_valid = -1, GemvArgs* extra = nullptr,
@@ -397,9 +400,9 @@ int tp_reduce_add(ls_exec* e, float* dst, long count) {
 }
 
 int resid_gemm(ls_exec* e, const char* w, int n, int k, int T, const CUtensorMap& map, float* dst,
-               const void* bias_bf16 = nullptr) {
-  if (!e->tp_on) return gemm(e, GEMM_RESID_F32, w, n, k, T, map, dst, n, bias_bf16);
-  RC(gemm(e, GEMM_F32, w, n, k, T, map, e->tp_buf, n, bias_bf16));
+               const void* bias_bf16 = nullptr, const char* ct_blob = nullptr, int ct_page0 = 0) {
+  if (!e->tp_on) return gemm(e, GEMM_RESID_F32, w, n, k, T, map, dst, n, bias_bf16, -1, ct_blob, ct_page0);
+  RC(gemm(e, GEMM_F32, w, n, k, T, map, e->tp_buf, n, bias_bf16, -1, ct_blob, ct_page0));
   return tp_reduce_add(e, dst, static_cast<long>(T) * n);
 }
 
@@ -410,13 +413,15 @@ int resid_gemv(ls_exec* e, const GemvPlan& p, const char* w, const float* x, flo
   return tp_reduce_add(e, dst, p.n);
 }
 
-int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L) {
+int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L, const CtView& ct = CtView()) {
   const ls_dims& d = e->d;
   const int T = e->Tv, D = d.vit_d, H = d.vit_heads * d.vit_hd, F = d.vit_ffn;
-  auto part = [&](int i) { return w + L.offset[i]; };
+  auto part = [&](int i) { return ct.blob ? ct.part(L, i) : w + L.offset[i]; };
+  const char* cb = ct.blob;
+  auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
   KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(8), (const bf16*)part(9), e->vit_ln, T, D, D,
                            d.vit_eps, e->ss));
-  RC(gemm(e, GEMM_BF16, part(0), 3 * H, D, T, e->m_vit_ln, e->vit_qkv, 3 * H, part(4)));
+  RC(gemm(e, GEMM_BF16, part(0), 3 * H, D, T, e->m_vit_ln, e->vit_qkv, 3 * H, part(4), -1, cb, pg(0)));
   FlashArgs f = flash_base(T, d.vit_heads, d.vit_heads, d.vit_hd);
   f.q = e->vit_qkv;
   f.q_tok_stride = 3 * H;
@@ -431,20 +436,24 @@ int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L) {
   f.o_head_stride = d.vit_hd;
   f.seg_len = d.vit_tokens_per_image;
   KL(launch_flash_attention(f, e->ss));
-  RC(resid_gemm(e, part(1), D, H, T, e->m_vit_attn, e->vit_h, part(5)));
+  RC(resid_gemm(e, part(1), D, H, T, e->m_vit_attn, e->vit_h, part(5), cb, pg(1)));
   KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(10), (const bf16*)part(11), e->vit_ln, T, D,
                            D, d.vit_eps, e->ss));
-  RC(gemm(e, GEMM_BF16_GELU, part(2), F, D, T, e->m_vit_ln, e->vit_fc1, e->vit_ffn_pad, part(6), F));
-  RC(resid_gemm(e, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, part(7)));
+  RC(gemm(e, GEMM_BF16_GELU, part(2), F, D, T, e->m_vit_ln, e->vit_fc1, e->vit_ffn_pad, part(6), F, cb,
+          pg(2)));
+  RC(resid_gemm(e, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, part(7), cb, pg(3)));
   return LS_OK;
 }
 
-int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
+int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
+                     const CtView& ct = CtView()) {
   const ls_dims& d = e->d;
   const int S = e->S, D = d.lm_d, QN = (d.lm_hq + 2 * d.lm_hkv) * d.lm_hd, AH = d.lm_hq * d.lm_hd;
-  auto part = [&](int i) { return w + L.offset[i]; };
+  auto part = [&](int i) { return ct.blob ? ct.part(L, i) : w + L.offset[i]; };
+  const char* cb = ct.blob;
+  auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
   KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(4), e->lm_norm, S, D, d.lm_eps, e->ss));
-  RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN));
+  RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN, nullptr, -1, cb, pg(0)));
   KL(launch_qk_norm_rope(e->lm_qkv, S, d.lm_hq, d.lm_hkv, d.lm_hd, (const bf16*)part(6),
                          (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], 0, e->lm_q,
                          e->kc(l), e->vc(l), e->cache_stride(), e->ss));
@@ -462,11 +471,11 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l)
   f.o_head_stride = d.lm_hd;
   f.causal = 1;
   KL(launch_flash_attention(f, e->ss));
-  RC(resid_gemm(e, part(1), D, AH, S, e->m_lm_attn, e->lm_h));
+  RC(resid_gemm(e, part(1), D, AH, S, e->m_lm_attn, e->lm_h, nullptr, cb, pg(1)));
   KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(5), e->lm_norm, S, D, d.lm_eps, e->ss));
   RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.lm_ffn, D, S, e->m_lm_norm, e->lm_mlp, d.lm_ffn,
-          nullptr, d.lm_ffn));
-  RC(resid_gemm(e, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h));
+          nullptr, d.lm_ffn, cb, pg(2)));
+  RC(resid_gemm(e, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h, nullptr, cb, pg(3)));
   return LS_OK;
 }
 
@@ -513,15 +522,18 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   return LS_OK;
 }
 
-int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
+int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
+                 const CtView& ct = CtView()) {
   const ls_dims& d = e->d;
   const int T = e->Te, D = d.ex_d, QN = (d.ex_hq + 2 * d.ex_hkv) * d.ex_hd, AH = d.ex_hq * d.ex_hd;
-  auto part = [&](int i) { return w + L.offset[i]; };
+  auto part = [&](int i) { return ct.blob ? ct.part(L, i) : w + L.offset[i]; };
+  const char* cb = ct.blob;
+  auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
   bf16* ek = e->ex_kv;
   bf16* ev = e->ex_kv + static_cast<long>(d.ex_hkv) * T * d.ex_hd;
   const long shift = static_cast<long>(e->ctx) * d.ex_hd;  // store index t, RoPE position ctx + t
   KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(4), e->ex_norm, T, D, d.lm_eps, e->ss));
-  RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN));
+  RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0)));
   KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
                          (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], e->ctx, e->ex_q,
                          ek - shift, ev - shift, T * d.ex_hd, e->ss));
@@ -546,11 +558,11 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l) {
   f.ws = e->flash_ws;
   f.counters = e->flash_cnt;
   KL(launch_flash_attention(f, e->ss));
-  RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h));
+  RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h, nullptr, cb, pg(1)));
   KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
   RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.ex_ffn, D, T, e->m_ex_norm, e->ex_mlp, d.ex_ffn,
-          nullptr, d.ex_ffn));
-  RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h));
+          nullptr, d.ex_ffn, cb, pg(2)));
+  RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, nullptr, cb, pg(3)));
   return LS_OK;
 }
 
@@ -616,11 +628,11 @@ int post_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* i
 int run_layer(ls_exec* e, const Module& m, int phase, int inv, int l, const char* w,
               const CtView& ct = CtView()) {
   switch (m.kind) {
-    case LS_KIND_VIT: return vit_layer(e, w, m.lay);
+    case LS_KIND_VIT: return vit_layer(e, w, m.lay, ct);
     case LS_KIND_LM:
-      return phase == 0 ? lm_prefill_layer(e, w, m.lay, l)
+      return phase == 0 ? lm_prefill_layer(e, w, m.lay, l, ct)
                         : lm_decode_layer(e, w, m.lay, l, e->S + inv, ct);
-    default: return expert_layer(e, w, m.lay, l);
+    default: return expert_layer(e, w, m.lay, l, ct);
   }
 }
 
@@ -636,7 +648,7 @@ int finalize_layout(ls_exec* e) {
   uint64_t scratch = 0;
   for (auto& m : e->mods) {
     e->slot_bytes = std::max(e->slot_bytes, m.ct ? m.ct_stride : m.lay.total);
-    if (m.ct) scratch = std::max(scratch, align_up(m.lay.total, 256) + 256);
+    if (m.ct && !e->ct_fused) scratch = std::max(scratch, align_up(m.lay.total, 256) + 256);
     std::fill(m.resident.begin(), m.resident.end(), nullptr);
   }
   for (auto& m : e->mods) {
@@ -1169,8 +1181,8 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             ++e->launches;  // decode + exception patch
           }
           CtView ct;
-          if (m.ct && m.kind == LS_KIND_LM && ph == 1 && e->ct_fused_decode) {
-            ct = CtView(w, m.lay);  // decode GEMVs read the blob's pages directly
+          if (m.ct && e->ct_fused) {
+            ct = CtView(w, m.lay);  // GEMV / GEMM kernels read the blob's pages directly
           } else if (m.ct) {
             // compact layer (slot or resident block) -> plain layer in the scratch;
             // the next kernel must not start early: its weight producer reads the scratch

@@ -22,35 +22,44 @@
 
 namespace lsb {
 
-template <int BN>
+// CT = true: weights arrive as ECT pages (12 KiB) in a staging ring and 8
+// decoder warps expand each into the swizzled 16 KiB A tile in shared memory
+// (no decoded copy of the layer in HBM, 25 % fewer weight bytes).
+template <int BN, bool CT = false>
 struct GemmCfg {
-  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kStages = CT ? (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5))
+                                    : (BN >= 256 ? 4 : (BN >= 128 ? 6 : 8));
   static constexpr int kABytes = kTileBytes;
   static constexpr int kBBytes = BN * 128;
+  static constexpr int kPBytes = CT ? kEctPageBytes : 0;  // page staging
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kAccCols = BN < 32 ? 32 : BN;     // one accumulator
   static constexpr int kTmemCols = 2 * kAccCols;         // double-buffered (<= 512)
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes +
-                                  128 * 17 * 4 + (2 * kStages + 4) * 8 + 16;
+  static constexpr int kDecWarps = CT ? 8 : 0;
+  static constexpr int kThreads = 192 + 32 * kDecWarps;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * (kStageBytes + kPBytes) +
+                                  128 * 17 * 4 + (3 * kStages + 4) * 8 + 16;
 };
 
 // Persistent: grid = min(#tiles, #SMs); CTA c takes tiles c, c+grid, ...  Tiles
 // are ordered token-tile fastest, so the CTAs working on one weight m-tile at
 // the same time share it through L2 (each weight byte read from HBM ~once).
 // Two TMEM accumulators: the epilogue of tile i overlaps the MMAs of tile i+1.
-template <int BN, int EPI>
-__global__ void __launch_bounds__(192, 1)
+template <int BN, int EPI, bool CT>
+__global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmArgs a) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
   uint8_t* sa = smem;
   uint8_t* sb = smem + Cfg::kStages * Cfg::kABytes;
-  float* stage_f = reinterpret_cast<float*>(sb + Cfg::kStages * Cfg::kBBytes);  // [128][17]
+  uint8_t* spg = sb + Cfg::kStages * Cfg::kBBytes;  // ECT page staging (CT)
+  float* stage_f = reinterpret_cast<float*>(spg + Cfg::kStages * Cfg::kPBytes);  // [128][17]
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_f + 128 * 17);
   uint64_t* empty = full + Cfg::kStages;
-  uint64_t* acc_full = empty + Cfg::kStages;   // [2]
+  uint64_t* dec = empty + Cfg::kStages;          // CT: A tile decoded (kDecWarps arrivals)
+  uint64_t* acc_full = dec + Cfg::kStages;     // [2]
   uint64_t* acc_empty = acc_full + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -65,6 +74,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&dec[s], Cfg::kDecWarps > 0 ? Cfg::kDecWarps : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -87,13 +97,14 @@ __global__ void __launch_bounds__(192, 1)
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int tile = t / ks, sp = t % ks;
         const int mt = tile / n_nt, n0 = (tile % n_nt) * BN;
-        const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kTileBytes;
+        constexpr int kWBytes = CT ? kEctPageBytes : kTileBytes;
+        const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kWBytes;
         const int kb1 = (sp + 1) * n_kb / ks;
         for (int kb = sp * n_kb / ks; kb < kb1; ++kb) {
           if (round) mbar_wait(&empty[s], (round - 1) & 1);
-          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-          bulk_g2s(sa + s * Cfg::kABytes, wt + static_cast<long>(kb) * kTileBytes, kTileBytes,
-                   &full[s]);
+          mbar_arrive_expect_tx(&full[s], kWBytes + Cfg::kBBytes);
+          bulk_g2s(CT ? spg + s * Cfg::kPBytes : sa + s * Cfg::kABytes,
+                   wt + static_cast<long>(kb) * kWBytes, kWBytes, &full[s]);
           tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &full[s]);
           if (++s == Cfg::kStages) {
             s = 0;
@@ -117,6 +128,7 @@ __global__ void __launch_bounds__(192, 1)
         const int sp = t % ks, kb0 = sp * n_kb / ks, kb1 = (sp + 1) * n_kb / ks;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], round & 1);
+          if constexpr (CT) mbar_wait(&dec[s], round & 1);
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
           const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
@@ -133,6 +145,46 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     __syncwarp();
+  } else if (CT && warp >= 6) {  // ---- ECT decoder warps: page -> swizzled A tile ----
+    const EctHeader* h = reinterpret_cast<const EctHeader*>(a.ct_blob);
+    const uint32_t e0p = (h->e0 << 7) | (h->e0 << 23);
+    const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_excoff) + a.ct_page0;
+    const uint32_t* exc = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_exc);
+    const int dt = threadIdx.x - 192;  // 0 .. 32 * kDecWarps - 1
+    int s = 0;
+    uint32_t round = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int tile = t / ks, sp = t % ks;
+      const int mt = tile / n_nt;
+      const int kb1 = (sp + 1) * n_kb / ks;
+      for (int kb = sp * n_kb / ks; kb < kb1; ++kb) {
+        if (round) mbar_wait(&empty[s], (round - 1) & 1);  // the MMA has released A[s]
+        mbar_wait(&full[s], round & 1);
+        const uint8_t* pg = spg + s * Cfg::kPBytes;
+        uint32_t* ta = reinterpret_cast<uint32_t*>(sa + s * Cfg::kABytes);
+        const uint32_t page = static_cast<uint32_t>(mt * n_kb + kb);
+#pragma unroll
+        for (int it = 0; it < 1024 / (32 * Cfg::kDecWarps); ++it) {
+          const uint32_t f = it * 32 * Cfg::kDecWarps + dt;  // fragment
+          const uint2 sm = *reinterpret_cast<const uint2*>(pg + f * 8);
+          const uint32_t nib = *reinterpret_cast<const uint32_t*>(pg + kEctPageWords + f * 4);
+          uint4 w = ect_decode8(sm, nib, e0p);
+          const uint32_t esc = ect_escapes(nib);
+          if (esc) w = ect_patch8(w, esc, page, f * 8, exc_off, exc);
+          ta[ect_plain_word(f * 8 + 0) >> 1] = w.x;
+          ta[ect_plain_word(f * 8 + 2) >> 1] = w.y;
+          ta[ect_plain_word(f * 8 + 4) >> 1] = w.z;
+          ta[ect_plain_word(f * 8 + 6) >> 1] = w.w;
+        }
+        fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dec[s]);
+        if (++s == Cfg::kStages) {
+          s = 0;
+          ++round;
+        }
+      }
+    }
   } else {  // ---- epilogue warps 2..5 ----
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int m = q * 32 + lane;
@@ -319,12 +371,12 @@ int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_
   return ks < 1 ? 1 : ks;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool CT>
 static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI, CT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
@@ -336,28 +388,33 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n) : 1;
   const int units = a.n_mt * ((a.T + BN - 1) / BN) * b.ks;
   dim3 grid(units < nsm ? units : nsm);
-  return launch_k(gemm_kernel<BN, EPI>, grid, dim3(192), Cfg::kSmem, st, map, b);
+  return launch_k(gemm_kernel<BN, EPI, CT>, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, map, b);
 }
 
-template <int BN>
+template <int BN, bool CT>
 static cudaError_t launch_epi(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
   switch (epi) {
-    case GEMM_BF16: return launch_bn<BN, GEMM_BF16>(a, map, st);
-    case GEMM_BF16_GELU: return launch_bn<BN, GEMM_BF16_GELU>(a, map, st);
-    case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32>(a, map, st);
-    case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16>(a, map, st);
-    case GEMM_F32: return launch_bn<BN, GEMM_F32>(a, map, st);
+    case GEMM_BF16: return launch_bn<BN, GEMM_BF16, CT>(a, map, st);
+    case GEMM_BF16_GELU: return launch_bn<BN, GEMM_BF16_GELU, CT>(a, map, st);
+    case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32, CT>(a, map, st);
+    case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16, CT>(a, map, st);
+    case GEMM_F32: return launch_bn<BN, GEMM_F32, CT>(a, map, st);
   }
   return cudaErrorInvalidValue;
 }
 
+template <bool CT>
+static cudaError_t launch_ct(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  switch (gemm_block_n(a.T)) {
+    case 64: return launch_epi<64, CT>(epi, a, map, st);
+    case 128: return launch_epi<128, CT>(epi, a, map, st);
+    default: return launch_epi<256, CT>(epi, a, map, st);
+  }
+}
+
 cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
   if (a.T <= 0) return cudaSuccess;
-  switch (gemm_block_n(a.T)) {
-    case 64: return launch_epi<64>(epi, a, map, st);
-    case 128: return launch_epi<128>(epi, a, map, st);
-    default: return launch_epi<256>(epi, a, map, st);
-  }
+  return a.ct_blob ? launch_ct<true>(epi, a, map, st) : launch_ct<false>(epi, a, map, st);
 }
 
 // ---- tensor-map encoding through the driver entry point (no -lcuda) ----------

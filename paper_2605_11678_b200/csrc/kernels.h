@@ -83,6 +83,9 @@ struct GemmArgs {
   int* sk_cnt;        // [tiles] arrival counters, zero between launches
   int sk_cnt_n;
   int ks;             // set by launch_gemm (callers leave 0)
+  // ECT weights (see GemvArgs): w = the matrix's first page, tile t = page ct_page0 + t
+  const uint8_t* ct_blob;
+  int ct_page0;
 };
 
 int gemm_block_n(int T);

@@ -63,7 +63,8 @@ def _lib():
             "ls_k_gemm": [C.c_int32, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int64, _vp,
                           C.c_int64, _vp, _vp, C.c_int32, _vp],
             "ls_k_gemm_ws": [C.c_int32, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int64, _vp,
-                             C.c_int64, _vp, _vp, C.c_int32, _vp, C.c_int64, _vp, C.c_int32, _vp],
+                             C.c_int64, _vp, _vp, C.c_int32, _vp, C.c_int64, _vp, C.c_int32, _vp,
+                             C.c_int32, _vp],
             "ls_gemm_splits": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32],
             "ls_k_decode_attention": [_vp, _vp],
             "ls_k_flash_attention": [_vp, _vp],
@@ -178,8 +179,10 @@ _SPLITK_WS: dict = {}
 
 
 def gemm(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: torch.Tensor,
-         *, bias=None, n_valid=None, ldo=None, stream=None, splitk: bool = False):
-    """splitk=True passes a split-K workspace (skinny shapes then split K)."""
+         *, bias=None, n_valid=None, ldo=None, stream=None, splitk: bool = False, ct_blob=None,
+         ct_page0: int = 0):
+    """splitk=True passes a split-K workspace (skinny shapes then split K);
+    ct_blob: weights are ECT pages ct_page0.. of that blob (decoded in smem)."""
     n_mt, n_kb = tile_dims(n, k)
     T = x.shape[0]
     bias_f = bias if bias is not None and bias.dtype == torch.float32 else None
@@ -187,7 +190,7 @@ def gemm(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: 
     common = (epi, _p(w_tiled), n_mt, n_kb, _p(x), T, x.stride(0), _p(out),
               ldo if ldo is not None else out.stride(0), _p(bias_f), _p(bias_b),
               n if n_valid is None else n_valid)
-    if not splitk:
+    if not splitk and ct_blob is None:
         _native.check(_lib().ls_k_gemm(*common, _stream(stream)), RuntimeError)
         return
     nsm = num_sms(x.device.index or 0)
@@ -196,7 +199,10 @@ def gemm(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: 
         _SPLITK_WS[key] = (torch.empty(nsm * 128 * 64, dtype=torch.float32, device=x.device),
                            torch.zeros(nsm, dtype=torch.int32, device=x.device))
     ws, cnt = _SPLITK_WS[key]
-    _native.check(_lib().ls_k_gemm_ws(*common, ws.data_ptr(), ws.numel(), cnt.data_ptr(), nsm,
+    if not splitk:
+        ws, cnt = None, None
+    _native.check(_lib().ls_k_gemm_ws(*common, _p(ws), ws.numel() if ws is not None else 0, _p(cnt),
+                                      nsm if cnt is not None else 0, _p(ct_blob), ct_page0,
                                       _stream(stream)), RuntimeError)
 
 

@@ -345,3 +345,30 @@ def test_gemm_split_k(epi, T, n, k):
         _close(outs[1], outs[0], rel=1e-3, abs_=2e-3)
     else:  # bf16 outputs: split and unsplit sums may round to adjacent bf16 values
         _close(outs[1].float(), outs[0].float(), rel=8e-3, abs_=8e-3)
+
+
+# epi: 0 BF16, 1 BF16_GELU, 2 RESID_F32, 3 SILU_BF16, 4 F32
+@pytest.mark.parametrize("epi,T,n,k,splitk,page0", [(0, 1024, 6144, 4096, False, 0), (2, 1024, 4096, 4096, False, 5),
+                                                    (3, 200, 1024, 512, False, 0), (2, 64, 2048, 4096, True, 2),
+                                                    (0, 64, 3072, 2048, True, 0), (1, 3072, 1152, 1152, False, 1)])
+def test_gemm_ect_pages_bit_identical(epi, T, n, k, splitk, page0):
+    """tcgen05 GEMM with ECT weight pages decoded into shared memory by decoder
+    warps == the same GEMM over plain tiles, bit for bit (escapes included)."""
+    from paper_2605_11678_b200 import ect
+    torch.manual_seed(12)
+    w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
+    w[3, :4] = torch.tensor([0.0, 1e-12, -7.0, 3e-30], device=DEV).to(torch.bfloat16)
+    tiled = K.pack_tiled(w)
+    lead = torch.zeros(page0 * ect.PAGE_PLAIN, dtype=torch.uint8, device=DEV)
+    layer = torch.cat([lead, tiled.view(torch.uint8).reshape(-1), torch.ones(32, dtype=torch.uint8, device=DEV)])
+    blob = ect.compress(layer, layer.numel() - 32)
+    assert ect.header(blob)["n_exc"] > 0
+    x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
+    ncol = n // 2 if epi == 3 else n
+    odt = torch.float32 if epi in (2, 4) else torch.bfloat16
+    base = torch.randn(T, ncol, device=DEV).to(odt)
+    a, b = base.clone(), base.clone()
+    K.gemm(epi, tiled, n, k, x, a, n_valid=ncol, splitk=splitk)
+    K.gemm(epi, None, n, k, x, b, n_valid=ncol, splitk=splitk, ct_blob=blob, ct_page0=page0)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
