@@ -18,30 +18,31 @@ namespace lsb {
 
 // ------------------------------- decode ---------------------------------------
 //
-// grid (hkv, n_split), 128 threads.  Each CTA owns <= kDecChunk consecutive
-// positions of one KV head: its K and V rows are contiguous in the cache, so
-// two 1-D bulk copies (TMA engine) land them in shared memory with a single
-// mbarrier wait -- one memory latency per CTA instead of one per position.
-// Scores: one thread per (query head, position) dot product, K rows read with
-// a per-lane rotation (conflict-free); softmax per head by one warp; P.V: one
-// thread per (head, dim pair).  No cross-lane reductions in the inner loops.
-// Per-CTA partials (max, sum, O) are merged by the last CTA of the head in
-// split order (deterministic).
+// grid (hkv, n_split) launched as clusters of n_split CTAs (<= 16) along y, 128
+// threads.  Each CTA owns <= kDecChunk consecutive positions of one KV head:
+// its K and V rows are contiguous in the cache, so two 1-D bulk copies (TMA
+// engine) land them in shared memory with one mbarrier wait.  Scores: one
+// thread per (query head, position) dot product, K rows read with a per-lane
+// rotation (conflict-free); softmax per head by one warp; P.V: one thread per
+// (head, dim pair).  The split partials (max, sum, O) never leave the chip:
+// after a cluster barrier CTA z merges a 1/n_split slice of the G x HD outputs
+// reading every peer's partial over DSMEM, in split order (deterministic).
 
-constexpr int kDecChunk = 64;
+constexpr int kDecChunk = 128;
+constexpr int kDecMaxSplits = 16;
 
 template <int HD, int G>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a) {
+  namespace cg = cooperative_groups;
   constexpr int HP = HD / 2;  // bf16 pairs per row
   extern __shared__ __align__(16) uint8_t dsm[];
   bf16* ks = reinterpret_cast<bf16*>(dsm);
   bf16* vs = ks + kDecChunk * HD;
   float* qs = reinterpret_cast<float*>(vs + kDecChunk * HD);  // [G][HD], pre-scaled
   float* ps = qs + G * HD;                                     // [G][kDecChunk] scores -> probs
-  float* comb = ps + G * kDecChunk;                            // combine scratch
+  float* po = ps + G * kDecChunk;                              // [G][HD] partial O (unnormalised)
   __shared__ __align__(8) uint64_t bar;
-  __shared__ float sm_m[G], sm_l[G];
-  __shared__ int s_last;
+  __shared__ float sm_ml[2 * G];                               // partial max (log2), sum
   pdl_trigger();
   const int kh = blockIdx.x, split = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
     ps[idx] = sc;
   }
   __syncthreads();
-  // ---- softmax per head: warp g (g < G, strided) ----
+  // ---- softmax per head: warp g (strided) ----
   for (int g = warp; g < G; g += 4) {
     float mx = -INFINITY;
     for (int p = lane; p < kDecChunk; p += 32) mx = fmaxf(mx, ps[g * kDecChunk + p]);
@@ -100,13 +101,12 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
     }
     sum = warp_sum(sum);
     if (lane == 0) {
-      sm_m[g] = mx;
-      sm_l[g] = sum;
+      sm_ml[g] = mx;
+      sm_ml[G + g] = sum;
     }
   }
   __syncthreads();
   // ---- O = P V: one thread per (head, dim pair) ----
-  const int W = HD + 2;  // workspace record: M, L, O[HD]
   for (int idx = threadIdx.x; idx < G * HP; idx += 128) {
     const int g = idx / HP, dp = idx % HP;
     const uint32_t* vc = reinterpret_cast<const uint32_t*>(vs) + dp;
@@ -119,86 +119,83 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
       o0 = fmaf(w, bf16_lo(v), o0);
       o1 = fmaf(w, bf16_hi(v), o1);
     }
-    const int h = kh * G + g;
     if (a.n_split == 1) {
-      const float inv = sm_l[g] > 0.f ? 1.0f / sm_l[g] : 0.f;
-      a.out[h * HD + 2 * dp] = o0 * inv;
-      a.out[h * HD + 2 * dp + 1] = o1 * inv;
+      const float l = sm_ml[G + g], inv = l > 0.f ? 1.0f / l : 0.f;
+      a.out[(kh * G + g) * HD + 2 * dp] = o0 * inv;
+      a.out[(kh * G + g) * HD + 2 * dp + 1] = o1 * inv;
     } else {
-      float* rec = a.ws + (static_cast<long>(h) * a.n_split + split) * W;
-      rec[2 + 2 * dp] = o0;
-      rec[3 + 2 * dp] = o1;
-      if (dp == 0) {
-        rec[0] = sm_m[g];
-        rec[1] = sm_l[g];
-      }
+      po[g * HD + 2 * dp] = o0;
+      po[g * HD + 2 * dp + 1] = o1;
     }
   }
   if (a.n_split == 1) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[kh], 1) == a.n_split - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // ---- last CTA: coalesced load of all G*n_split records, then merge in split order ----
-  float* recs = comb;  // [G][n_split][W]  (fits: host caps n_split * G * W floats)
-  const float* base = a.ws + static_cast<long>(kh * G) * a.n_split * W;
-  const int total = G * a.n_split * W;
-  // 16 independent loads in flight per thread per round (L2 latency-bound otherwise)
-  for (int i0 = 0; i0 < total; i0 += 16 * 128) {
-    float v[16];
+  // ---- merge across the cluster (DSMEM) ----
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();
+  const int S = a.n_split;
+  const int lo = split * G * HD / S, hi = (split + 1) * G * HD / S;
+  for (int i = lo + threadIdx.x; i < hi; i += 128) {
+    const int g = i / HD;
+    float mz[kDecMaxSplits], M = -INFINITY;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * 128 + threadIdx.x;
-      v[u] = i < total ? __ldcg(base + i) : 0.f;
+    for (int z = 0; z < kDecMaxSplits; ++z) {
+      mz[z] = z < S ? cluster.map_shared_rank(sm_ml, z)[g] : -INFINITY;
+      M = fmaxf(M, mz[z]);
     }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * 128 + threadIdx.x;
-      if (i < total) recs[i] = v[u];
-    }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-    const int g = idx / HD, d = idx % HD, h = kh * G + g;
-    const float* r = recs + g * a.n_split * W;
-    float M = -INFINITY;
-    for (int sp = 0; sp < a.n_split; ++sp) M = fmaxf(M, r[sp * W]);
     float L = 0.f, O = 0.f;
-    for (int sp = 0; sp < a.n_split; ++sp) {
-      const float ms = r[sp * W];
-      if (ms == -INFINITY) continue;
-      const float f = exp2f(ms - M);
-      L += r[sp * W + 1] * f;
-      O += r[sp * W + 2 + d] * f;
+#pragma unroll
+    for (int z = 0; z < kDecMaxSplits; ++z) {
+      if (z < S && mz[z] != -INFINITY) {
+        const float f = exp2f(mz[z] - M);
+        L = fmaf(cluster.map_shared_rank(sm_ml, z)[G + g], f, L);
+        O = fmaf(cluster.map_shared_rank(po, z)[i], f, O);
+      }
     }
-    a.out[h * HD + d] = O / L;
+    a.out[kh * G * HD + i] = L > 0.f ? O / L : 0.f;
   }
-  if (threadIdx.x == 0) a.counters[kh] = 0;
+  cluster.sync();  // peers keep their shared memory until every slice is merged
 }
 
-int decode_attn_splits(int n_ctx) { return (n_ctx + kDecChunk - 1) / kDecChunk; }
+int decode_attn_splits(int n_ctx) {
+  const int s = (n_ctx + 63) / 64;
+  return s < kDecMaxSplits ? (s < 1 ? 1 : s) : kDecMaxSplits;
+}
 
 template <int HD, int G>
 static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
-  const size_t kv = 2ull * kDecChunk * HD * 2 + 4ull * G * (HD + kDecChunk);
-  const size_t comb = 4ull * static_cast<size_t>(G) * a.n_split * (HD + 2);
-  const size_t smem = kv + comb;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const size_t smem = 2ull * kDecChunk * HD * 2 + 4ull * G * (2 * HD + kDecChunk);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_k(decode_attn_kernel<HD, G>, dim3(a.hkv, a.n_split), dim3(128), smem, st, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.hkv, a.n_split);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = take_launch_pdl() ? 1 : 0;
+  la[1].id = cudaLaunchAttributeClusterDimension;
+  la[1].val.clusterDim.x = 1;
+  la[1].val.clusterDim.y = static_cast<unsigned>(a.n_split);
+  la[1].val.clusterDim.z = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = a.n_split > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, decode_attn_kernel<HD, G>, a);
 }
 
 template <int HD>
 static cudaError_t decode_hd(const DecodeAttnArgs& a, cudaStream_t st) {
-  if ((a.n_ctx + a.n_split - 1) / a.n_split > kDecChunk) return cudaErrorInvalidValue;
+  if (a.n_split < 1 || a.n_split > kDecMaxSplits || (a.n_ctx + a.n_split - 1) / a.n_split > kDecChunk)
+    return cudaErrorInvalidValue;
   switch (a.hq / a.hkv) {
     case 1: return decode_launch<HD, 1>(a, st);
     case 2: return decode_launch<HD, 2>(a, st);

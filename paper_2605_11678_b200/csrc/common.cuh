@@ -128,6 +128,14 @@ __device__ __forceinline__ uint32_t ect_escapes(uint32_t nib) {
   const uint32_t t = ((nib & 0x77777777u) + 0x11111111u) & nib & 0x88888888u;
   return t >> 3;
 }
+// Escaped words default to exponent 0 (zeros / subnormals have no exc entry).
+__device__ __forceinline__ uint4 ect_zero_escapes(uint4 w, uint32_t t) {
+  uint32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if ((t >> (4 * k)) & 1u) v[k >> 1] &= ~(0x7F80u << (16 * (k & 1)));
+  return make_uint4(v[0], v[1], v[2], v[3]);
+}
 // Slow path: t = ect_escapes(nib) of the chunk starting at page word `word0`;
 // true exponents come from the page's exception list.
 static __device__ __noinline__ uint4 ect_patch8(uint4 w, uint32_t t, uint32_t page, uint32_t word0,

@@ -13,29 +13,38 @@
 
 namespace lsb {
 
+// Pages [page0, page0 + n_pages) -> plain tiles at out (page0 lands at out[0]);
+// with_tail also copies the raw vectors after them (whole-layer decode).
 __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restrict__ blob,
-                                                         uint8_t* __restrict__ out) {
+                                                         uint32_t page0, uint32_t n_pages,
+                                                         int with_tail, uint8_t* __restrict__ out) {
   __shared__ __align__(16) uint32_t tile[kTileBytes / 4];
   pdl_trigger();
   pdl_wait();  // `out` (the decode scratch) is read by the previous layer's kernels
   const EctHeader* h = reinterpret_cast<const EctHeader*>(blob);
   const uint32_t e0p = (h->e0 << 7) | (h->e0 << 23);
-  const uint8_t* pages = blob + h->off_pages;
+  const uint8_t* pages = blob + h->off_pages + static_cast<uint64_t>(page0) * kEctPageBytes;
   // one page per CTA iteration: fragments decoded into the plain tile image in
   // shared memory (pair stores are bank-conflict-free thanks to the 128 B
   // swizzle), then streamed out as coalesced 16-byte stores
-  for (uint32_t page = blockIdx.x; page < h->n_pages; page += gridDim.x) {
+  uint32_t pos[4];  // plain-tile u32 slots of fragment threadIdx.x's word pairs
+#pragma unroll
+  for (int p = 0; p < 4; ++p) pos[p] = ect_plain_word(threadIdx.x * 8 + 2 * p) >> 1;
+  for (uint32_t page = blockIdx.x; page < n_pages; page += gridDim.x) {
     const uint8_t* pg = pages + static_cast<uint64_t>(page) * kEctPageBytes;
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const uint32_t f = it * 256 + threadIdx.x;  // fragment index in the page
       const uint2 sm = __ldcs(reinterpret_cast<const uint2*>(pg) + f);
       const uint32_t nib = __ldcs(reinterpret_cast<const uint32_t*>(pg + kEctPageWords) + f);
-      const uint4 w = ect_decode8(sm, nib, e0p);
-      tile[ect_plain_word(f * 8 + 0) >> 1] = w.x;
-      tile[ect_plain_word(f * 8 + 2) >> 1] = w.y;
-      tile[ect_plain_word(f * 8 + 4) >> 1] = w.z;
-      tile[ect_plain_word(f * 8 + 6) >> 1] = w.w;
+      uint4 w = ect_decode8(sm, nib, e0p);
+      const uint32_t esc = ect_escapes(nib);
+      if (esc) w = ect_zero_escapes(w, esc);  // exponent 0 unless the scatter below patches it
+      uint32_t* tb = tile + it * 1024;  // fragment + 256 = 2 row blocks (32 rows) lower
+      tb[pos[0]] = w.x;
+      tb[pos[1]] = w.y;
+      tb[pos[2]] = w.z;
+      tb[pos[3]] = w.w;
     }
     __syncthreads();
     uint4* dst = reinterpret_cast<uint4*>(out + static_cast<uint64_t>(page) * kTileBytes);
@@ -44,6 +53,7 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
       dst[it * 256 + threadIdx.x] = reinterpret_cast<const uint4*>(tile)[it * 256 + threadIdx.x];
     __syncthreads();
   }
+  if (!with_tail) return;
   // raw tail (vectors), whole 16-byte chunks
   const uint64_t tail = (h->total - h->mat_bytes + 15) / 16;
   const uint4* src = reinterpret_cast<const uint4*>(blob + h->off_tail);
@@ -55,14 +65,16 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
 
 // Escaped words: one thread per exception, page found by binary search in exc_off.
 __global__ void __launch_bounds__(256) ect_patch_kernel(const uint8_t* __restrict__ blob,
+                                                        uint32_t page0, uint32_t n_pages,
                                                         uint16_t* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   const EctHeader* h = reinterpret_cast<const EctHeader*>(blob);
-  const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(blob + h->off_excoff);
+  const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(blob + h->off_excoff) + page0;
   const uint32_t* exc = reinterpret_cast<const uint32_t*>(blob + h->off_exc);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h->n_exc; i += gridDim.x * blockDim.x) {
-    uint32_t lo = 0, hi = h->n_pages;  // largest page with exc_off[page] <= i
+  const uint32_t e_lo = exc_off[0], e_hi = exc_off[n_pages];
+  for (uint32_t i = e_lo + blockIdx.x * blockDim.x + threadIdx.x; i < e_hi; i += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n_pages;  // largest page with exc_off[page] <= i
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
       if (exc_off[mid] <= i) lo = mid;
@@ -74,12 +86,22 @@ __global__ void __launch_bounds__(256) ect_patch_kernel(const uint8_t* __restric
   }
 }
 
-cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st) {
-  cudaError_t e = launch_k(ect_decode_kernel, dim3(6 * num_sms), dim3(256), 0, st, blob,
-                           static_cast<uint8_t*>(out));
+cudaError_t launch_ect_decode_pages(const uint8_t* blob, uint32_t page0, uint32_t n_pages,
+                                    bool with_tail, void* out, int num_sms, cudaStream_t st) {
+  cudaError_t e = launch_k(ect_decode_kernel, dim3(6 * num_sms), dim3(256), 0, st, blob, page0,
+                           n_pages, with_tail ? 1 : 0, static_cast<uint8_t*>(out));
   if (e != cudaSuccess) return e;
   set_launch_pdl(true);  // the scatter follows the decode kernel directly
-  return launch_k(ect_patch_kernel, dim3(num_sms), dim3(256), 0, st, blob, static_cast<uint16_t*>(out));
+  return launch_k(ect_patch_kernel, dim3(num_sms), dim3(256), 0, st, blob, page0, n_pages,
+                  static_cast<uint16_t*>(out));
+}
+
+cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st) {
+  const EctHeader* h = nullptr;
+  EctHeader hh;
+  if (cudaMemcpy(&hh, blob, sizeof(hh), cudaMemcpyDefault) != cudaSuccess) return cudaErrorInvalidValue;
+  h = &hh;
+  return launch_ect_decode_pages(blob, 0, h->n_pages, true, out, num_sms, st);
 }
 
 }  // namespace lsb

@@ -328,6 +328,18 @@ int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensor
          long ldo, const void* bias_bf16 = nullptr, int n_valid = -1, const char* ct_blob = nullptr,
          int ct_page0 = 0) {
   GemmArgs a{};
+  if (ct_blob && (T + gemm_block_n(T) - 1) / gemm_block_n(T) > 1) {
+    // several token tiles would each re-decode every page inside the GEMM: expand
+    // this matrix's pages once into the decode scratch and run the plain GEMM on it
+    // (the GEMM then must not prefetch weights before the decode has finished)
+    KL(launch_ect_decode_pages(reinterpret_cast<const uint8_t*>(ct_blob), static_cast<uint32_t>(ct_page0),
+                               static_cast<uint32_t>(n_mt(n)) * static_cast<uint32_t>(n_kb(k)), false,
+                               e->scratch, e->nsm, e->ss));
+    ++e->launches;  // decode + exception scatter
+    e->pdl_ok = false;
+    w = e->scratch;
+    ct_blob = nullptr;
+  }
   a.w = reinterpret_cast<const uint8_t*>(w);
   a.ct_blob = reinterpret_cast<const uint8_t*>(ct_blob);
   a.ct_page0 = ct_page0;
@@ -649,6 +661,9 @@ int finalize_layout(ls_exec* e) {
   for (auto& m : e->mods) {
     e->slot_bytes = std::max(e->slot_bytes, m.ct ? m.ct_stride : m.lay.total);
     if (m.ct && !e->ct_fused) scratch = std::max(scratch, align_up(m.lay.total, 256) + 256);
+    // fused mode: multi-token-tile GEMMs (ViT, LM prefill) expand one matrix at a time
+    if (m.ct && e->ct_fused)
+      for (int i = 0; i < 4; ++i) scratch = std::max(scratch, align_up(m.lay.bytes[i], 256));
     std::fill(m.resident.begin(), m.resident.end(), nullptr);
   }
   for (auto& m : e->mods) {
@@ -1186,7 +1201,9 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
           } else if (m.ct) {
             // compact layer (slot or resident block) -> plain layer in the scratch;
             // the next kernel must not start early: its weight producer reads the scratch
-            KL(launch_ect_decode(reinterpret_cast<const uint8_t*>(w), e->scratch, e->nsm, e->ss));
+            KL(launch_ect_decode_pages(reinterpret_cast<const uint8_t*>(w), 0,
+                                       static_cast<uint32_t>((m.lay.offset[3] + m.lay.bytes[3]) / 16384),
+                                       true, e->scratch, e->nsm, e->ss));
             ++e->launches;  // decode + exception scatter
             e->pdl_ok = false;
             w = e->scratch;

@@ -151,6 +151,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
     const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_excoff) + a.ct_page0;
     const uint32_t* exc = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_exc);
     const int dt = threadIdx.x - 192;  // 0 .. 32 * kDecWarps - 1
+    // u32 slots of this thread's 4 word pairs in the plain tile for fragment dt; fragment
+    // dt + it * 32 * kDecWarps sits 2 * it * kDecWarps / 8 row blocks (x 32 rows) lower
+    uint32_t pos[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) pos[p] = ect_plain_word(dt * 8 + 2 * p) >> 1;
+    constexpr uint32_t kItStride = (32u * Cfg::kDecWarps / 128u) * 16u * 32u;  // u32 per iteration
     int s = 0;
     uint32_t round = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -171,10 +177,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
           uint4 w = ect_decode8(sm, nib, e0p);
           const uint32_t esc = ect_escapes(nib);
           if (esc) w = ect_patch8(w, esc, page, f * 8, exc_off, exc);
-          ta[ect_plain_word(f * 8 + 0) >> 1] = w.x;
-          ta[ect_plain_word(f * 8 + 2) >> 1] = w.y;
-          ta[ect_plain_word(f * 8 + 4) >> 1] = w.z;
-          ta[ect_plain_word(f * 8 + 6) >> 1] = w.w;
+          uint32_t* tb = ta + it * kItStride;
+          tb[pos[0]] = w.x;
+          tb[pos[1]] = w.y;
+          tb[pos[2]] = w.z;
+          tb[pos[3]] = w.w;
         }
         fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
         __syncwarp();
@@ -360,10 +367,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
 
 int gemm_block_n(int T) { return T <= 64 ? 64 : (T <= 256 ? 128 : 256); }
 
-int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n) {
+int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n, bool ct) {
   const int bn = gemm_block_n(T);
   const int tiles = n_mt * ((T + bn - 1) / bn);
-  if (tiles * 4 > num_sms || tiles > cnt_n) return 1;  // >= 4 splits or not worth the fix-up
+  // plain tiles: >= 4 splits or not worth the fix-up; ECT pages: the in-CTA
+  // decode is the bottleneck of skinny shapes, so spreading it pays from 2 splits
+  if (tiles * (ct ? 2 : 4) > num_sms || tiles > cnt_n) return 1;
   int ks = num_sms / tiles;                 // one wave of units: all co-resident (fix-up waits)
   if (ks > n_kb / 4) ks = n_kb / 4;         // >= 4 k-blocks (256 of K) per unit
   if (ks > 16) ks = 16;                     // the fix-up loads <= 16 partials per token at once
@@ -385,7 +394,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   GemmArgs b = a;
-  b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n) : 1;
+  b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n, CT) : 1;
   const int units = a.n_mt * ((a.T + BN - 1) / BN) * b.ks;
   dim3 grid(units < nsm ? units : nsm);
   return launch_k(gemm_kernel<BN, EPI, CT>, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, map, b);

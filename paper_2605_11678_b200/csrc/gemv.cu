@@ -15,6 +15,8 @@
 //     in a workspace slot per contributor and the last arriving CTA sums them
 //     in contributor order (bit-reproducible), then runs the fused epilogue
 //     (residual add / SiLU*up / q,k-norm + RoPE + KV-cache append / argmax).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemv_common.cuh"
 #include "kernels.h"
@@ -29,11 +31,18 @@ template <bool CT>
 __host__ __device__ inline int gemv_stages(int n_kb) {
   constexpr int stage = CT ? kEctPageBytes : kTileBytes;
   constexpr int cap = CT ? 16 : 12;
-  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 1536) / stage;
+  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 2560) / stage;
   return avail > cap ? cap : avail;
 }
-constexpr int kGemvConsumers = 512;  // 16 warps: 8 row blocks x 2 k-halves of every tile
-constexpr int kGemvThreads = kGemvConsumers + 32;
+// NW consumer warps = 8 row blocks x NW/8 k-parts of every tile (16: two k-steps
+// per warp, 32: one).  The RMSNorm reduction always uses the first 16 warps.
+template <int NW>
+struct GemvShape {
+  static constexpr int kConsumers = NW * 32;
+  static constexpr int kThreads = kConsumers + 32;
+  static constexpr int kQ = NW / 8;  // k-parts per tile
+};
+constexpr int kNormThreads = 512;
 
 __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
   return static_cast<int>(((t + 1) * G - 1) / T);
@@ -52,8 +61,10 @@ __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
 // a lane's four B words for two k-steps are one 16-byte load, and an ECT page
 // keeps a lane's two fragments for its k-step pair adjacent (one 16-byte +
 // one 8-byte load).  Plain and ECT tiles give bit-identical results.
-template <int EPI, bool CT>
-__global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
+template <int EPI, bool CT, int NW>
+__global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const GemvArgs a) {
+  constexpr int kGemvConsumers = GemvShape<NW>::kConsumers;
+  constexpr int kQ = GemvShape<NW>::kQ;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kStage = CT ? kEctPageBytes : kTileBytes;
   const int K = a.n_kb * kTileCols;
@@ -61,8 +72,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   const int NS = gemv_stages<CT>(a.n_kb);
   // x as bf16x2 B words: [kb][half h][column hi|lo][t4][b0(2h), b1(2h), b0(2h+1), b1(2h+1)]
   uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NS * kStage);
-  float* red = reinterpret_cast<float*>(xq + K);  // [2][128]: k-half 0, k-half 1
-  float* scratch = red + 2 * kTileRows;  // 16 floats for block reductions
+  float* red = reinterpret_cast<float*>(xq + K);  // [kQ][128]: one slice per k-part
+  float* scratch = red + kQ * kTileRows;  // 16 floats for block reductions
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
   uint64_t* empty = full + kGemvMaxStages;
   int* flag = reinterpret_cast<int*>(empty + kGemvMaxStages);
@@ -119,16 +130,17 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   float rstd = 1.f;
   if (a.norm_w) {
     float ss = 0.f;
-    for (int k = tid; k < K; k += kGemvConsumers) {
-      const float v = a.x[k];
-      ss = fmaf(v, v, ss);
-    }
+    if (tid < kNormThreads)
+      for (int k = tid; k < K; k += kNormThreads) {
+        const float v = a.x[k];
+        ss = fmaf(v, v, ss);
+      }
     ss = warp_sum(ss);
-    if (lane == 0) scratch[warp] = ss;
+    if (lane == 0 && warp < kNormThreads / 32) scratch[warp] = ss;
     named_bar(1, kGemvConsumers);
     float tot = 0.f;
 #pragma unroll
-    for (int w = 0; w < kGemvConsumers / 32; ++w) tot += scratch[w];
+    for (int w = 0; w < kNormThreads / 32; ++w) tot += scratch[w];
     rstd = rsqrtf(tot / K + a.eps);
   }
   // x -> (hi, lo) bf16 pairs, scattered into the B-word layout above
@@ -153,7 +165,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   float acc[4] = {0.f, 0.f, 0.f, 0.f};  // mma C: rows g, g+8 x columns (hi, lo) in lanes t4 == 0
   int cur_mt = t0 < t1 ? static_cast<int>(t0 / a.n_kb) : -1;
 
-  const int rb = warp & 7, kh = warp >> 3;  // row block, k-half
+  const int rb = warp & 7, kh = warp >> 3;  // row block, k-part
   auto flush = [&](int mt) {
     if (t4 == 0) {
       red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
@@ -162,7 +174,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = 0.f;
     named_bar(1, kGemvConsumers);
-    if (tid < kTileRows) red[tid] += red[kTileRows + tid];
+    if (tid < kTileRows) {
+      float v = red[tid];
+#pragma unroll
+      for (int q = 1; q < kQ; ++q) v += red[q * kTileRows + tid];
+      red[tid] = v;
+    }
     named_bar(1, kGemvConsumers);
     const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
     const int c_first = cta_of_tile(first, G, T);
@@ -198,12 +215,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   };
 
   // B words: column g = 0 -> hi, g = 1 -> lo, other columns zero
-  const uint32_t* xb = xq + kh * 32 + (g & 1) * 16 + t4 * 4;
+  const uint32_t* xb = xq + (kQ == 2 ? kh : kh >> 1) * 32 + (g & 1) * 16 + t4 * 4 +
+                       (kQ == 2 ? 0 : (kh & 1) * 2);
   const bool bcol = g < 2;
   // ldmatrix.x4 row address of this lane inside a plain tile (k-step added per use)
   const int lr = rb * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
   const int lc = lane >> 4;  // 0: k 0-7 of the step, 1: k 8-15
-  const int f0 = ((rb * 2 + kh) * 32 + lane) * 2;  // ECT: this lane's fragments for k-steps 2kh, 2kh+1
+  // ECT: this lane's fragments (k-steps 2kh, 2kh+1 for kQ = 2; k-step kh for kQ = 4)
+  const int f0 = kQ == 2 ? ((rb * 2 + kh) * 32 + lane) * 2 : ((rb * 2 + (kh >> 1)) * 32 + lane) * 2 + (kh & 1);
   int kb = t0 < t1 ? static_cast<int>(t0 - static_cast<long>(cur_mt) * a.n_kb) : 0;
   int s = 0;
   uint32_t round = 0;
@@ -217,6 +236,22 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
     mbar_wait(&full[s], round & 1);
     const uint8_t* st = stages + s * kStage;
+    if constexpr (kQ == 4) {  // one k-step per warp and tile
+      uint2 bw = make_uint2(0u, 0u);
+      if (bcol) bw = *reinterpret_cast<const uint2*>(xb + kb * 64);
+      uint32_t af[4];
+      if constexpr (CT) {
+        const uint2 sm = *reinterpret_cast<const uint2*>(st + f0 * 8);
+        const uint32_t nib = *reinterpret_cast<const uint32_t*>(st + kEctPageWords + f0 * 4);
+        uint4 w0 = ect_decode8(sm, nib, e0p);
+        const uint32_t esc = ect_escapes(nib);
+        if (esc) w0 = ect_patch8(w0, esc, tile, f0 * 8, exc_off, exc);
+        af[0] = w0.x; af[1] = w0.y; af[2] = w0.z; af[3] = w0.w;
+      } else {
+        ldsm_x4(af, st + lr * 128 + (((2 * kh + lc) ^ (lr & 7)) << 4));
+      }
+      mma_bf16_16816(acc, af, bw.x, bw.y);
+    } else {
     uint4 bw = make_uint4(0u, 0u, 0u, 0u);
     if (bcol) bw = *reinterpret_cast<const uint4*>(xb + kb * 64);
     uint32_t af[2][4];
@@ -238,6 +273,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
     mma_bf16_16816(acc, af[0], bw.x, bw.y);
     mma_bf16_16816(acc, af[1], bw.z, bw.w);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     ++kb;
@@ -269,37 +305,50 @@ int gemv_max_contrib(int n_mt, int n_kb, int grid) {
 template <bool CT>
 static size_t gemv_smem(int n_kb) {
   return static_cast<size_t>(gemv_stages<CT>(n_kb)) * (CT ? kEctPageBytes : kTileBytes) +
-         static_cast<size_t>(n_kb) * kTileCols * 4 + 2 * kTileRows * 4 + 16 * 4 +
+         static_cast<size_t>(n_kb) * kTileCols * 4 + 4 * kTileRows * 4 + 16 * 4 +
          2 * kGemvMaxStages * 8 + 16;
 }
 
-template <int EPI, bool CT>
+template <int EPI, bool CT, int NW>
 static cudaError_t launch_t(const GemvArgs& a, int grid, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<EPI, CT>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<EPI, CT, NW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_k(gemv_kernel<EPI, CT>, dim3(grid), dim3(kGemvThreads), gemv_smem<CT>(a.n_kb), st, a);
+  return launch_k(gemv_kernel<EPI, CT, NW>, dim3(grid), dim3(GemvShape<NW>::kThreads),
+                  gemv_smem<CT>(a.n_kb), st, a);
 }
 
-template <bool CT>
+template <bool CT, int NW>
 static cudaError_t launch_ct(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
   if (gemv_smem<CT>(a.n_kb) > 227 * 1024) return cudaErrorInvalidValue;
   switch (epi) {
-    case GEMV_F32: return launch_t<GEMV_F32, CT>(a, grid, st);
-    case GEMV_RESID: return launch_t<GEMV_RESID, CT>(a, grid, st);
-    case GEMV_SILU: return launch_t<GEMV_SILU, CT>(a, grid, st);
-    case GEMV_QKV: return launch_t<GEMV_QKV, CT>(a, grid, st);
-    case GEMV_ARGMAX: return launch_t<GEMV_ARGMAX, CT>(a, grid, st);
+    case GEMV_F32: return launch_t<GEMV_F32, CT, NW>(a, grid, st);
+    case GEMV_RESID: return launch_t<GEMV_RESID, CT, NW>(a, grid, st);
+    case GEMV_SILU: return launch_t<GEMV_SILU, CT, NW>(a, grid, st);
+    case GEMV_QKV: return launch_t<GEMV_QKV, CT, NW>(a, grid, st);
+    case GEMV_ARGMAX: return launch_t<GEMV_ARGMAX, CT, NW>(a, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
+// consumer warps (16 or 32; LS_GEMV_WARPS=32 selects 32 for A/B runs -- plain and
+// ECT must use the same count to stay bit-identical)
+static int gemv_warps() {
+  static const int w = [] {
+    const char* v = getenv("LS_GEMV_WARPS");
+    return (v && atoi(v) == 32) ? 32 : 16;
+  }();
+  return w;
+}
+
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
-  return a.ct_blob ? launch_ct<true>(epi, a, grid, st) : launch_ct<false>(epi, a, grid, st);
+  if (gemv_warps() == 32)
+    return a.ct_blob ? launch_ct<true, 32>(epi, a, grid, st) : launch_ct<false, 32>(epi, a, grid, st);
+  return a.ct_blob ? launch_ct<true, 16>(epi, a, grid, st) : launch_ct<false, 16>(epi, a, grid, st);
 }
 
 }  // namespace lsb

@@ -90,7 +90,7 @@ struct GemmArgs {
 
 int gemm_block_n(int T);
 // split factor launch_gemm picks for a shape (1 = no split)
-int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n);
+int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n, bool ct = false);
 cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st);
 // Encode a row-major bf16 [rows x cols] tensor map with box {64, box_rows}, SWIZZLE_128B.
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -110,7 +110,7 @@ struct DecodeAttnArgs {
   int n_split;
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
-// splits so every CTA covers <= 64 positions (the kernel requires it)
+// splits (one cluster of <= 16 CTAs per KV head, <= 128 positions per CTA)
 int decode_attn_splits(int n_ctx);
 
 struct FlashArgs {
@@ -206,7 +206,12 @@ struct EctHeader {
 };
 static_assert(sizeof(EctHeader) == 128, "ECT header is 128 bytes");
 // blob -> plain layer bytes (whole 16-byte chunks: out needs a16(total) bytes);
-// a decode kernel then an exception scatter (PDL-chained)
+// a decode kernel then an exception scatter (PDL-chained).  Reads the header
+// synchronously (test / tool entry point).
 cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st);
+// pages [page0, page0 + n_pages) of a device blob -> plain tiles at out (+ the
+// raw vectors when with_tail, for a whole-layer decode)
+cudaError_t launch_ect_decode_pages(const uint8_t* blob, uint32_t page0, uint32_t n_pages,
+                                    bool with_tail, void* out, int num_sms, cudaStream_t st);
 
 }  // namespace lsb

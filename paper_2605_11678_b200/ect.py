@@ -26,8 +26,9 @@ Blob (all offsets 16-byte aligned, csrc/kernels.h EctHeader):
 The code window is contiguous: code c < 15 means exponent e0 + c, where
 [e0, e0 + 14] is the 15-exponent window holding the most words, so decoding
 is integer arithmetic (no table).  Escaped words (exponent outside the
-window, e.g. zeros) keep sign+mantissa in the page and take their exponent
-from exc.  Decoding is bit-exact.
+window) keep sign+mantissa in the page and take their exponent from exc; an
+escaped word with no exc entry has exponent 0 (zeros and subnormals, e.g. the
+tile padding, cost no exception entries).  Decoding is bit-exact.
 """
 from __future__ import annotations
 
@@ -94,7 +95,9 @@ def compress(buf: torch.Tensor, mat_bytes: int) -> torch.Tensor:
     sm = (((w >> 8) & 0x80) | (w & 0x7F)).to(torch.uint8).view(n_pages, PAGE_WORDS)
     nib = (code[0::2] | (code[1::2] << 4)).to(torch.uint8).view(n_pages, PAGE_WORDS // 2)
     pages = torch.cat([sm, nib], dim=1).reshape(-1)
-    esc = torch.nonzero(code == 15).flatten()
+    # escapes of exponent 0 (zeros / subnormals, e.g. tile padding) are implicit:
+    # an escaped word without an exc entry decodes with exponent 0
+    esc = torch.nonzero((code == 15) & (e != 0)).flatten()
     n_exc = esc.numel()
     page_of = esc // PAGE_WORDS
     exc = (((esc % PAGE_WORDS) << 8) | e[esc]).to(torch.int32)

@@ -184,8 +184,9 @@ def test_gemm_padded_k_and_n():
     _close(out2, out[:, :n].float() @ w2.float().t(), rel=1.5e-2, abs_=2e-2)
 
 
-@pytest.mark.parametrize("hq,hkv,hd,n_ctx,n_split", [(32, 8, 128, 1045, 18), (8, 2, 32, 24, 1),
-                                                     (32, 8, 128, 7, 4)])
+@pytest.mark.parametrize("hq,hkv,hd,n_ctx,n_split", [(32, 8, 128, 1045, 16), (8, 2, 32, 24, 1),
+                                                     (32, 8, 128, 7, 4), (32, 8, 128, 1045, 9),
+                                                     (16, 8, 64, 300, 3)])
 def test_decode_attention(hq, hkv, hd, n_ctx, n_split):
     torch.manual_seed(7)
     max_ctx = 1100

@@ -165,7 +165,7 @@ def main():
         res.append(bench_gemv_ect(6144, 4096, K.GEMV_F32))
         res.append(bench_ect_decode())
     if args.only in ("all", "attn"):
-        for s in (18, 66):
+        for s in (16, 9):
             res.append(bench_decode_attn(n_split=s))
     if args.only in ("all", "gemm"):
         res.append(bench_gemm(1024, 6144, 4096))
