@@ -272,7 +272,8 @@ typedef struct ls_run_io {
 
 typedef struct ls_run_opts {
   ls_simconfig cfg;
-  int32_t record_timeline; /* 1: per-layer CUDA event timestamps */
+  int32_t record_timeline; /* 1: per-layer CUDA event timestamps; 2: one EXE span per
+                              invocation (layer = -1), PDL chaining left intact */
 } ls_run_opts;
 
 /* One inference.  total_ms: device time from the first layer transfer /

@@ -1109,7 +1109,10 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   const bool seq = opts->cfg.mode == LS_MODE_SEQUENTIAL;
   const bool barrier = seq || !opts->cfg.cross_invocation_prefetch;
   const int nsl = std::max(1, std::min(opts->cfg.slot_count, e->n_slots));
-  const bool timing = opts->record_timeline && events;
+  // 1: per-layer DMA / EXE events (the Timeline); 2: one EXE span per invocation
+  // (events only around the layer loop, so PDL chaining inside it is untouched)
+  const bool coarse = opts->record_timeline == 2 && events;
+  const bool timing = opts->record_timeline == 1 && events;
   if (e->tp_on && !e->comm)
     return set_error(LS_ERR_VALUE, "tensor-parallel executor has no communicator (ls_exec_set_tp)");
   for (auto& m : e->mods)
@@ -1120,7 +1123,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   int64_t need = 0;
   for (auto& m : e->mods)
     for (int r : m.phase_reps) need += 4ll * r * m.layers;
-  if (timing) {
+  if (timing || coarse) {
     if (capacity * 2 < need) return set_error(LS_ERR_VALUE, "event buffer too small");
     while (static_cast<int64_t>(e->tev.size()) < need) {
       cudaEvent_t v;
@@ -1132,7 +1135,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
     int engine, module, phase, inv, layer, ev0, ev1;
   };
   std::vector<Rec> recs;
-  if (timing) recs.reserve(static_cast<size_t>(need / 2));
+  if (timing || coarse) recs.reserve(static_cast<size_t>(need / 2));
   int next_ev = 0;
   auto tick = [&](cudaStream_t s) {
     cudaEventRecord(e->tev[next_ev], s);
@@ -1162,6 +1165,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
     for (int ph = 0; ph < static_cast<int>(m.phase_reps.size()); ++ph) {
       for (int inv = 0; inv < m.phase_reps[ph]; ++inv) {
         RC(pre_invocation(e, m.kind, ph, inv, io));
+        const int span0 = coarse ? tick(e->ss) : -1;
         int sseq = 0;
         for (int l = 0; l < m.layers; ++l) {
           const char* w = m.resident[l];
@@ -1220,6 +1224,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             recs.push_back({1, mi, ph, inv, l, x0, x1});
           }
         }
+        if (coarse) recs.push_back({1, mi, ph, inv, -1, span0, tick(e->ss)});
         if (barrier) {
           SSOP(cudaEventRecord(e->inv_done, e->ss));
           pending_barrier = true;
@@ -1244,7 +1249,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   CK(cudaEventElapsedTime(&ms, e->ev_begin, e->ev_end));
   if (e2e_ms) *e2e_ms = ms;
   int64_t n = 0;
-  if (timing) {
+  if (timing || coarse) {
     for (const Rec& r : recs) {
       float a = 0.f, b = 0.f;
       CK(cudaEventElapsedTime(&a, e->ev_t0, e->tev[r.ev0]));

@@ -336,8 +336,11 @@ class DemandLayeringEngine:
                              e.invocation, e.layer, e.start_ms, e.end_ms) for e in events[:n])
         return Timeline(events=evs, total_ms=total_ms)
 
-    def _run(self, io: RunIO, config: SimConfig, record_timeline: bool):
-        opts = RunOpts(_native.simcfg(config), 1 if record_timeline else 0)
+    def _run(self, io: RunIO, config: SimConfig, record_timeline):
+        """record_timeline: True (per-layer events), "invocations" (one EXE span
+        per invocation, PDL chaining untouched) or False."""
+        mode = 2 if record_timeline == "invocations" else (1 if record_timeline else 0)
+        opts = RunOpts(_native.simcfg(config), mode)
         cap = self._event_capacity() if record_timeline else 0
         events = (_native.Event * max(cap, 1))() if record_timeline else None
         n = C.c_int64()
@@ -394,8 +397,34 @@ class DemandLayeringEngine:
         return h2d, d2h
 
     # ------------------------------------------------------------- profiling --
+    def _resident_exe(self, config: SimConfig, iterations: int) -> dict:
+        """Per-layer EXE of each module with ALL its layers resident, from
+        invocation spans (no per-layer events, so the kernels chain through
+        programmatic dependent launch exactly as in a timed run).  Modules whose
+        layers do not all fit the cap are skipped (their streamed EXE stands)."""
+        out = {}
+        for kind in self.kinds:
+            name = M.MODULE_NAMES[kind]
+            n = self.cfg.layers_of(kind)
+            pl = Placement.of({name: range(n)})
+            try:
+                self.set_placement(pl)
+            except MemoryError:
+                continue
+            self.execute(pl, config, record_timeline=False)  # warm-up
+            spans: dict[str, list[float]] = {}
+            for _ in range(iterations):
+                res = self.execute(pl, config, record_timeline="invocations")
+                for e in res.timeline.events:
+                    if e.module == name:
+                        spans.setdefault(e.phase, []).append((e.end_ms - e.start_ms) / n)
+            out[name] = {ph: statistics.fmean(v) for ph, v in spans.items()}
+        self.set_placement(Placement.empty())
+        return out
+
     def profile_run(self, iterations: int = 3, warmup: int = 1, calibrate: bool = True,
-                    config: SimConfig = SimConfig(), sequential: bool = False) -> ModelProfile:
+                    config: SimConfig = SimConfig(), sequential: bool = False,
+                    resident_exe: bool = True) -> ModelProfile:
         """Every layer streamed; per-layer DMA and EXE (CUDA events) averaged
         per (module, phase) -> reference-schema profile.
 
@@ -406,6 +435,10 @@ class DemandLayeringEngine:
         ~0.4 % faster on B200, which shows up as predictor intercept error)."""
         run_cfg = (SimConfig(mode=Mode.SEQUENTIAL, slot_count=config.slot_count) if sequential
                    else config)
+        # resident_exe: EXE of a layer is taken from all-resident invocation spans
+        # (what a resident layer costs in a timed run: kernels PDL-chained, no
+        # per-layer events); DMA always from the streamed per-layer timeline.
+        res_exe = self._resident_exe(config, iterations) if resident_exe else {}
         samples: dict[tuple[str, str, str], list[float]] = {}
         for it in range(warmup + iterations):
             res = self.execute(Placement.empty(), run_cfg)
@@ -421,7 +454,7 @@ class DemandLayeringEngine:
             phases = []
             for ph, reps in zip(M.PHASES[kind], self.cfg.repetitions(kind)):
                 dma = statistics.fmean(samples[(name, ph, "copy")])
-                exe = statistics.fmean(samples[(name, ph, "execute")])
+                exe = res_exe.get(name, {}).get(ph) or statistics.fmean(samples[(name, ph, "execute")])
                 phases.append(PhaseProfile(name=ph, repetitions=reps, dma_ms=dma, exe_ms=exe))
                 dma_bytes += (statistics.fmean(self.stream_bytes[kind])
                               * len(samples[(name, ph, "copy")]))

@@ -232,3 +232,21 @@ def test_compact_layers_bit_identical_to_plain():
     finally:
         plain.close()
         comp.close()
+
+
+def test_invocation_span_timing_and_resident_exe_profile(tiny_alp):
+    """record_timeline="invocations": one EXE span per (module, phase,
+    invocation), no per-layer events; profile_run(resident_exe=True) takes EXE
+    from those spans with every layer of a module resident."""
+    pl = ls.Placement.of({"vlm": range(tiny_alp.cfg.lm_layers)})
+    res = tiny_alp.execute(pl, record_timeline="invocations")
+    evs = res.timeline.events
+    n_inv = sum(r for k in tiny_alp.cfg.kinds for r in tiny_alp.cfg.repetitions(k))
+    assert len(evs) == n_inv and all(e.layer == -1 for e in evs)
+    assert all(e.end_ms >= e.start_ms >= 0 for e in evs)
+    prof = tiny_alp.profile_run(iterations=2, warmup=1, resident_exe=True)
+    ref = tiny_alp.profile_run(iterations=2, warmup=1, resident_exe=False)
+    for m, r in zip(prof.modules, ref.modules):
+        for ph, phr in zip(m.phases, r.phases):
+            assert ph.dma_ms > 0 and ph.exe_ms > 0
+            assert ph.exe_ms <= 1.5 * phr.exe_ms  # resident chained EXE is not slower
