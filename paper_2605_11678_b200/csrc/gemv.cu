@@ -227,12 +227,58 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
   int s = 0;
   uint32_t round = 0;
   uint32_t tile = static_cast<uint32_t>(t0);
+  // ECT, two k-steps per warp: pages are consumed in pairs (same m-tile), so a
+  // warp has four independent decode chains in flight and the per-page
+  // barrier / bookkeeping cost is shared
+  auto ect_frags = [&](const uint8_t* st, uint32_t pg_idx, uint32_t (&af)[2][4]) {
+    const uint4 sm = *reinterpret_cast<const uint4*>(st + f0 * 8);
+    const uint2 nib = *reinterpret_cast<const uint2*>(st + kEctPageWords + f0 * 4);
+    uint4 w0 = ect_decode8(make_uint2(sm.x, sm.y), nib.x, e0p);
+    uint4 w1 = ect_decode8(make_uint2(sm.z, sm.w), nib.y, e0p);
+    if (ect_escapes(nib.x) | ect_escapes(nib.y)) {
+      w0 = ect_patch8(w0, ect_escapes(nib.x), pg_idx, f0 * 8, exc_off, exc);
+      w1 = ect_patch8(w1, ect_escapes(nib.y), pg_idx, f0 * 8 + 8, exc_off, exc);
+    }
+    af[0][0] = w0.x; af[0][1] = w0.y; af[0][2] = w0.z; af[0][3] = w0.w;
+    af[1][0] = w1.x; af[1][1] = w1.y; af[1][2] = w1.z; af[1][3] = w1.w;
+  };
   for (int n = static_cast<int>(t1 - t0), mt = cur_mt; n > 0; --n, ++tile) {
     if (kb == a.n_kb) {
       kb = 0;
       ++mt;
       flush(cur_mt);
       cur_mt = mt;
+    }
+    if constexpr (CT && kQ == 2) {
+      if (n > 1 && kb + 1 < a.n_kb) {
+        const int s1 = s + 1 == NS ? 0 : s + 1;
+        const uint32_t round1 = s + 1 == NS ? round + 1 : round;
+        uint4 bw0 = make_uint4(0u, 0u, 0u, 0u), bw1 = bw0;
+        if (bcol) {
+          bw0 = *reinterpret_cast<const uint4*>(xb + kb * 64);
+          bw1 = *reinterpret_cast<const uint4*>(xb + (kb + 1) * 64);
+        }
+        uint32_t fa[2][4], fb[2][4];
+        mbar_wait(&full[s], round & 1);
+        ect_frags(stages + s * kStage, tile, fa);
+        mbar_wait(&full[s1], round1 & 1);
+        ect_frags(stages + s1 * kStage, tile + 1, fb);
+        mma_bf16_16816(acc, fa[0], bw0.x, bw0.y);
+        mma_bf16_16816(acc, fa[1], bw0.z, bw0.w);
+        mma_bf16_16816(acc, fb[0], bw1.x, bw1.y);
+        mma_bf16_16816(acc, fb[1], bw1.z, bw1.w);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[s]);
+          mbar_arrive(&empty[s1]);
+        }
+        kb += 2;
+        s = s1 + 1 == NS ? 0 : s1 + 1;
+        round = s1 + 1 == NS ? round1 + 1 : round1;
+        --n;
+        ++tile;
+        continue;
+      }
     }
     mbar_wait(&full[s], round & 1);
     const uint8_t* st = stages + s * kStage;
@@ -256,16 +302,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
     if (bcol) bw = *reinterpret_cast<const uint4*>(xb + kb * 64);
     uint32_t af[2][4];
     if constexpr (CT) {
-      const uint4 sm = *reinterpret_cast<const uint4*>(st + f0 * 8);
-      const uint2 nib = *reinterpret_cast<const uint2*>(st + kEctPageWords + f0 * 4);
-      uint4 w0 = ect_decode8(make_uint2(sm.x, sm.y), nib.x, e0p);
-      uint4 w1 = ect_decode8(make_uint2(sm.z, sm.w), nib.y, e0p);
-      if (ect_escapes(nib.x) | ect_escapes(nib.y)) {
-        w0 = ect_patch8(w0, ect_escapes(nib.x), tile, f0 * 8, exc_off, exc);
-        w1 = ect_patch8(w1, ect_escapes(nib.y), tile, f0 * 8 + 8, exc_off, exc);
-      }
-      af[0][0] = w0.x; af[0][1] = w0.y; af[0][2] = w0.z; af[0][3] = w0.w;
-      af[1][0] = w1.x; af[1][1] = w1.y; af[1][2] = w1.z; af[1][3] = w1.w;
+      ect_frags(st, tile, af);
     } else {
 #pragma unroll
       for (int q = 0; q < 2; ++q)
