@@ -125,29 +125,39 @@ def measure_h2d_peak(torch, device, nbytes=1 << 30, reps=6):
     return best
 
 
-def gemv_microbench(torch, device, n, k, reps=30):
-    """Dominant decode kernel alone: gate|up GEMV (+fused RMSNorm, SiLU*up)."""
+def gemv_microbench(torch, device, n, k, reps=30, ect_pages=False):
+    """Dominant decode kernel alone: gate|up GEMV (+fused RMSNorm, SiLU*up),
+    over plain tiles or (ect_pages) the ECT pages the engine actually stores."""
+    from paper_2605_11678_b200 import ect
     from paper_2605_11678_b200 import kernels as K
     w = K.pack_tiled((torch.randn(n, k, device=device) * 0.02).to(torch.bfloat16))
     # rotate through several weight copies > L2 so every launch streams from HBM
     copies = [w] + [w.clone() for _ in range(2)]
+    blobs = None
+    if ect_pages:
+        blobs = [ect.compress(c.view(torch.uint8).reshape(-1), c.view(torch.uint8).numel()) for c in copies]
     x = torch.randn(k, device=device)
     nw = torch.ones(k, dtype=torch.bfloat16, device=device)
     out = torch.empty(n // 2, device=device)
     ws = K.GemvWorkspace(device)
     s = torch.cuda.Stream(device)
+    def launch(i):
+        K.gemv(K.GEMV_SILU, copies[i % 3], n, k, x, out, ws, norm_w=nw, n_valid=n // 2, stream=s,
+               ct_blob=blobs[i % 3] if blobs else None)
     with torch.cuda.stream(s):
         for i in range(5):
-            K.gemv(K.GEMV_SILU, copies[i % 3], n, k, x, out, ws, norm_w=nw, n_valid=n // 2, stream=s)
+            launch(i)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for i in range(reps):
-            K.gemv(K.GEMV_SILU, copies[i % 3], n, k, x, out, ws, norm_w=nw, n_valid=n // 2, stream=s)
+            launch(i)
         e1.record(s)
     s.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    algo_bytes = n * k * 2 + k * 4 + k * 2 + (n // 2) * 4
-    return {"bytes": algo_bytes, "ms": ms, "gbs": algo_bytes / (ms * 1e6)}
+    w_bytes = n * k * 2 * 3 // 4 if ect_pages else n * k * 2
+    algo_bytes = w_bytes + k * 4 + k * 2 + (n // 2) * 4
+    return {"bytes": algo_bytes, "ms": ms, "gbs": algo_bytes / (ms * 1e6),
+            "plain_equiv_gbs": (n * k * 2) / (ms * 1e6)}
 
 
 def gemm_microbench(torch, device, T, n, k, reps=20):
@@ -339,7 +349,9 @@ def main():
         eng.set_placement(placement)
 
     # dominant-kernel roofline: the decode gate|up GEMV (largest HBM stream of the step)
-    gv = gemv_microbench(torch, device, 2 * cfg.lm_ffn, cfg.lm_d)
+    ect_dec = M.KIND_LM in eng.ct_kinds
+    gv = gemv_microbench(torch, device, 2 * cfg.lm_ffn, cfg.lm_d, ect_pages=ect_dec)
+    gv_plain = gemv_microbench(torch, device, 2 * cfg.lm_ffn, cfg.lm_d) if ect_dec else gv
     gm = gemm_microbench(torch, device, cfg.prompt_len, (cfg.lm_hq + 2 * cfg.lm_hkv) * cfg.lm_hd, cfg.lm_d)
 
     cpu = None
@@ -387,9 +399,16 @@ def main():
                         "note": "dfbsim total of the chosen placement on the measured profile"},
         "roofline": {"bound": "hbm", "achieved": gv["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": gv["gbs"] / peaks["hbm_gbs"],
-                     "traffic": ncu_traffic(f"gemv_kernel<SILU> gate|up {2 * cfg.lm_ffn}x{cfg.lm_d}"),
-                     "kernel": f"gemv_kernel<SILU> gate|up {2 * cfg.lm_ffn}x{cfg.lm_d} bf16 "
-                               f"({gv['bytes']} B/launch, {gv['ms'] * 1e3:.1f} us)",
+                     "traffic": ncu_traffic(f"gemv_kernel<SILU{', ECT' if ect_dec else ''}> gate|up "
+                                            f"{2 * cfg.lm_ffn}x{cfg.lm_d}"),
+                     "kernel": f"gemv_kernel<SILU{', ECT pages' if ect_dec else ''}> gate|up "
+                               f"{2 * cfg.lm_ffn}x{cfg.lm_d} bf16 ({gv['bytes']} algorithmic B/launch, "
+                               f"{gv['ms'] * 1e3:.1f} us)",
+                     "plain_equivalent_gbs": gv["plain_equiv_gbs"],
+                     "plain_tile_kernel": {"gbs": gv_plain["gbs"], "us": gv_plain["ms"] * 1e3,
+                                           "frac": gv_plain["gbs"] / peaks["hbm_gbs"],
+                                           "traffic": ncu_traffic(f"gemv_kernel<SILU> gate|up "
+                                                                  f"{2 * cfg.lm_ffn}x{cfg.lm_d}")},
                      "peak_source": peaks_src,
                      "decode_layer_gbs_live": statistics.fmean(dec_rates) if dec_rates else None},
         "tensor": {"kernel": f"gemm_kernel tcgen05 prefill QKV T={cfg.prompt_len}",

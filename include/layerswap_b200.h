@@ -309,6 +309,10 @@ int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64
 int ls_k_decode_attention(const void* args, void* stream);
 /* Lossless exponent-coded BF16 (ECF) blob -> BF16 words (decode + exception patch). */
 int ls_k_ecf_decode(const void* blob, void* out, void* stream);
+/* Diagnostic: `grid` CTAs each stream `per_cta` bytes from src through a ring of
+   `stages` x `stage_bytes` TMA bulk copies (per-SM streaming bandwidth probe). */
+int ls_probe_bulk_stream(const void* src, uint64_t per_cta, int32_t stage_bytes, int32_t stages,
+                         int32_t grid, void* sink, void* stream);
 /* Exponent-coded-tiles (ECT) blob -> plain packed layer (tiles + vectors).
    out must hold the plain size rounded up to 16 bytes. */
 int ls_k_ect_decode(const void* blob, void* out, void* stream);

@@ -112,6 +112,13 @@ int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64
   return gemm_splits(n_mt, n_kb, T, num_sms, ws_floats, cnt_n);
 }
 
+int ls_probe_bulk_stream(const void* src, uint64_t per_cta, int32_t stage_bytes, int32_t stages,
+                         int32_t grid, void* sink, void* stream) {
+  return cuda_rc(launch_bulk_stream(src, per_cta, stage_bytes, stages, grid, static_cast<uint32_t*>(sink),
+                                    static_cast<cudaStream_t>(stream)),
+                 "ls_probe_bulk_stream");
+}
+
 int ls_k_ecf_decode(const void* blob, void* out, void* stream) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);

@@ -35,7 +35,7 @@ struct GemmCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kAccCols = BN < 32 ? 32 : BN;     // one accumulator
   static constexpr int kTmemCols = 2 * kAccCols;         // double-buffered (<= 512)
-  static constexpr int kDecWarps = CT ? 8 : 0;
+  static constexpr int kDecWarps = CT ? 16 : 0;
   static constexpr int kThreads = 192 + 32 * kDecWarps;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * (kStageBytes + kPBytes) +
                                   128 * 17 * 4 + (3 * kStages + 4) * 8 + 16;

@@ -15,8 +15,6 @@
 //     in a workspace slot per contributor and the last arriving CTA sums them
 //     in contributor order (bit-reproducible), then runs the fused epilogue
 //     (residual add / SiLU*up / q,k-norm + RoPE + KV-cache append / argmax).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "gemv_common.cuh"
 #include "kernels.h"
@@ -24,6 +22,14 @@
 namespace lsb {
 
 constexpr int kGemvMaxStages = 16;
+// Shared-memory budget per CTA: <= ~113 KiB lets two GEMV CTAs share an SM, so
+// with programmatic dependent launch the next GEMV's CTAs become resident and
+// start streaming their weights while the previous GEMV's CTAs drain (the
+// pipeline fill and the stream-K fix-up tail overlap instead of serialising).
+#ifndef LS_GEMV_SMEM_KB
+#define LS_GEMV_SMEM_KB 113
+#endif
+constexpr int kGemvSmemBudget = LS_GEMV_SMEM_KB * 1024;
 
 // Ring depth from the shared-memory left after x (fp32, K floats): 12 x 16 KiB
 // plain tiles or 16 x 12 KiB ECT pages (192 KiB in flight per SM) for K = 4096.
@@ -31,11 +37,12 @@ template <bool CT>
 __host__ __device__ inline int gemv_stages(int n_kb) {
   constexpr int stage = CT ? kEctPageBytes : kTileBytes;
   constexpr int cap = CT ? 16 : 12;
-  const int avail = (227 * 1024 - n_kb * kTileCols * 4 - 2560) / stage;
+  const int avail = (kGemvSmemBudget - n_kb * kTileCols * 4 - 2560) / stage;
   return avail > cap ? cap : avail;
 }
 // NW consumer warps = 8 row blocks x NW/8 k-parts of every tile (16: two k-steps
-// per warp, 32: one).  The RMSNorm reduction always uses the first 16 warps.
+// per warp -- the launched configuration; 32 would exceed 1024 threads with the
+// producer warp).  The RMSNorm reduction always uses the first 16 warps.
 template <int NW>
 struct GemvShape {
   static constexpr int kConsumers = NW * 32;
@@ -62,7 +69,7 @@ __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
 // keeps a lane's two fragments for its k-step pair adjacent (one 16-byte +
 // one 8-byte load).  Plain and ECT tiles give bit-identical results.
 template <int EPI, bool CT, int NW>
-__global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(GemvShape<NW>::kThreads, 2) gemv_kernel(const GemvArgs a) {
   constexpr int kGemvConsumers = GemvShape<NW>::kConsumers;
   constexpr int kQ = GemvShape<NW>::kQ;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -361,7 +368,7 @@ static cudaError_t launch_t(const GemvArgs& a, int grid, cudaStream_t st) {
 
 template <bool CT, int NW>
 static cudaError_t launch_ct(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
-  if (gemv_smem<CT>(a.n_kb) > 227 * 1024) return cudaErrorInvalidValue;
+  if (gemv_smem<CT>(a.n_kb) > kGemvSmemBudget) return cudaErrorInvalidValue;
   switch (epi) {
     case GEMV_F32: return launch_t<GEMV_F32, CT, NW>(a, grid, st);
     case GEMV_RESID: return launch_t<GEMV_RESID, CT, NW>(a, grid, st);
@@ -372,19 +379,7 @@ static cudaError_t launch_ct(int epi, const GemvArgs& a, int grid, cudaStream_t 
   return cudaErrorInvalidValue;
 }
 
-// consumer warps (16 or 32; LS_GEMV_WARPS=32 selects 32 for A/B runs -- plain and
-// ECT must use the same count to stay bit-identical)
-static int gemv_warps() {
-  static const int w = [] {
-    const char* v = getenv("LS_GEMV_WARPS");
-    return (v && atoi(v) == 32) ? 32 : 16;
-  }();
-  return w;
-}
-
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
-  if (gemv_warps() == 32)
-    return a.ct_blob ? launch_ct<true, 32>(epi, a, grid, st) : launch_ct<false, 32>(epi, a, grid, st);
   return a.ct_blob ? launch_ct<true, 16>(epi, a, grid, st) : launch_ct<false, 16>(epi, a, grid, st);
 }
 

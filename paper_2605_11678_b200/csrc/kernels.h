@@ -214,4 +214,9 @@ cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaS
 cudaError_t launch_ect_decode_pages(const uint8_t* blob, uint32_t page0, uint32_t n_pages,
                                     bool with_tail, void* out, int num_sms, cudaStream_t st);
 
+// diagnostic (probe.cu): `grid` CTAs each stream `per_cta` bytes of src through a
+// `stages` x `stage_bytes` bulk-copy ring, no compute
+cudaError_t launch_bulk_stream(const void* src, uint64_t per_cta, int stage_bytes, int stages, int grid,
+                               uint32_t* sink, cudaStream_t st);
+
 }  // namespace lsb

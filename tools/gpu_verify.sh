@@ -16,9 +16,11 @@ if [ -f "$PROF" ] && [ -z "$SKIP_NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -s $N -c $N --csv \
       --log-file $OUT/launches.csv python tools/profile_step.py --profile $PROF --runs 2 > $OUT/launches.log 2>&1
   python tools/ncu_summary.py $OUT/launches.csv > $OUT/launches_summary.txt 2>&1; head -30 $OUT/launches_summary.txt
+  # the dominant decode kernel as launched in the step: gate|up GEMV over ECT pages
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-      -k 'regex:gemv_kernel<.int.2>' -s 40 -c 1 -o $OUT/gemv_silu python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_gemv.log 2>&1
-  ncu -i $OUT/gemv_silu.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > $OUT/gemv_silu_dram.csv 2>&1
-  cat $OUT/gemv_silu_dram.csv | tail -3
+      -k 'regex:gemv_kernel<.int.2, .bool.1' -s 40 -c 1 -o $OUT/gemv_silu_ect python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_gemv.log 2>&1
+  ncu -i $OUT/gemv_silu_ect.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > $OUT/gemv_silu_ect_dram.csv 2>&1
+  cat $OUT/gemv_silu_ect_dram.csv | tail -3
+  python tools/ncu_kv.py $OUT/gemv_silu_ect.ncu-rep > $OUT/gemv_silu_ect_summary.txt 2>&1
 fi
 ls -la $OUT

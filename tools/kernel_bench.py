@@ -109,11 +109,15 @@ def bench_ect_decode(nbytes=385_892_352, copies=2):
     return {"kernel": f"ect_decode {nbytes} B", "us": ms * 1e3, "GBps_moved": moved / (ms * 1e6)}
 
 
-def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False):
+def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False, ct=False):
     dev = "cuda"
     # rotate weight copies so skinny (weight-bound) shapes stream from HBM, not L2
     copies = max(1, min(12, (256 << 20) // (n * k * 2)))
     ws_ = [K.pack_tiled((torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)) for _ in range(copies)]
+    blobs = None
+    if ct:
+        from paper_2605_11678_b200 import ect
+        blobs = [ect.compress(w.view(torch.uint8).reshape(-1), w.view(torch.uint8).numel()) for w in ws_]
     x = torch.randn(T, k, device=dev).to(torch.bfloat16)
     ncol = n // 2 if epi == K.GEMM_SILU_BF16 else n
     out = torch.zeros(T, ncol, dtype=torch.bfloat16 if epi != K.GEMM_RESID_F32 else torch.float32,
@@ -121,11 +125,14 @@ def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False):
     it = [0]
 
     def run():
-        K.gemm(epi, ws_[it[0] % copies], n, k, x, out, n_valid=ncol, splitk=splitk)
+        i = it[0] % copies
+        K.gemm(epi, ws_[i], n, k, x, out, n_valid=ncol, splitk=splitk,
+               ct_blob=blobs[i] if blobs else None)
         it[0] += 1
     ms = timed(run)
     f = 2.0 * T * n * k
-    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}" + (" splitk" if splitk else ""), "us": ms * 1e3,
+    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}" + (" splitk" if splitk else "") + (" ect" if ct else ""),
+            "us": ms * 1e3,
             "TFLOPs": f / (ms * 1e9), "weight_GBps": n * k * 2 / (ms * 1e6)}
 
 
@@ -159,6 +166,11 @@ def main():
                              (64, 6144, 2048, K.GEMM_BF16), (64, 13824, 2048, K.GEMM_SILU_BF16)):
             res.append(bench_gemm(T, n, k, epi))
             res.append(bench_gemm(T, n, k, epi, splitk=True))
+    if args.only in ("all", "ectgemm"):
+        for T, n, k, epi in ((64, 2048, 4096, K.GEMM_RESID_F32), (64, 2048, 6912, K.GEMM_RESID_F32),
+                             (64, 6144, 2048, K.GEMM_BF16), (64, 13824, 2048, K.GEMM_SILU_BF16)):
+            res.append(bench_gemm(T, n, k, epi, splitk=True))
+            res.append(bench_gemm(T, n, k, epi, splitk=True, ct=True))
     if args.only in ("all", "ect"):
         res.append(bench_gemv_ect(24576, 4096, K.GEMV_SILU))
         res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
@@ -177,5 +189,33 @@ def main():
         print(json.dumps(r))
 
 
-if __name__ == "__main__":
+
+
+def probe_bulk(grid, stage_bytes, stages, per_cta=4 << 20, shared=False):
+    """Per-SM TMA bulk-copy streaming bandwidth (probe.cu)."""
+    import ctypes as C
+    from paper_2605_11678_b200 import _native
+    fn = _native.lib().ls_probe_bulk_stream
+    fn.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+    fn.restype = C.c_int
+    src = torch.empty(grid * per_cta, dtype=torch.uint8, device="cuda")
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    flag = (1 << 63) if shared else 0
+    ms = timed(lambda: fn(src.data_ptr(), per_cta | flag, stage_bytes, stages, grid, sink.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream), reps=5, warm=2)
+    return {"probe": f"grid={grid} stage={stage_bytes} stages={stages} shared={shared}", "us": ms * 1e3,
+            "GBps": grid * per_cta / (ms * 1e6), "per_sm_GBps": per_cta / (ms * 1e6)}
+
+
+if __name__ == "__main__" and "--probe" in sys.argv:
+    out = []
+    for grid in (16, 108, 148):
+        for sb, st in ((16384, 8), (8192, 16)):
+            out.append(probe_bulk(grid, sb, st))
+            out.append(probe_bulk(grid, sb, st, per_cta=256 << 10, shared=True))
+    for r in out:
+        print(json.dumps(r))
+
+
+if __name__ == "__main__" and "--probe" not in sys.argv:
     main()
