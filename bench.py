@@ -417,6 +417,7 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches["kernel_launches"] * args.steps,
+        "host_enqueue_ms_per_step": launches["host_enqueue_ms"],
         "memory_mib": {k: round(v / 2 ** 20, 1) for k, v in mem.items()},
         "wall_s_timed": wall,
     }

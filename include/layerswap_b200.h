@@ -258,6 +258,9 @@ int ls_exec_memory(ls_exec* e, uint64_t out[7]);
 int ls_exec_streams(ls_exec* e, void** copy_stream, void** compute_stream);
 /* out: kernels launched, streamed-layer H2D copies, H2D bytes -- of the last run */
 int ls_exec_stats(ls_exec* e, int64_t out[3]);
+/* Host wall time (us) the last ls_exec_run spent enqueueing work, i.e. before
+   its final stream synchronisation (enqueue-bound when close to the device time). */
+int ls_exec_enqueue_us(ls_exec* e, double* us);
 
 typedef struct ls_run_io {
   int32_t on_host;         /* 1: pointers are pinned host memory (copies inside the run) */

@@ -22,6 +22,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -262,6 +263,7 @@ struct ls_exec {
   float* tp_buf = nullptr;
   uint64_t tp_buf_elems = 0;
   int64_t launches = 0, h2d_copies = 0;
+  double enqueue_us = 0.0;  // host time to enqueue the last run (before its final sync)
   uint64_t h2d_bytes = 0;
 
   bf16* kc(int l) { return kv + static_cast<long>(l) * 2 * d.lm_hkv * (ctx + 1) * d.lm_hd; }
@@ -1097,6 +1099,11 @@ int ls_exec_stats(ls_exec* e, int64_t out[3]) {
   return LS_OK;
 }
 
+int ls_exec_enqueue_us(ls_exec* e, double* us) {
+  *us = e->enqueue_us;
+  return LS_OK;
+}
+
 int ls_exec_streams(ls_exec* e, void** copy_stream, void** compute_stream) {
   *copy_stream = e->cs;
   *compute_stream = e->ss;
@@ -1143,6 +1150,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
     return next_ev++;
   };
 
+  const auto host_t0 = std::chrono::steady_clock::now();
   e->launches = 0;
   e->h2d_copies = 0;
   e->h2d_bytes = 0;
@@ -1240,6 +1248,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   if (d.has_expert && io->actions_out)
     CK(cudaMemcpyAsync(io->actions_out, e->actions, 4ull * e->Te * d.action_dim, kout, e->ss));
   CK(cudaEventRecord(e->ev_end, e->ss));
+  e->enqueue_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count();
   CK(cudaStreamSynchronize(e->ss));
   CK(cudaStreamSynchronize(e->cs));
   CK(cudaGetLastError());

@@ -22,12 +22,12 @@
 namespace lsb {
 
 constexpr int kGemvMaxStages = 16;
-// Shared-memory budget per CTA: <= ~113 KiB lets two GEMV CTAs share an SM, so
-// with programmatic dependent launch the next GEMV's CTAs become resident and
-// start streaming their weights while the previous GEMV's CTAs drain (the
-// pipeline fill and the stream-K fix-up tail overlap instead of serialising).
+// Shared-memory budget per CTA.  Measured: capping it at 113 KiB so two GEMV
+// CTAs (of consecutive PDL-chained launches) can share an SM is a net loss
+// (decode layer 127 -> 193 us): the shallower ring costs more than the overlap
+// gains, so each GEMV owns its SM's shared memory.
 #ifndef LS_GEMV_SMEM_KB
-#define LS_GEMV_SMEM_KB 113
+#define LS_GEMV_SMEM_KB 227
 #endif
 constexpr int kGemvSmemBudget = LS_GEMV_SMEM_KB * 1024;
 
@@ -69,7 +69,7 @@ __device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
 // keeps a lane's two fragments for its k-step pair adjacent (one 16-byte +
 // one 8-byte load).  Plain and ECT tiles give bit-identical results.
 template <int EPI, bool CT, int NW>
-__global__ void __launch_bounds__(GemvShape<NW>::kThreads, 2) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const GemvArgs a) {
   constexpr int kGemvConsumers = GemvShape<NW>::kConsumers;
   constexpr int kQ = GemvShape<NW>::kQ;
   extern __shared__ __align__(1024) uint8_t smem[];

@@ -59,6 +59,7 @@ def _bind():
         "ls_exec_memory": [vp, C.POINTER(C.c_uint64)],
         "ls_exec_streams": [vp, C.POINTER(vp), C.POINTER(vp)],
         "ls_exec_stats": [vp, C.POINTER(C.c_int64)],
+        "ls_exec_enqueue_us": [vp, C.POINTER(C.c_double)],
         "ls_exec_run": [vp, C.POINTER(RunIO), C.POINTER(RunOpts), C.POINTER(_native.Event),
                         C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                         C.POINTER(C.c_double)],
@@ -292,7 +293,10 @@ class DemandLayeringEngine:
     def last_run_stats(self) -> dict:
         out = (C.c_int64 * 3)()
         _native.check(self.lib.ls_exec_stats(self.handle, out), RuntimeError)
-        return {"kernel_launches": out[0], "h2d_copies": out[1], "h2d_bytes": out[2]}
+        us = C.c_double()
+        _native.check(self.lib.ls_exec_enqueue_us(self.handle, C.byref(us)), RuntimeError)
+        return {"kernel_launches": out[0], "h2d_copies": out[1], "h2d_bytes": out[2],
+                "host_enqueue_ms": us.value / 1e3}
 
     def streams(self) -> tuple[int, int]:
         cs, ss = C.c_void_p(), C.c_void_p()
