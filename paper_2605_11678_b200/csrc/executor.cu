@@ -191,6 +191,11 @@ struct GemvPlan {
   int n, k, grid, max_contrib;
 };
 
+// one DMA / EXE (or invocation span) timestamp pair of a run
+struct RunRec {
+  int engine, module, phase, inv, layer, ev0, ev1;
+};
+
 struct Module {
   int kind;
   int layers;
@@ -264,6 +269,16 @@ struct ls_exec {
   uint64_t tp_buf_elems = 0;
   int64_t launches = 0, h2d_copies = 0;
   double enqueue_us = 0.0;  // host time to enqueue the last run (before its final sync)
+  // Untimed runs are captured once into a CUDA graph (both streams, events,
+  // copies, PDL edges) and replayed: ~8k kernel launches per inference cost
+  // ~20 us of host time each when enqueued one by one.  Any change of the
+  // placement / layout / IO pointers / schedule config re-captures.
+  bool use_graph = true;
+  uint64_t gen = 0;  // bumped whenever resident pointers or the layout change
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t gkey[12] = {};
+  std::vector<RunRec> grecs;  // invocation-span records of the captured run
+  cudaEvent_t join_ev = nullptr, fork_ev = nullptr;
   uint64_t h2d_bytes = 0;
 
   bf16* kc(int l) { return kv + static_cast<long>(l) * 2 * d.lm_hkv * (ctx + 1) * d.lm_hd; }
@@ -656,6 +671,7 @@ int run_layer(ls_exec* e, const Module& m, int phase, int inv, int l, const char
 // layer_mem = what a resident layer occupies.  Drops resident layers (the
 // next ls_exec_set_placement re-creates them).
 int finalize_layout(ls_exec* e) {
+  ++e->gen;
   e->ar.used = e->mark0;
   e->bytes_slots = 0;
   e->slot_bytes = 0;
@@ -921,7 +937,7 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
   }
   e->mark0 = e->ar.used;
   if (int rc = finalize_layout(e)) return fail(rc);
-  cudaEvent_t* evs[] = {&e->inv_done, &e->exe_done};
+  cudaEvent_t* evs[] = {&e->inv_done, &e->exe_done, &e->join_ev, &e->fork_ev};
   for (auto p : evs) cudaEventCreateWithFlags(p, cudaEventDisableTiming);
   cudaEvent_t* tevs[] = {&e->ev_begin, &e->ev_t0, &e->ev_t1, &e->ev_end};
   for (auto p : tevs) cudaEventCreate(p);
@@ -940,6 +956,9 @@ int ls_exec_destroy(ls_exec* e) {
   cudaEvent_t evs[] = {e->inv_done, e->exe_done, e->ev_begin, e->ev_t0, e->ev_t1, e->ev_end};
   for (auto v : evs)
     if (v) cudaEventDestroy(v);
+  if (e->gexec) cudaGraphExecDestroy(e->gexec);
+  if (e->join_ev) cudaEventDestroy(e->join_ev);
+  if (e->fork_ev) cudaEventDestroy(e->fork_ev);
   if (e->comm && nccl_api().ok) nccl_api().comm_destroy(e->comm);
   if (e->cs) cudaStreamDestroy(e->cs);
   if (e->ss) cudaStreamDestroy(e->ss);
@@ -1057,6 +1076,7 @@ int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n) {
                                    static_cast<long long>(n), static_cast<long long>(total));
   CK(cudaStreamSynchronize(e->ss));
   CK(cudaStreamSynchronize(e->cs));
+  ++e->gen;
   e->ar.used = e->mark;
   int64_t off = 0;
   for (auto& m : e->mods) {
@@ -1138,35 +1158,54 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
       e->tev.push_back(v);
     }
   }
-  struct Rec {
-    int engine, module, phase, inv, layer, ev0, ev1;
-  };
+  using Rec = RunRec;
   std::vector<Rec> recs;
   if (timing || coarse) recs.reserve(static_cast<size_t>(need / 2));
   int next_ev = 0;
+  bool capturing = false;
   auto tick = [&](cudaStream_t s) {
-    cudaEventRecord(e->tev[next_ev], s);
+    if (capturing) cudaEventRecordWithFlags(e->tev[next_ev], s, cudaEventRecordExternal);
+    else cudaEventRecord(e->tev[next_ev], s);
     if (s == e->ss) e->pdl_ok = false;
     return next_ev++;
   };
 
   const auto host_t0 = std::chrono::steady_clock::now();
+  const bool graph = e->use_graph && !timing && !e->tp_on;
+  const uint64_t key[12] = {reinterpret_cast<uint64_t>(io->patches), reinterpret_cast<uint64_t>(io->text_ids),
+                            reinterpret_cast<uint64_t>(io->noise), reinterpret_cast<uint64_t>(io->tokens_out),
+                            reinterpret_cast<uint64_t>(io->actions_out), reinterpret_cast<uint64_t>(io->logits_out),
+                            static_cast<uint64_t>(io->on_host), static_cast<uint64_t>(opts->cfg.mode),
+                            static_cast<uint64_t>(opts->cfg.cross_invocation_prefetch),
+                            static_cast<uint64_t>(nsl), e->gen, coarse ? 2ull : 1ull};
+  const bool replay = graph && e->gexec && std::memcmp(key, e->gkey, sizeof(key)) == 0;
+  capturing = graph && !replay;
+  // timestamps inside a capture must be external event-record nodes
+  auto rec = [&](cudaEvent_t ev) {
+    return capturing ? cudaEventRecordWithFlags(ev, e->ss, cudaEventRecordExternal) : cudaEventRecord(ev, e->ss);
+  };
+  // the whole enqueue (as a lambda so a failure during capture can end it cleanly)
+  auto enqueue = [&]() -> int {
   e->launches = 0;
   e->h2d_copies = 0;
   e->h2d_bytes = 0;
   const cudaMemcpyKind kin = io->on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  CK(cudaEventRecord(e->ev_begin, e->ss));
+  CK(rec(e->ev_begin));
   if (d.has_vit && io->patches)
     CK(cudaMemcpyAsync(e->patches, io->patches, 2ull * e->Tv * d.vit_patch_dim, kin, e->ss));
   if (io->text_ids)
     CK(cudaMemcpyAsync(e->text_ids, io->text_ids, 4ull * (d.prompt_prefix + d.prompt_suffix), kin, e->ss));
   if (d.has_expert && io->noise)
     CK(cudaMemcpyAsync(e->noise, io->noise, 4ull * e->Te * d.action_dim, kin, e->ss));
-  CK(cudaEventRecord(e->ev_t0, e->ss));
+  CK(rec(e->ev_t0));
   e->pdl_ok = false;
-  CK(cudaStreamWaitEvent(e->cs, e->ev_t0, 0));
+  // fork the copy stream off the compute stream (a plain event: timestamp
+  // records inside a capture are external and create no dependencies)
+  CK(cudaEventRecord(e->fork_ev, e->ss));
+  CK(cudaStreamWaitEvent(e->cs, e->fork_ev, 0));
 
   std::vector<bool> slot_used(static_cast<size_t>(nsl), false);
+  bool exe_rec = false;
   bool pending_barrier = false;
   for (int mi = 0; mi < static_cast<int>(e->mods.size()); ++mi) {
     const Module& m = e->mods[mi];
@@ -1182,7 +1221,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
           if (!w) {
             slot = sseq++ % nsl;
             if (slot_used[slot]) CK(cudaStreamWaitEvent(e->cs, e->comp_done[slot], 0));
-            if (seq) CK(cudaStreamWaitEvent(e->cs, e->exe_done, 0));
+            if (seq && exe_rec) CK(cudaStreamWaitEvent(e->cs, e->exe_done, 0));
             if (pending_barrier) {
               CK(cudaStreamWaitEvent(e->cs, e->inv_done, 0));
               pending_barrier = false;
@@ -1226,7 +1265,10 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             SSOP(cudaEventRecord(e->comp_done[slot], e->ss));
             slot_used[slot] = true;
           }
-          if (seq) SSOP(cudaEventRecord(e->exe_done, e->ss));
+          if (seq) {
+            SSOP(cudaEventRecord(e->exe_done, e->ss));
+            exe_rec = true;  // (events last recorded by another run / a capture are not waited on)
+          }
           if (timing) {
             if (slot >= 0) recs.push_back({0, mi, ph, inv, l, dma0, dma1});
             recs.push_back({1, mi, ph, inv, l, x0, x1});
@@ -1241,13 +1283,41 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
       }
     }
   }
-  CK(cudaEventRecord(e->ev_t1, e->ss));
+  CK(rec(e->ev_t1));
   const cudaMemcpyKind kout = io->on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   if (io->tokens_out)
     CK(cudaMemcpyAsync(io->tokens_out, e->hist, 4ull * (d.decode_steps + 1), kout, e->ss));
   if (d.has_expert && io->actions_out)
     CK(cudaMemcpyAsync(io->actions_out, e->actions, 4ull * e->Te * d.action_dim, kout, e->ss));
-  CK(cudaEventRecord(e->ev_end, e->ss));
+  CK(rec(e->ev_end));
+  if (capturing) {  // join the copy stream back into the origin stream
+    CK(cudaEventRecord(e->join_ev, e->cs));
+    CK(cudaStreamWaitEvent(e->ss, e->join_ev, 0));
+  }
+  return LS_OK;
+  };
+  if (capturing) {
+    CK(cudaStreamBeginCapture(e->ss, cudaStreamCaptureModeRelaxed));
+    const int rc = enqueue();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(e->ss, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CK(ce);
+    if (e->gexec) cudaGraphExecDestroy(e->gexec);
+    e->gexec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&e->gexec, g, 0);
+    cudaGraphDestroy(g);
+    CK(ie);
+    std::memcpy(e->gkey, key, sizeof(key));
+    e->grecs = recs;
+  } else if (!replay) {
+    RC(enqueue());
+  }
+  if (replay) recs = e->grecs;
+  if (graph) CK(cudaGraphLaunch(e->gexec, e->ss));
   e->enqueue_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count();
   CK(cudaStreamSynchronize(e->ss));
   CK(cudaStreamSynchronize(e->cs));
