@@ -87,7 +87,10 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
 // Per word pair: PRMT places both sm bytes with their sign bit replicated into
 // the byte above (sign lands on bit 15 / 31), one LOP3 keeps sign + mantissa
 // and ORs the window base, one PRMT lines up the pair's codes, one IMAD adds
-// them into the exponent fields: ~2.4 integer ops per word.
+// them into the exponent fields: ~2.4 integer ops per word.  (Measured: a
+// PRMT-free variant -- sm bytes pre-interleaved, codes pre-split by the encoder,
+// ~3.3 ALU/FMA ops per word -- is 3 % slower in the decode GEMV; the narrow
+// XU pipe PRMT issues on is not what bounds it.)
 // prmt.b32 in its default mode: bit 3 of a selector nibble replicates the sign
 // of the selected byte (__byte_perm ignores that bit)
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {

@@ -266,9 +266,10 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
           bw1 = *reinterpret_cast<const uint4*>(xb + (kb + 1) * 64);
         }
         uint32_t fa[2][4], fb[2][4];
+        // both pages first, so the two pages' loads and decode chains interleave
         mbar_wait(&full[s], round & 1);
-        ect_frags(stages + s * kStage, tile, fa);
         mbar_wait(&full[s1], round1 & 1);
+        ect_frags(stages + s * kStage, tile, fa);
         ect_frags(stages + s1 * kStage, tile + 1, fb);
         mma_bf16_16816(acc, fa[0], bw0.x, bw0.y);
         mma_bf16_16816(acc, fa[1], bw0.z, bw0.w);

@@ -166,6 +166,11 @@ def main():
                              (64, 6144, 2048, K.GEMM_BF16), (64, 13824, 2048, K.GEMM_SILU_BF16)):
             res.append(bench_gemm(T, n, k, epi))
             res.append(bench_gemm(T, n, k, epi, splitk=True))
+    if args.only in ("all", "ectprefill"):
+        for T, n, k, epi in ((1024, 6144, 4096, K.GEMM_BF16), (1024, 24576, 4096, K.GEMM_SILU_BF16),
+                             (1024, 4096, 12288, K.GEMM_RESID_F32), (3072, 4352, 1152, K.GEMM_BF16_GELU)):
+            res.append(bench_gemm(T, n, k, epi))
+            res.append(bench_gemm(T, n, k, epi, ct=True))
     if args.only in ("all", "ectgemm"):
         for T, n, k, epi in ((64, 2048, 4096, K.GEMM_RESID_F32), (64, 2048, 6912, K.GEMM_RESID_F32),
                              (64, 6144, 2048, K.GEMM_BF16), (64, 13824, 2048, K.GEMM_SILU_BF16)):
