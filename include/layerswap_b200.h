@@ -277,6 +277,10 @@ typedef struct ls_run_opts {
   ls_simconfig cfg;
   int32_t record_timeline; /* 1: per-layer CUDA event timestamps; 2: one EXE span per
                               invocation (layer = -1), PDL chaining left intact */
+  int32_t blind_offload;   /* 1: Accelerate-style blind offload baseline:
+                              per-tensor synchronous copies of every streamed layer, no
+                              copy/compute overlap, a device-wide sync after each layer;
+                              plain (non-compact) modules only */
 } ls_run_opts;
 
 /* One inference.  total_ms: device time from the first layer transfer /

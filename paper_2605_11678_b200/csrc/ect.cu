@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
   const EctHeader* h = reinterpret_cast<const EctHeader*>(blob);
   const uint32_t e0p = (h->e0 << 7) | (h->e0 << 23);
   const uint8_t* pages = blob + h->off_pages + static_cast<uint64_t>(page0) * kEctPageBytes;
+  const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(blob + h->off_excoff);
+  const uint32_t* exc = reinterpret_cast<const uint32_t*>(blob + h->off_exc);
   // one page per CTA iteration: fragments decoded into the plain tile image in
   // shared memory (pair stores are bank-conflict-free thanks to the 128 B
   // swizzle), then streamed out as coalesced 16-byte stores
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
       const uint32_t nib = __ldcs(reinterpret_cast<const uint32_t*>(pg + kEctPageWords) + f);
       uint4 w = ect_decode8(sm, nib, e0p);
       const uint32_t esc = ect_escapes(nib);
-      if (esc) w = ect_zero_escapes(w, esc);  // exponent 0 unless the scatter below patches it
+      if (esc) w = ect_zero_escapes(w, esc);  // exponent 0 unless an exc entry patches it below
       uint32_t* tb = tile + it * 1024;  // fragment + 256 = 2 row blocks (32 rows) lower
       tb[pos[0]] = w.x;
       tb[pos[1]] = w.y;
@@ -47,6 +49,17 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
       tb[pos[3]] = w.w;
     }
     __syncthreads();
+    // the page's exceptions (true exponents of escaped words) patched in shared memory
+    {
+      const uint32_t e_lo = exc_off[page0 + page], e_hi = exc_off[page0 + page + 1];
+      uint16_t* t16 = reinterpret_cast<uint16_t*>(tile);
+      for (uint32_t i = e_lo + threadIdx.x; i < e_hi; i += blockDim.x) {
+        const uint32_t x = exc[i];
+        const uint32_t k = ect_plain_word(x >> 8);
+        t16[k] = static_cast<uint16_t>((t16[k] & 0x807Fu) | ((x & 0xFFu) << 7));
+      }
+      if (e_hi > e_lo) __syncthreads();
+    }
     uint4* dst = reinterpret_cast<uint4*>(out + static_cast<uint64_t>(page) * kTileBytes);
 #pragma unroll
     for (int it = 0; it < 4; ++it)
@@ -63,37 +76,10 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
     dst[i] = src[i];
 }
 
-// Escaped words: one thread per exception, page found by binary search in exc_off.
-__global__ void __launch_bounds__(256) ect_patch_kernel(const uint8_t* __restrict__ blob,
-                                                        uint32_t page0, uint32_t n_pages,
-                                                        uint16_t* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const EctHeader* h = reinterpret_cast<const EctHeader*>(blob);
-  const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(blob + h->off_excoff) + page0;
-  const uint32_t* exc = reinterpret_cast<const uint32_t*>(blob + h->off_exc);
-  const uint32_t e_lo = exc_off[0], e_hi = exc_off[n_pages];
-  for (uint32_t i = e_lo + blockIdx.x * blockDim.x + threadIdx.x; i < e_hi; i += gridDim.x * blockDim.x) {
-    uint32_t lo = 0, hi = n_pages;  // largest page with exc_off[page] <= i
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (exc_off[mid] <= i) lo = mid;
-      else hi = mid;
-    }
-    const uint32_t x = exc[i];
-    const uint64_t k = static_cast<uint64_t>(lo) * kEctPageWords + ect_plain_word(x >> 8);
-    out[k] = static_cast<uint16_t>((out[k] & 0x807Fu) | ((x & 0xFFu) << 7));
-  }
-}
-
 cudaError_t launch_ect_decode_pages(const uint8_t* blob, uint32_t page0, uint32_t n_pages,
                                     bool with_tail, void* out, int num_sms, cudaStream_t st) {
-  cudaError_t e = launch_k(ect_decode_kernel, dim3(6 * num_sms), dim3(256), 0, st, blob, page0,
-                           n_pages, with_tail ? 1 : 0, static_cast<uint8_t*>(out));
-  if (e != cudaSuccess) return e;
-  set_launch_pdl(true);  // the scatter follows the decode kernel directly
-  return launch_k(ect_patch_kernel, dim3(num_sms), dim3(256), 0, st, blob, page0, n_pages,
-                  static_cast<uint16_t*>(out));
+  return launch_k(ect_decode_kernel, dim3(6 * num_sms), dim3(256), 0, st, blob, page0, n_pages,
+                  with_tail ? 1 : 0, static_cast<uint8_t*>(out));
 }
 
 cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st) {

@@ -352,7 +352,6 @@ int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensor
     KL(launch_ect_decode_pages(reinterpret_cast<const uint8_t*>(ct_blob), static_cast<uint32_t>(ct_page0),
                                static_cast<uint32_t>(n_mt(n)) * static_cast<uint32_t>(n_kb(k)), false,
                                e->scratch, e->nsm, e->ss));
-    ++e->launches;  // decode + exception scatter
     e->pdl_ok = false;
     w = e->scratch;
     ct_blob = nullptr;
@@ -1171,7 +1170,11 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   };
 
   const auto host_t0 = std::chrono::steady_clock::now();
-  const bool graph = e->use_graph && !timing && !e->tp_on;
+  const bool blind = opts->blind_offload != 0;
+  if (blind)
+    for (auto& m : e->mods)
+      if (m.ct || m.ecf) return set_error(LS_ERR_VALUE, "blind offload runs plain (non-compact, non-ECF) layers only");
+  const bool graph = e->use_graph && !timing && !e->tp_on && !blind;
   const uint64_t key[12] = {reinterpret_cast<uint64_t>(io->patches), reinterpret_cast<uint64_t>(io->text_ids),
                             reinterpret_cast<uint64_t>(io->noise), reinterpret_cast<uint64_t>(io->tokens_out),
                             reinterpret_cast<uint64_t>(io->actions_out), reinterpret_cast<uint64_t>(io->logits_out),
@@ -1231,8 +1234,18 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             char* dst = m.ecf ? e->slots[slot] + ((e->slot_bytes - nbytes) & ~uint64_t(255))
                               : e->slots[slot];
             if (timing) dma0 = tick(e->cs);
+            if (blind) {
+              // the layer's compute stream is idle (device-wide sync after every layer);
+              // one host-blocking copy per weight tensor
+              for (int i = 0; i < m.lay.n_parts; ++i) {
+                CK(cudaMemcpyAsync(dst + m.lay.offset[i], m.host[l] + m.lay.offset[i], m.lay.bytes[i],
+                                   cudaMemcpyHostToDevice, e->cs));
+                CK(cudaStreamSynchronize(e->cs));
+              }
+            } else {
             CK(cudaMemcpyAsync(dst, m.ct ? m.host_ct[l] : m.ecf ? m.host_ecf[l] : m.host[l], nbytes,
                                cudaMemcpyHostToDevice, e->cs));
+            }
             ++e->h2d_copies;
             e->h2d_bytes += nbytes;
             if (timing) dma1 = tick(e->cs);
@@ -1255,7 +1268,6 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             KL(launch_ect_decode_pages(reinterpret_cast<const uint8_t*>(w), 0,
                                        static_cast<uint32_t>((m.lay.offset[3] + m.lay.bytes[3]) / 16384),
                                        true, e->scratch, e->nsm, e->ss));
-            ++e->launches;  // decode + exception scatter
             e->pdl_ok = false;
             w = e->scratch;
           }
@@ -1268,6 +1280,10 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
           if (seq) {
             SSOP(cudaEventRecord(e->exe_done, e->ss));
             exe_rec = true;  // (events last recorded by another run / a capture are not waited on)
+          }
+          if (blind && slot >= 0) {  // module deletion + empty_cache: global synchronisation
+            CK(cudaDeviceSynchronize());
+            e->pdl_ok = false;
           }
           if (timing) {
             if (slot >= 0) recs.push_back({0, mi, ph, inv, l, dma0, dma1});

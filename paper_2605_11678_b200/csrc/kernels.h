@@ -206,7 +206,7 @@ struct EctHeader {
 };
 static_assert(sizeof(EctHeader) == 128, "ECT header is 128 bytes");
 // blob -> plain layer bytes (whole 16-byte chunks: out needs a16(total) bytes);
-// a decode kernel then an exception scatter (PDL-chained).  Reads the header
+// one kernel (exceptions patched per page in shared memory).  Reads the header
 // synchronously (test / tool entry point).
 cudaError_t launch_ect_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st);
 // pages [page0, page0 + n_pages) of a device blob -> plain tiles at out (+ the

@@ -37,7 +37,7 @@ class RunIO(C.Structure):
 
 
 class RunOpts(C.Structure):
-    _fields_ = [("cfg", _native.SimCfg), ("record_timeline", C.c_int32)]
+    _fields_ = [("cfg", _native.SimCfg), ("record_timeline", C.c_int32), ("blind_offload", C.c_int32)]
 
 
 def _bind():
@@ -344,7 +344,7 @@ class DemandLayeringEngine:
         """record_timeline: True (per-layer events), "invocations" (one EXE span
         per invocation, PDL chaining untouched) or False."""
         mode = 2 if record_timeline == "invocations" else (1 if record_timeline else 0)
-        opts = RunOpts(_native.simcfg(config), mode)
+        opts = RunOpts(_native.simcfg(config), mode, 1 if getattr(self, "_blind", False) else 0)
         cap = self._event_capacity() if record_timeline else 0
         events = (_native.Event * max(cap, 1))() if record_timeline else None
         n = C.c_int64()
@@ -394,6 +394,24 @@ class DemandLayeringEngine:
         total, e2e, tl = self._run(io, config, record_timeline)
         return RunResult(b["tokens"].clone(), b["actions"].clone() if "actions" in b else None,
                          b["logits"].clone() if "logits" in b else None, total, e2e, tl)
+
+    def execute_blind_offload(self, placement: Placement, inputs: dict | None = None,
+                              record_timeline: bool = False) -> RunResult:
+        """Accelerate-style blind offload baseline on this
+        engine's kernels: every streamed layer is fetched tensor by tensor with
+        host-blocking copies (14 per LM layer, like per-parameter .to("cuda")),
+        nothing overlaps, and a device-wide synchronisation follows each layer
+        (module deletion / empty_cache).  Needs plain layers (compact=False).
+        The source is the pinned arena, so the baseline is if anything faster
+        than real pageable-memory offloading."""
+        if self.ct_kinds:
+            raise ValueError("blind offload needs plain layers: create the engine with compact=False")
+        self._blind = True
+        try:
+            return self.execute(placement, SimConfig(mode=Mode.SEQUENTIAL), inputs,
+                                record_timeline=record_timeline)
+        finally:
+            self._blind = False
 
     def infer(self, host_inputs: dict, placement: Placement | None = None,
               config: SimConfig = SimConfig()) -> RunResult:

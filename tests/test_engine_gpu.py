@@ -267,3 +267,23 @@ def test_graph_replay_reads_new_inputs(tiny_alp):
     assert not torch.equal(a1.logits, b1.logits)
     e2e = tiny_alp.infer(b_in, pl)  # pinned-host IO, its own captured graph
     assert torch.equal(e2e.tokens.to(b1.tokens.device), b1.tokens)
+
+
+def test_blind_offload_baseline_matches_and_is_slower():
+    """Accelerate-style blind offload (per-tensor blocking copies, no overlap,
+    device sync per layer) runs the same kernels: identical outputs, slower."""
+    eng = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=2, compact=False, ecf=False)
+    try:
+        inputs = M.synthetic_inputs(M.TINY_ALPAMAYO, seed=8)
+        pl = ls.Placement.of({"vit": [0]})
+        a = eng.execute(pl, inputs=inputs, want_logits=True, record_timeline=False)
+        b = eng.execute_blind_offload(pl, inputs=inputs)
+        assert torch.equal(a.tokens, b.tokens) and torch.equal(a.actions, b.actions)
+    finally:
+        eng.close()
+    comp = DemandLayeringEngine(M.TINY_LM, vram_cap_mb=512, n_slots=2)
+    try:
+        with pytest.raises(ValueError):
+            comp.execute_blind_offload(ls.Placement.empty())
+    finally:
+        comp.close()
