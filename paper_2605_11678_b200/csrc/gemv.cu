@@ -257,6 +257,41 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
       cur_mt = mt;
     }
     if constexpr (CT && kQ == 2) {
+      if (n > 3 && kb + 3 < a.n_kb) {  // four pages of one m-tile
+        int ss[4];
+        uint32_t rr[4];
+        ss[0] = s;
+        rr[0] = round;
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+          ss[q] = ss[q - 1] + 1 == NS ? 0 : ss[q - 1] + 1;
+          rr[q] = ss[q - 1] + 1 == NS ? rr[q - 1] + 1 : rr[q - 1];
+        }
+        uint4 bw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          bw[q] = bcol ? *reinterpret_cast<const uint4*>(xb + (kb + q) * 64) : make_uint4(0u, 0u, 0u, 0u);
+        uint32_t fr[4][2][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mbar_wait(&full[ss[q]], rr[q] & 1);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ect_frags(stages + ss[q] * kStage, tile + q, fr[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          mma_bf16_16816(acc, fr[q][0], bw[q].x, bw[q].y);
+          mma_bf16_16816(acc, fr[q][1], bw[q].z, bw[q].w);
+        }
+        __syncwarp();
+        if (lane == 0)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) mbar_arrive(&empty[ss[q]]);
+        kb += 4;
+        s = ss[3] + 1 == NS ? 0 : ss[3] + 1;
+        round = ss[3] + 1 == NS ? rr[3] + 1 : rr[3];
+        n -= 3;
+        tile += 3;
+        continue;
+      }
       if (n > 1 && kb + 1 < a.n_kb) {
         const int s1 = s + 1 == NS ? 0 : s + 1;
         const uint32_t round1 = s + 1 == NS ? round + 1 : round;
