@@ -237,17 +237,17 @@ struct ls_exec {
   char* scratch = nullptr;       // decoded ECT layer (counted as overhead)
   bool ct_fused = true;          // kernels read ECT pages (else decode each layer to the scratch)
   uint64_t scratch_bytes = 0;
-  int S = 0, ctx = 0, Tv = 0, Te = 0, vit_ffn_pad = 0, n_split = 1;
+  int S = 0, ctx = 0, Tv = 0, Te = 0, vit_ffn_pad = 0;
   // activations
   float *vit_h = nullptr, *lm_h = nullptr, *dec_h = nullptr, *dec_q = nullptr, *dec_attn = nullptr,
-        *dec_mlp = nullptr, *logits = nullptr, *attn_ws = nullptr, *gemv_ws = nullptr,
+        *dec_mlp = nullptr, *logits = nullptr, *gemv_ws = nullptr,
         *ex_h = nullptr, *temb_in = nullptr, *temb_mid = nullptr, *temb = nullptr,
         *actions = nullptr, *velocity = nullptr, *noise = nullptr;
   bf16 *patches = nullptr, *vit_ln = nullptr, *vit_qkv = nullptr, *vit_attn = nullptr,
        *vit_fc1 = nullptr, *merger_mid = nullptr, *lm_norm = nullptr, *lm_qkv = nullptr,
        *lm_q = nullptr, *lm_attn = nullptr, *lm_mlp = nullptr, *kv = nullptr, *ex_norm = nullptr,
        *ex_qkv = nullptr, *ex_q = nullptr, *ex_kv = nullptr, *ex_attn = nullptr, *ex_mlp = nullptr;
-  int *text_ids = nullptr, *token = nullptr, *hist = nullptr, *attn_cnt = nullptr,
+  int *text_ids = nullptr, *token = nullptr, *hist = nullptr,
       *gemv_cnt = nullptr, *flash_cnt = nullptr;
   float* flash_ws = nullptr;  // split-KV partials of the expert's joint attention
   float* gemm_ws = nullptr;   // split-K partials of skinny GEMMs (expert, T = 64)
@@ -539,9 +539,7 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.n_ctx = pos + 1;
   a.scale = 1.0f / std::sqrt(static_cast<float>(d.lm_hd));
   a.out = e->dec_attn;
-  a.ws = e->attn_ws;
-  a.counters = e->attn_cnt;
-  a.n_split = decode_attn_splits(pos + 1);  // <= 64 positions per CTA
+  a.n_split = decode_attn_splits(pos + 1);  // one cluster of <= 16 CTAs, merged over DSMEM
   KL(launch_decode_attention(a, e->ss));
   RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h, cb, pg(1)));
   RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn, nullptr,
@@ -816,9 +814,6 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     OV(amax, 16);
     OV(token, 16);
     OV(hist, 4ull * (d.decode_steps + 1));
-    e->n_split = decode_attn_splits(e->ctx + 1);
-    OV(attn_ws, 4ull * d.lm_hq * e->n_split * (d.lm_hd + 2));
-    OV(attn_cnt, 4ull * d.lm_hkv);
     e->gp_qkv = plan_gemv(QN, d.lm_d, e->nsm);
     e->gp_o = plan_gemv(d.lm_d, AH, e->nsm);
     e->gp_gu = plan_gemv(2 * d.lm_ffn, d.lm_d, e->nsm);

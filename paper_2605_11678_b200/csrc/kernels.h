@@ -105,8 +105,8 @@ struct DecodeAttnArgs {
   int hq, hkv, hd, n_ctx;
   float scale;
   float* out;              // [hq*hd]
-  float* ws;               // partials
-  int* counters;           // [hkv]
+  float* ws;               // unused (splits merge over DSMEM); kept for ABI stability
+  int* counters;           // unused
   int n_split;
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
