@@ -169,19 +169,17 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
   named_bar(1, kGemvConsumers);
 
   const int g = lane >> 2, t4 = lane & 3;
-  // mma C: rows g, g+8 x columns (hi, lo) in lanes t4 == 0; two accumulators (even /
-  // odd k-step of a warp) halve the length of the dependent HMMA chain
-  float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};  // mma C: rows g, g+8 x columns (hi, lo) in lanes t4 == 0
   int cur_mt = t0 < t1 ? static_cast<int>(t0 / a.n_kb) : -1;
 
   const int rb = warp & 7, kh = warp >> 3;  // row block, k-part
   auto flush = [&](int mt) {
     if (t4 == 0) {
-      red[kh * kTileRows + rb * 16 + g] = (acc[0] + acc1[0]) + (acc[1] + acc1[1]);
-      red[kh * kTileRows + rb * 16 + g + 8] = (acc[2] + acc1[2]) + (acc[3] + acc1[3]);
+      red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
+      red[kh * kTileRows + rb * 16 + g + 8] = acc[2] + acc[3];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = acc1[j] = 0.f;
+    for (int j = 0; j < 4; ++j) acc[j] = 0.f;
     named_bar(1, kGemvConsumers);
     if (tid < kTileRows) {
       float v = red[tid];
@@ -281,7 +279,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           mma_bf16_16816(acc, fr[q][0], bw[q].x, bw[q].y);
-          mma_bf16_16816(acc1, fr[q][1], bw[q].z, bw[q].w);
+          mma_bf16_16816(acc, fr[q][1], bw[q].z, bw[q].w);
         }
         __syncwarp();
         if (lane == 0)
@@ -309,9 +307,9 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
         ect_frags(stages + s * kStage, tile, fa);
         ect_frags(stages + s1 * kStage, tile + 1, fb);
         mma_bf16_16816(acc, fa[0], bw0.x, bw0.y);
-        mma_bf16_16816(acc1, fa[1], bw0.z, bw0.w);
+        mma_bf16_16816(acc, fa[1], bw0.z, bw0.w);
         mma_bf16_16816(acc, fb[0], bw1.x, bw1.y);
-        mma_bf16_16816(acc1, fb[1], bw1.z, bw1.w);
+        mma_bf16_16816(acc, fb[1], bw1.z, bw1.w);
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&empty[s]);
@@ -354,7 +352,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
         ldsm_x4(af[q], st + lr * 128 + (((2 * (2 * kh + q) + lc) ^ (lr & 7)) << 4));
     }
     mma_bf16_16816(acc, af[0], bw.x, bw.y);
-    mma_bf16_16816(acc1, af[1], bw.z, bw.w);
+    mma_bf16_16816(acc, af[1], bw.z, bw.w);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
