@@ -10,9 +10,11 @@ from __future__ import annotations
 import ctypes as C
 import threading
 import weakref
+import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblayerswap_b200.so"
+_LIB_PATH = Path(os.environ.get("LS_LIB_PATH") or  # diagnostic builds (tools/); default: the in-tree build
+                 Path(__file__).resolve().parent / "_lib" / "liblayerswap_b200.so")
 
 LS_OK = 0
 LS_ERR_VALUE = 1

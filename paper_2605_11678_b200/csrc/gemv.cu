@@ -42,17 +42,23 @@ __host__ __device__ inline int gemv_stages(int n_kb) {
 }
 // NW consumer warps = 8 row blocks x NW/8 k-parts of every tile (16: two k-steps
 // per warp -- the launched configuration; 32 would exceed 1024 threads with the
-// producer warp).  The RMSNorm reduction always uses the first 16 warps.
+// producer warp).
 template <int NW>
 struct GemvShape {
   static constexpr int kConsumers = NW * 32;
   static constexpr int kThreads = kConsumers + 32;
   static constexpr int kQ = NW / 8;  // k-parts per tile
 };
-constexpr int kNormThreads = 512;
 
-__device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
-  return static_cast<int>(((t + 1) * G - 1) / T);
+#ifndef LS_GEMV_EXP
+#define LS_GEMV_EXP 0
+#endif
+__device__ __forceinline__ void gemv_mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+#if LS_GEMV_EXP & 2  // diagnostic build: operands consumed, no tensor-core work
+  asm volatile("" ::"r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+#else
+  mma_bf16_16816(c, a, b0, b1);
+#endif
 }
 
 // Consumers run the dot products on the tensor cores: mma.sync m16n8k16 with
@@ -132,40 +138,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
     exc_off = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_excoff) + a.ct_page0;
     exc = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_exc);
   }
-  pdl_wait();  // x, workspace and outputs belong to the previous kernel until here
-  // fused RMSNorm: sum of squares in a fixed order (threads < 256, stride 256)
-  float rstd = 1.f;
-  if (a.norm_w) {
-    float ss = 0.f;
-    if (tid < kNormThreads)
-      for (int k = tid; k < K; k += kNormThreads) {
-        const float v = a.x[k];
-        ss = fmaf(v, v, ss);
-      }
-    ss = warp_sum(ss);
-    if (lane == 0 && warp < kNormThreads / 32) scratch[warp] = ss;
-    named_bar(1, kGemvConsumers);
-    float tot = 0.f;
-#pragma unroll
-    for (int w = 0; w < kNormThreads / 32; ++w) tot += scratch[w];
-    rstd = rsqrtf(tot / K + a.eps);
-  }
-  // x -> (hi, lo) bf16 pairs, scattered into the B-word layout above
-  for (int i = tid; i < K / 2; i += kGemvConsumers) {  // pair i = k 2i, 2i+1
-    float v0 = a.x[2 * i], v1 = a.x[2 * i + 1];
-    if (a.norm_w) {
-      v0 = v0 * rstd * bf2f(a.norm_w[2 * i]);
-      v1 = v1 * rstd * bf2f(a.norm_w[2 * i + 1]);
-    }
-    const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
-    const float2 hf = __bfloat1622float2(hi);
-    const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
-    const int kb = i >> 5, pp = i & 31;  // pair within the k-block: 16 h + 8 (ks&1) + 4 (b1) + t4
-    const int h = pp >> 4, slot = ((pp >> 3) & 1) * 2 + ((pp >> 2) & 1), t4i = pp & 3;
-    const int base = kb * 64 + h * 32 + t4i * 4 + slot;
-    xq[base] = *reinterpret_cast<const uint32_t*>(&hi);
-    xq[base + 16] = *reinterpret_cast<const uint32_t*>(&lo);
-  }
+  gemv_stage_x<kGemvConsumers>(a, xq, scratch, K, tid, lane, warp);
   named_bar(1, kGemvConsumers);
 
   const int g = lane >> 2, t4 = lane & 3;
@@ -174,51 +147,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
 
   const int rb = warp & 7, kh = warp >> 3;  // row block, k-part
   auto flush = [&](int mt) {
-    if (t4 == 0) {
-      red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
-      red[kh * kTileRows + rb * 16 + g + 8] = acc[2] + acc[3];
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = 0.f;
-    named_bar(1, kGemvConsumers);
-    if (tid < kTileRows) {
-      float v = red[tid];
-#pragma unroll
-      for (int q = 1; q < kQ; ++q) v += red[q * kTileRows + tid];
-      red[tid] = v;
-    }
-    named_bar(1, kGemvConsumers);
-    const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
-    const int c_first = cta_of_tile(first, G, T);
-    const int n_contrib = cta_of_tile(last, G, T) - c_first + 1;
-    if (n_contrib == 1) {
-      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
-      named_bar(1, kGemvConsumers);
-      return;
-    }
-    const int slot = c - c_first;
-    float* mine = a.ws + (static_cast<long>(mt) * a.max_contrib + slot) * kTileRows;
-    if (tid < kTileRows) mine[tid] = red[tid];
-    __threadfence();
-    named_bar(1, kGemvConsumers);
-    if (tid == 0) {
-      const int old = atomicAdd(&a.counters[mt], 1);
-      *flag = (old == n_contrib - 1);
-    }
-    named_bar(1, kGemvConsumers);
-    if (*flag) {
-      __threadfence();
-      if (tid < kTileRows) {
-        const float* base = a.ws + static_cast<long>(mt) * a.max_contrib * kTileRows;
-        float s = 0.f;
-        for (int j = 0; j < n_contrib; ++j) s += __ldcg(base + j * kTileRows + tid);
-        red[tid] = s;
-      }
-      named_bar(1, kGemvConsumers);
-      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
-      if (tid == 0) a.counters[mt] = 0;
-    }
-    named_bar(1, kGemvConsumers);
+    gemv_flush<EPI, kGemvConsumers, kQ>(a, acc, red, flag, mt, G, T, c, tid, g, t4, rb, kh);
   };
 
   // B words: column g = 0 -> hi, g = 1 -> lo, other columns zero
@@ -240,6 +169,11 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
   auto ect_frags = [&](const uint8_t* st, uint32_t pg_idx, uint32_t (&af)[2][4]) {
     const uint4 sm = *reinterpret_cast<const uint4*>(st + f0 * 8);
     const uint2 nib = *reinterpret_cast<const uint2*>(st + kEctPageWords + f0 * 4);
+#if LS_GEMV_EXP & 1  // diagnostic build: no decode (wrong results, timing only)
+    af[0][0] = sm.x; af[0][1] = sm.y; af[0][2] = nib.x; af[0][3] = sm.x ^ nib.x;
+    af[1][0] = sm.z; af[1][1] = sm.w; af[1][2] = nib.y; af[1][3] = sm.z ^ nib.y;
+    return;
+#endif
     uint4 w0 = ect_decode8(make_uint2(sm.x, sm.y), nib.x, e0p);
     uint4 w1 = ect_decode8(make_uint2(sm.z, sm.w), nib.y, e0p);
     if (ect_escapes(nib.x) | ect_escapes(nib.y)) {
@@ -278,8 +212,8 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
         for (int q = 0; q < 4; ++q) ect_frags(stages + ss[q] * kStage, tile + q, fr[q]);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          mma_bf16_16816(acc, fr[q][0], bw[q].x, bw[q].y);
-          mma_bf16_16816(acc, fr[q][1], bw[q].z, bw[q].w);
+          gemv_mma(acc, fr[q][0], bw[q].x, bw[q].y);
+          gemv_mma(acc, fr[q][1], bw[q].z, bw[q].w);
         }
         __syncwarp();
         if (lane == 0)
@@ -306,10 +240,10 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
         mbar_wait(&full[s1], round1 & 1);
         ect_frags(stages + s * kStage, tile, fa);
         ect_frags(stages + s1 * kStage, tile + 1, fb);
-        mma_bf16_16816(acc, fa[0], bw0.x, bw0.y);
-        mma_bf16_16816(acc, fa[1], bw0.z, bw0.w);
-        mma_bf16_16816(acc, fb[0], bw1.x, bw1.y);
-        mma_bf16_16816(acc, fb[1], bw1.z, bw1.w);
+        gemv_mma(acc, fa[0], bw0.x, bw0.y);
+        gemv_mma(acc, fa[1], bw0.z, bw0.w);
+        gemv_mma(acc, fb[0], bw1.x, bw1.y);
+        gemv_mma(acc, fb[1], bw1.z, bw1.w);
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&empty[s]);
@@ -339,7 +273,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
       } else {
         ldsm_x4(af, st + lr * 128 + (((2 * kh + lc) ^ (lr & 7)) << 4));
       }
-      mma_bf16_16816(acc, af, bw.x, bw.y);
+      gemv_mma(acc, af, bw.x, bw.y);
     } else {
     uint4 bw = make_uint4(0u, 0u, 0u, 0u);
     if (bcol) bw = *reinterpret_cast<const uint4*>(xb + kb * 64);
@@ -351,8 +285,8 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
       for (int q = 0; q < 2; ++q)
         ldsm_x4(af[q], st + lr * 128 + (((2 * (2 * kh + q) + lc) ^ (lr & 7)) << 4));
     }
-    mma_bf16_16816(acc, af[0], bw.x, bw.y);
-    mma_bf16_16816(acc, af[1], bw.z, bw.w);
+    gemv_mma(acc, af[0], bw.x, bw.y);
+    gemv_mma(acc, af[1], bw.z, bw.w);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -416,7 +350,11 @@ static cudaError_t launch_ct(int epi, const GemvArgs& a, int grid, cudaStream_t 
 }
 
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
+#if LS_GEMV_ECT_LEGACY  // diagnostic build: ECT pages through the generic kernel
   return a.ct_blob ? launch_ct<true, 16>(epi, a, grid, st) : launch_ct<false, 16>(epi, a, grid, st);
+#else
+  return a.ct_blob ? launch_gemv_ect(epi, a, grid, st) : launch_ct<false, 16>(epi, a, grid, st);
+#endif
 }
 
 }  // namespace lsb

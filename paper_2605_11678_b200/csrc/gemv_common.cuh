@@ -19,6 +19,55 @@ __device__ __forceinline__ float dot8(uint4 w, const float4& a, const float4& b)
   return s;
 }
 
+// x pairs held in registers by the GEMV prologue: K <= 2 * kXRegPairs * 512
+constexpr int kXRegPairs = 12;
+
+// pair i = (x[2i], x[2i+1]) -> (hi, lo) bf16 B words in the layout of gemv_kernel's xq
+__device__ __forceinline__ void gemv_stage_pair(uint32_t* xq, int i, float v0, float v1) {
+  const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+  const float2 hf = __bfloat1622float2(hi);
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+  const int kb = i >> 5, pp = i & 31;  // pair within the k-block: 16 h + 8 (ks&1) + 4 (b1) + t4
+  const int h = pp >> 4, slot = ((pp >> 3) & 1) * 2 + ((pp >> 2) & 1), t4i = pp & 3;
+  const int base = kb * 64 + h * 32 + t4i * 4 + slot;
+  xq[base] = *reinterpret_cast<const uint32_t*>(&hi);
+  xq[base + 16] = *reinterpret_cast<const uint32_t*>(&lo);
+}
+
+// Prologue for K beyond the register path: two passes over x in global memory.
+static __device__ __noinline__ void gemv_stage_x_loop(const float* x, const bf16* norm_w, float eps, uint32_t* xq,
+                                               float* scratch, int K, int tid, int lane, int warp,
+                                               int n_consumers) {
+  float rstd = 1.f;
+  if (norm_w) {
+    float ss = 0.f;
+    for (int i = tid; i < K / 2; i += n_consumers) {
+      const float2 v = reinterpret_cast<const float2*>(x)[i];
+      ss = fmaf(v.x, v.x, ss);
+      ss = fmaf(v.y, v.y, ss);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) scratch[warp] = ss;
+    named_bar(1, n_consumers);
+    float tot = 0.f;
+    for (int w = 0; w < n_consumers / 32; ++w) tot += scratch[w];
+    rstd = rsqrtf(tot / K + eps);
+  }
+  for (int i = tid; i < K / 2; i += n_consumers) {
+    float2 v = reinterpret_cast<const float2*>(x)[i];
+    if (norm_w) {
+      const float2 nw = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(norm_w)[i]);
+      v.x = v.x * rstd * nw.x;
+      v.y = v.y * rstd * nw.y;
+    }
+    gemv_stage_pair(xq, i, v.x, v.y);
+  }
+}
+
+__device__ __forceinline__ int cta_of_tile(long t, int G, long T) {
+  return static_cast<int>(((t + 1) * G - 1) / T);
+}
+
 template <int EPI>
 __device__ void gemv_epilogue(const GemvArgs& a, int mt, const float* red, int tid) {
   // tid in [0,128): one output row each
@@ -95,5 +144,112 @@ __device__ inline void gemv_epilogue_any(int epi, const GemvArgs& a, int mt, con
     default: gemv_epilogue<GEMV_ARGMAX>(a, mt, red, tid); break;
   }
 }
+
+// Consumer prologue shared by the decode GEMVs: x (fp32, optional fused
+// RMSNorm) -> the (hi, lo) bf16 B-word layout in shared memory.  Contains the
+// kernel's pdl_wait.  Ends without a barrier (callers sync the NC consumers).
+template <int NC>
+__device__ __forceinline__ void gemv_stage_x(const GemvArgs& a, uint32_t* xq, float* scratch, int K, int tid,
+                                             int lane, int warp) {
+  // x pairs i = tid + j * consumers live in registers between the load, the
+  // RMSNorm reduction and the scatter (one global round trip after pdl_wait);
+  // the norm weights do not come from the previous kernel and load before it.
+  const int KP = K / 2;
+  if (KP <= kXRegPairs * NC) {
+    float2 xv[kXRegPairs];
+    float2 nv[kXRegPairs];
+#pragma unroll
+    for (int j = 0; j < kXRegPairs; ++j) {
+      const int i = tid + j * NC;
+      nv[j] = make_float2(1.f, 1.f);
+      if (a.norm_w && i < KP)
+        nv[j] = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(a.norm_w)[i]);
+    }
+    pdl_wait();  // x, workspace and outputs belong to the previous kernel until here
+#pragma unroll
+    for (int j = 0; j < kXRegPairs; ++j) {
+      const int i = tid + j * NC;
+      xv[j] = i < KP ? reinterpret_cast<const float2*>(a.x)[i] : make_float2(0.f, 0.f);
+    }
+    float rstd = 1.f;
+    if (a.norm_w) {  // sum of squares: per-thread pairs in j order, warps in order
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < kXRegPairs; ++j) {
+        ss = fmaf(xv[j].x, xv[j].x, ss);
+        ss = fmaf(xv[j].y, xv[j].y, ss);
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) scratch[warp] = ss;
+      named_bar(1, NC);
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < NC / 32; ++w) tot += scratch[w];
+      rstd = rsqrtf(tot / K + a.eps);
+    }
+#pragma unroll
+    for (int j = 0; j < kXRegPairs; ++j) {
+      const int i = tid + j * NC;
+      if (i < KP) gemv_stage_pair(xq, i, xv[j].x * rstd * nv[j].x, xv[j].y * rstd * nv[j].y);
+    }
+  } else {
+    pdl_wait();
+    gemv_stage_x_loop(a.x, a.norm_w, a.eps, xq, scratch, K, tid, lane, warp, NC);
+  }
+}
+
+// End of an m-tile: the NC consumer warps' partials (acc: rows g, g + 8 of row
+// block rb, k-part kh) -> red, k-parts summed in order, then either the fused
+// epilogue or the deterministic stream-K fix-up (workspace slot per
+// contributing CTA, last arriver sums in contributor order).  Zeroes acc.
+template <int EPI, int NC, int kQ>
+__device__ __forceinline__ void gemv_flush(const GemvArgs& a, float (&acc)[4], float* red, int* flag, int mt,
+                                           int G, long T, int c, int tid, int g, int t4, int rb, int kh) {
+    if (t4 == 0) {
+      red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
+      red[kh * kTileRows + rb * 16 + g + 8] = acc[2] + acc[3];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = 0.f;
+    named_bar(1, NC);
+    if (tid < kTileRows) {
+      float v = red[tid];
+#pragma unroll
+      for (int q = 1; q < kQ; ++q) v += red[q * kTileRows + tid];
+      red[tid] = v;
+    }
+    named_bar(1, NC);
+    const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
+    const int c_first = cta_of_tile(first, G, T);
+    const int n_contrib = cta_of_tile(last, G, T) - c_first + 1;
+    if (n_contrib == 1) {
+      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
+      named_bar(1, NC);
+      return;
+    }
+    const int slot = c - c_first;
+    float* mine = a.ws + (static_cast<long>(mt) * a.max_contrib + slot) * kTileRows;
+    if (tid < kTileRows) mine[tid] = red[tid];
+    __threadfence();
+    named_bar(1, NC);
+    if (tid == 0) {
+      const int old = atomicAdd(&a.counters[mt], 1);
+      *flag = (old == n_contrib - 1);
+    }
+    named_bar(1, NC);
+    if (*flag) {
+      __threadfence();
+      if (tid < kTileRows) {
+        const float* base = a.ws + static_cast<long>(mt) * a.max_contrib * kTileRows;
+        float s = 0.f;
+        for (int j = 0; j < n_contrib; ++j) s += __ldcg(base + j * kTileRows + tid);
+        red[tid] = s;
+      }
+      named_bar(1, NC);
+      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
+      if (tid == 0) a.counters[mt] = 0;
+    }
+    named_bar(1, NC);
+  }
 
 }  // namespace lsb

@@ -55,6 +55,8 @@ struct GemvArgs {
 int gemv_max_contrib(int n_mt, int n_kb, int grid);
 int gemv_grid(int n_mt, int n_kb, int num_sms);
 cudaError_t launch_gemv(int epi, const GemvArgs& a, int grid, cudaStream_t st);
+// ECT pages (a.ct_blob set): gemv_ect.cu; launch_gemv dispatches there
+cudaError_t launch_gemv_ect(int epi, const GemvArgs& a, int grid, cudaStream_t st);
 
 // ---------------- tcgen05 GEMM: Y[T x N] = X[T x K] * W^T ---------------------
 enum GemmEpi : int {
@@ -202,7 +204,10 @@ struct EctHeader {
   uint64_t off_pages, off_tail, off_excoff, off_exc;
   uint32_t n_exc, e0;
   uint8_t codebook[16];
-  uint8_t _pad[48];
+  // per page u32: bit r set <=> page words [256 r, 256 r + 256) hold an escape
+  // (code 15); 0 = section absent (decoders then test every code)
+  uint64_t off_escmask;
+  uint8_t _pad[40];
 };
 static_assert(sizeof(EctHeader) == 128, "ECT header is 128 bytes");
 // blob -> plain layer bytes (whole 16-byte chunks: out needs a16(total) bytes);

@@ -28,6 +28,30 @@ def test_cpu_roundtrip_ratio_and_escapes():
     assert blob.numel() / buf.numel() < 0.76
 
 
+def test_escape_region_mask_matches_codes():
+    """escmask word r bit l of page p <=> a code-15 nibble among page words
+    [16 (32 r + l), +16) -- the 16 words decode-GEMV lane l of warp region r
+    decodes -- so the GEMV tests codes only where the mask says so."""
+    buf, mat = _layer(6, 0, seed=3)
+    blob = ect.compress(buf, mat)
+    h = ect.header(blob)
+    n = h["n_pages"]
+    assert h["off_escmask"] % 16 == 0 and h["off_exc"] >= h["off_escmask"] + 64 * n
+    pages = blob[h["off_pages"]:h["off_pages"] + n * ect.PAGE_BYTES].view(n, ect.PAGE_BYTES)
+    nib = pages[:, ect.PAGE_WORDS:].to(torch.int64)
+    code = torch.stack([nib & 0xF, nib >> 4], 2).reshape(n, ect.PAGE_WORDS)
+    mask = blob[h["off_escmask"]:h["off_escmask"] + 64 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    mask = mask.view(n, 16)
+    for p in range(n):
+        for r in range(16):
+            for lane in range(32):
+                w0 = 16 * (32 * r + lane)
+                want = bool((code[p, w0:w0 + 16] == 15).any())
+                assert bool((mask[p, r] >> lane) & 1) == want, (p, r, lane)
+    assert int(mask[0, 0]) & 1  # the zero padding rows escape (exponent 0)
+    assert int(mask.sum()) < n * 16 * 0xFFFFFFFF  # most groups are escape-free
+
+
 def test_cpu_roundtrip_no_tail_and_single_page():
     buf, mat = _layer(1, 0, seed=2)
     assert torch.equal(ect.decompress_cpu(ect.compress(buf, mat)), buf)
