@@ -143,13 +143,14 @@ __device__ __forceinline__ uint4 ect_zero_escapes(uint4 w, uint32_t t) {
 // true exponents come from the page's exception list.
 static __device__ __noinline__ uint4 ect_patch8(uint4 w, uint32_t t, uint32_t page, uint32_t word0,
                                                 const uint32_t* exc_off, const uint32_t* exc) {
-  const uint32_t b = exc_off[page], e = exc_off[page + 1];
+  const uint32_t b = __ldg(exc_off + page), e = __ldg(exc_off + page + 1);
   uint32_t v[4] = {w.x, w.y, w.z, w.w};
-  for (int k = 0; k < 8; ++k) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // unrolled: v stays in registers
     if (!((t >> (4 * k)) & 1u)) continue;
     uint32_t ex = 0;
     for (uint32_t i = b; i < e; ++i) {
-      const uint32_t x = exc[i];
+      const uint32_t x = __ldg(exc + i);
       if ((x >> 8) == word0 + k) {
         ex = x & 0xFFu;
         break;
@@ -211,6 +212,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// Same on a precomputed shared-memory address (hot loops: no address conversion)
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"

@@ -150,10 +150,10 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
     gemv_flush<EPI, kGemvConsumers, kQ>(a, acc, red, flag, mt, G, T, c, tid, g, t4, rb, kh);
   };
 
-  // B words: column g = 0 -> hi, g = 1 -> lo, other columns zero
+  // B words: column g = 0 -> hi, g = 1 -> lo; columns g >= 2 repeat them and
+  // only reach C columns >= 2 (lanes t4 != 0), which the flush ignores
   const uint32_t* xb = xq + (kQ == 2 ? kh : kh >> 1) * 32 + (g & 1) * 16 + t4 * 4 +
                        (kQ == 2 ? 0 : (kh & 1) * 2);
-  const bool bcol = g < 2;
   // ldmatrix.x4 row address of this lane inside a plain tile (k-step added per use)
   const int lr = rb * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
   const int lc = lane >> 4;  // 0: k 0-7 of the step, 1: k 8-15
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
         uint4 bw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          bw[q] = bcol ? *reinterpret_cast<const uint4*>(xb + (kb + q) * 64) : make_uint4(0u, 0u, 0u, 0u);
+          bw[q] = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
         uint32_t fr[4][2][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) mbar_wait(&full[ss[q]], rr[q] & 1);
@@ -229,11 +229,8 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
       if (n > 1 && kb + 1 < a.n_kb) {
         const int s1 = s + 1 == NS ? 0 : s + 1;
         const uint32_t round1 = s + 1 == NS ? round + 1 : round;
-        uint4 bw0 = make_uint4(0u, 0u, 0u, 0u), bw1 = bw0;
-        if (bcol) {
-          bw0 = *reinterpret_cast<const uint4*>(xb + kb * 64);
-          bw1 = *reinterpret_cast<const uint4*>(xb + (kb + 1) * 64);
-        }
+        const uint4 bw0 = *reinterpret_cast<const uint4*>(xb + kb * 64);
+        const uint4 bw1 = *reinterpret_cast<const uint4*>(xb + (kb + 1) * 64);
         uint32_t fa[2][4], fb[2][4];
         // both pages first, so the two pages' loads and decode chains interleave
         mbar_wait(&full[s], round & 1);
@@ -260,8 +257,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
     mbar_wait(&full[s], round & 1);
     const uint8_t* st = stages + s * kStage;
     if constexpr (kQ == 4) {  // one k-step per warp and tile
-      uint2 bw = make_uint2(0u, 0u);
-      if (bcol) bw = *reinterpret_cast<const uint2*>(xb + kb * 64);
+      const uint2 bw = *reinterpret_cast<const uint2*>(xb + kb * 64);
       uint32_t af[4];
       if constexpr (CT) {
         const uint2 sm = *reinterpret_cast<const uint2*>(st + f0 * 8);
@@ -275,8 +271,7 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
       }
       gemv_mma(acc, af, bw.x, bw.y);
     } else {
-    uint4 bw = make_uint4(0u, 0u, 0u, 0u);
-    if (bcol) bw = *reinterpret_cast<const uint4*>(xb + kb * 64);
+    const uint4 bw = *reinterpret_cast<const uint4*>(xb + kb * 64);
     uint32_t af[2][4];
     if constexpr (CT) {
       ect_frags(st, tile, af);

@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   const int rb = warp & 7, kh = warp >> 3;  // row block, k-part (k-steps 2 kh, 2 kh + 1)
   const int wreg = rb * 2 + kh;             // escape-mask word of this warp
   const int f0 = (wreg * 32 + lane) * 2;    // this lane's two fragments in a page
-  const uint32_t* xb = xq + kh * 32 + (g & 1) * 16 + t4 * 4;  // B words: g 0 -> hi, 1 -> lo
-  const bool bcol = g < 2;
+  // B words: column g = 0 -> hi, 1 -> lo; columns g >= 2 repeat them and only
+  // reach C columns >= 2, which lanes t4 != 0 hold and the flush ignores
+  const uint32_t* xb = xq + kh * 32 + (g & 1) * 16 + t4 * 4;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 
   auto frags = [&](const uint8_t* pg, uint32_t page, bool esc, uint32_t (&af)[2][4]) {
@@ -132,29 +133,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
     af[0][0] = w0.x; af[0][1] = w0.y; af[0][2] = w0.z; af[0][3] = w0.w;
     af[1][0] = w1.x; af[1][1] = w1.y; af[1][2] = w1.z; af[1][3] = w1.w;
   };
+  // without a mask section every lane takes the escape test (the slot's mask
+  // area then holds stale bytes, overridden by no_mask)
+  const uint32_t no_mask = has_mask ? 0u : 0xffffffffu;
   auto lane_esc = [&](const uint8_t* st, int q) -> bool {
-    if (!has_mask) return true;
     const uint32_t m = *reinterpret_cast<const uint32_t*>(st + kChunk * kEctPageBytes + q * kMaskBytes + wreg * 4);
-    return (m >> lane) & 1u;
+    return ((m | no_mask) >> lane) & 1u;
   };
 
   int kb = static_cast<int>(t0 % a.n_kb), mt = static_cast<int>(t0 / a.n_kb), s = 0;
-  uint32_t round = 0;
-  for (long t = t0; t < t1;) {
-    int np = a.n_kb - kb;
-    if (np > kChunk) np = kChunk;
-    if (np > t1 - t) np = static_cast<int>(t1 - t);
+  int rem = static_cast<int>(t1 - t0);
+  uint32_t t = static_cast<uint32_t>(t0), round = 0;
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  while (rem > 0) {
+    const int np = min(min(kChunk, a.n_kb - kb), rem);
     const uint8_t* st = slots + s * kSlotBytes;
-    mbar_wait(&full[s], round & 1);
+    mbar_wait_u32(full0 + 8 * s, round & 1);
     if (np == kChunk) {
       uint4 bw[kChunk];
 #pragma unroll
       for (int q = 0; q < kChunk; ++q)
-        bw[q] = bcol ? *reinterpret_cast<const uint4*>(xb + (kb + q) * 64) : make_uint4(0u, 0u, 0u, 0u);
+        bw[q] = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
       uint32_t fr[kChunk][2][4];
 #pragma unroll
       for (int q = 0; q < kChunk; ++q)
-        frags(st + q * kEctPageBytes, static_cast<uint32_t>(t) + q, lane_esc(st, q), fr[q]);
+        frags(st + q * kEctPageBytes, t + q, lane_esc(st, q), fr[q]);
 #pragma unroll
       for (int q = 0; q < kChunk; ++q) {
         mma_bf16_16816(acc, fr[q][0], bw[q].x, bw[q].y);
@@ -162,20 +165,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
       }
     } else {
       for (int q = 0; q < np; ++q) {
-        const uint4 bw = bcol ? *reinterpret_cast<const uint4*>(xb + (kb + q) * 64) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 bw = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
         uint32_t fr[2][4];
-        frags(st + q * kEctPageBytes, static_cast<uint32_t>(t) + q, lane_esc(st, q), fr);
+        frags(st + q * kEctPageBytes, t + q, lane_esc(st, q), fr);
         mma_bf16_16816(acc, fr[0], bw.x, bw.y);
         mma_bf16_16816(acc, fr[1], bw.z, bw.w);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive_u32(empty0 + 8 * s);
     if (++s == NQ) {
       s = 0;
       ++round;
     }
     t += np;
+    rem -= np;
     kb += np;
     if (kb == a.n_kb) {
       gemv_flush<EPI, kConsumers, 2>(a, acc, red, flag, mt, G, T, c, tid, g, t4, rb, kh);
