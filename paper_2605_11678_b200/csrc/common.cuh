@@ -162,6 +162,29 @@ static __device__ __noinline__ uint4 ect_patch8(uint4 w, uint32_t t, uint32_t pa
   return make_uint4(v[0], v[1], v[2], v[3]);
 }
 
+// Slow path for one lane's 16 consecutive page words (two fragments from
+// page word `word0`; t0 / t1 = ect_escapes of their code words): escaped words
+// take exponent 0, then the page's exceptions inside [word0, word0 + 16) --
+// usually none or one -- set the true exponents.
+__device__ __forceinline__ void ect_patch16(uint4& w0, uint4& w1, uint32_t t0, uint32_t t1, uint32_t page,
+                                            uint32_t word0, const uint32_t* exc_off, const uint32_t* exc) {
+  w0 = ect_zero_escapes(w0, t0);
+  w1 = ect_zero_escapes(w1, t1);
+  const uint32_t b = __ldg(exc_off + page), e = __ldg(exc_off + page + 1);
+  for (uint32_t i = b; i < e; ++i) {
+    const uint32_t x = __ldg(exc + i);
+    const uint32_t k = (x >> 8) - word0;  // word within this lane's 16 (wraps when below)
+    if (k >= 16u) continue;
+    const uint32_t sh = 16u * (k & 1u), ex = ((x & 0xFFu) << 7) << sh;
+    const uint32_t j = (k >> 1) & 3u;
+    uint4& w = k < 8u ? w0 : w1;
+    if (j == 0) w.x |= ex;
+    else if (j == 1) w.y |= ex;
+    else if (j == 2) w.z |= ex;
+    else w.w |= ex;
+  }
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

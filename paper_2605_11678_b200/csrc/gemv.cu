@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
   const int NS = gemv_stages<CT>(a.n_kb);
   // x as bf16x2 B words: [kb][half h][column hi|lo][t4][b0(2h), b1(2h), b0(2h+1), b1(2h+1)]
   uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NS * kStage);
-  float* red = reinterpret_cast<float*>(xq + K);  // [kQ][128]: one slice per k-part
-  float* scratch = red + kQ * kTileRows;  // 16 floats for block reductions
+  float* red = reinterpret_cast<float*>(xq + K);  // 2 x [kQ][128]: one slice per k-part
+  float* scratch = red + 2 * kQ * kTileRows;      // 16 floats for block reductions
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
   uint64_t* empty = full + kGemvMaxStages;
   int* flag = reinterpret_cast<int*>(empty + kGemvMaxStages);
@@ -146,8 +146,9 @@ __global__ void __launch_bounds__(GemvShape<NW>::kThreads, 1) gemv_kernel(const 
   int cur_mt = t0 < t1 ? static_cast<int>(t0 / a.n_kb) : -1;
 
   const int rb = warp & 7, kh = warp >> 3;  // row block, k-part
+  int par = 0;  // red buffer of the next flush
   auto flush = [&](int mt) {
-    gemv_flush<EPI, kGemvConsumers, kQ>(a, acc, red, flag, mt, G, T, c, tid, g, t4, rb, kh);
+    gemv_flush<EPI, kGemvConsumers, kQ>(a, acc, red, par, flag, mt, G, T, c, tid, g, t4, rb, kh);
   };
 
   // B words: column g = 0 -> hi, g = 1 -> lo; columns g >= 2 repeat them and
@@ -314,7 +315,7 @@ int gemv_max_contrib(int n_mt, int n_kb, int grid) {
 template <bool CT>
 static size_t gemv_smem(int n_kb) {
   return static_cast<size_t>(gemv_stages<CT>(n_kb)) * (CT ? kEctPageBytes : kTileBytes) +
-         static_cast<size_t>(n_kb) * kTileCols * 4 + 4 * kTileRows * 4 + 16 * 4 +
+         static_cast<size_t>(n_kb) * kTileCols * 4 + 2 * 2 * kTileRows * 4 + 16 * 4 +
          2 * kGemvMaxStages * 8 + 16;
 }
 

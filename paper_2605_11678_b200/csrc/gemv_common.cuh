@@ -202,54 +202,62 @@ __device__ __forceinline__ void gemv_stage_x(const GemvArgs& a, uint32_t* xq, fl
 // block rb, k-part kh) -> red, k-parts summed in order, then either the fused
 // epilogue or the deterministic stream-K fix-up (workspace slot per
 // contributing CTA, last arriver sums in contributor order).  Zeroes acc.
+// red holds two [kQ][128] buffers used alternately (par flips per call): after
+// the one all-consumer barrier only warps 0-3 (one thread per row) finish the
+// m-tile -- fix-up and epilogue under their own barrier -- while the other
+// warps go on decoding; the next call's barrier orders buffer reuse.
+__device__ __forceinline__ int gemv_cta_of_tile(long t, int G, long T) {
+  if (T * G < (1l << 32))  // 32-bit division when it fits (all decode shapes)
+    return static_cast<int>((static_cast<uint32_t>(t + 1) * static_cast<uint32_t>(G) - 1u) /
+                            static_cast<uint32_t>(T));
+  return cta_of_tile(t, G, T);
+}
+
 template <int EPI, int NC, int kQ>
-__device__ __forceinline__ void gemv_flush(const GemvArgs& a, float (&acc)[4], float* red, int* flag, int mt,
-                                           int G, long T, int c, int tid, int g, int t4, int rb, int kh) {
-    if (t4 == 0) {
-      red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
-      red[kh * kTileRows + rb * 16 + g + 8] = acc[2] + acc[3];
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = 0.f;
-    named_bar(1, NC);
-    if (tid < kTileRows) {
-      float v = red[tid];
-#pragma unroll
-      for (int q = 1; q < kQ; ++q) v += red[q * kTileRows + tid];
-      red[tid] = v;
-    }
-    named_bar(1, NC);
-    const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
-    const int c_first = cta_of_tile(first, G, T);
-    const int n_contrib = cta_of_tile(last, G, T) - c_first + 1;
-    if (n_contrib == 1) {
-      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
-      named_bar(1, NC);
-      return;
-    }
-    const int slot = c - c_first;
-    float* mine = a.ws + (static_cast<long>(mt) * a.max_contrib + slot) * kTileRows;
-    if (tid < kTileRows) mine[tid] = red[tid];
-    __threadfence();
-    named_bar(1, NC);
-    if (tid == 0) {
-      const int old = atomicAdd(&a.counters[mt], 1);
-      *flag = (old == n_contrib - 1);
-    }
-    named_bar(1, NC);
-    if (*flag) {
-      __threadfence();
-      if (tid < kTileRows) {
-        const float* base = a.ws + static_cast<long>(mt) * a.max_contrib * kTileRows;
-        float s = 0.f;
-        for (int j = 0; j < n_contrib; ++j) s += __ldcg(base + j * kTileRows + tid);
-        red[tid] = s;
-      }
-      named_bar(1, NC);
-      if (tid < kTileRows) gemv_epilogue<EPI>(a, mt, red, tid);
-      if (tid == 0) a.counters[mt] = 0;
-    }
-    named_bar(1, NC);
+__device__ __forceinline__ void gemv_flush(const GemvArgs& a, float (&acc)[4], float* red_base, int& par,
+                                           int* flag, int mt, int G, long T, int c, int tid, int g, int t4,
+                                           int rb, int kh) {
+  float* red = red_base + par * kQ * kTileRows;
+  par ^= 1;
+  if (t4 == 0) {
+    red[kh * kTileRows + rb * 16 + g] = acc[0] + acc[1];
+    red[kh * kTileRows + rb * 16 + g + 8] = acc[2] + acc[3];
   }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = 0.f;
+  named_bar(1, NC);
+  if (tid >= kTileRows) return;
+  float v = red[tid];
+#pragma unroll
+  for (int q = 1; q < kQ; ++q) v += red[q * kTileRows + tid];
+  const long first = static_cast<long>(mt) * a.n_kb, last = first + a.n_kb - 1;
+  const int c_first = gemv_cta_of_tile(first, G, T);
+  const int n_contrib = gemv_cta_of_tile(last, G, T) - c_first + 1;
+  if (n_contrib == 1) {
+    red[tid] = v;
+    named_bar(2, kTileRows);
+    gemv_epilogue<EPI>(a, mt, red, tid);
+    return;
+  }
+  float* mine = a.ws + (static_cast<long>(mt) * a.max_contrib + (c - c_first)) * kTileRows;
+  mine[tid] = v;
+  named_bar(2, kTileRows);
+  if (tid == 0) {
+    __threadfence();  // cumulative: orders the 128 rows' stores (via the barrier) before the count
+    const int old = atomicAdd(&a.counters[mt], 1);
+    *flag = (old == n_contrib - 1);
+  }
+  named_bar(2, kTileRows);
+  if (*flag) {
+    __threadfence();
+    const float* base = a.ws + static_cast<long>(mt) * a.max_contrib * kTileRows;
+    float s = 0.f;
+    for (int j = 0; j < n_contrib; ++j) s += __ldcg(base + j * kTileRows + tid);
+    red[tid] = s;
+    named_bar(2, kTileRows);
+    gemv_epilogue<EPI>(a, mt, red, tid);
+    if (tid == 0) a.counters[mt] = 0;
+  }
+}
 
 }  // namespace lsb

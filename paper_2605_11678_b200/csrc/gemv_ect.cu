@@ -32,14 +32,14 @@ constexpr int kMaxSlots = 4;
 constexpr int kSmemBudget = 227 * 1024;
 
 __host__ __device__ inline int ect_slots(int n_kb) {
-  const int avail = (kSmemBudget - n_kb * kTileCols * 4 - 2 * kTileRows * 4 - 64 - 2 * kMaxSlots * 8 - 16) /
+  const int avail = (kSmemBudget - n_kb * kTileCols * 4 - 4 * kTileRows * 4 - 64 - 2 * kMaxSlots * 8 - 16) /
                     kSlotBytes;
   return avail > kMaxSlots ? kMaxSlots : avail;
 }
 
 size_t ect_smem(int n_kb) {
   return static_cast<size_t>(ect_slots(n_kb)) * kSlotBytes + static_cast<size_t>(n_kb) * kTileCols * 4 +
-         2 * kTileRows * 4 + 64 + 2 * kMaxSlots * 8 + 16;
+         4 * kTileRows * 4 + 64 + 2 * kMaxSlots * 8 + 16;
 }
 }  // namespace
 
@@ -50,8 +50,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   const int NQ = ect_slots(a.n_kb);
   uint8_t* slots = smem;
   uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NQ * kSlotBytes);  // B words (gemv.cu layout)
-  float* red = reinterpret_cast<float*>(xq + K);                        // [2][128]
-  float* scratch = red + 2 * kTileRows;
+  float* red = reinterpret_cast<float*>(xq + K);                        // 2 x [2][128]
+  float* scratch = red + 4 * kTileRows;
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 16);
   uint64_t* empty = full + kMaxSlots;
   int* flag = reinterpret_cast<int*>(empty + kMaxSlots);
@@ -126,9 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
     uint4 w0 = ect_decode8(make_uint2(sm.x, sm.y), nib.x, e0p);
     uint4 w1 = ect_decode8(make_uint2(sm.z, sm.w), nib.y, e0p);
     if (esc) {  // this lane's 16 words hold an escape (rare, divergent)
-      const uint32_t e0 = ect_escapes(nib.x), e1 = ect_escapes(nib.y);
-      if (e0) w0 = ect_patch8(w0, e0, page, f0 * 8, exc_off, exc);
-      if (e1) w1 = ect_patch8(w1, e1, page, f0 * 8 + 8, exc_off, exc);
+      ect_patch16(w0, w1, ect_escapes(nib.x), ect_escapes(nib.y), page, f0 * 8, exc_off, exc);
     }
     af[0][0] = w0.x; af[0][1] = w0.y; af[0][2] = w0.z; af[0][3] = w0.w;
     af[1][0] = w1.x; af[1][1] = w1.y; af[1][2] = w1.z; af[1][3] = w1.w;
@@ -142,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   };
 
   int kb = static_cast<int>(t0 % a.n_kb), mt = static_cast<int>(t0 / a.n_kb), s = 0;
-  int rem = static_cast<int>(t1 - t0);
+  int rem = static_cast<int>(t1 - t0), par = 0;
   uint32_t t = static_cast<uint32_t>(t0), round = 0;
   const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
   while (rem > 0) {
@@ -182,12 +180,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
     rem -= np;
     kb += np;
     if (kb == a.n_kb) {
-      gemv_flush<EPI, kConsumers, 2>(a, acc, red, flag, mt, G, T, c, tid, g, t4, rb, kh);
+      gemv_flush<EPI, kConsumers, 2>(a, acc, red, par, flag, mt, G, T, c, tid, g, t4, rb, kh);
       kb = 0;
       ++mt;
     }
   }
-  if (kb != 0) gemv_flush<EPI, kConsumers, 2>(a, acc, red, flag, mt, G, T, c, tid, g, t4, rb, kh);
+  if (kb != 0) gemv_flush<EPI, kConsumers, 2>(a, acc, red, par, flag, mt, G, T, c, tid, g, t4, rb, kh);
 }
 
 template <int EPI>
