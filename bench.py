@@ -154,7 +154,8 @@ def gemv_microbench(torch, device, n, k, reps=30, ect_pages=False):
         e1.record(s)
     s.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    w_bytes = n * k * 2 * 3 // 4 if ect_pages else n * k * 2
+    # ECT: 12 KiB page + 64 B escape mask per 16 KiB tile (the bytes the kernel moves)
+    w_bytes = n * k * 2 * 3 // 4 + (n * k * 2 // 16384) * 64 if ect_pages else n * k * 2
     algo_bytes = w_bytes + k * 4 + k * 2 + (n // 2) * 4
     return {"bytes": algo_bytes, "ms": ms, "gbs": algo_bytes / (ms * 1e6),
             "plain_equiv_gbs": (n * k * 2) / (ms * 1e6)}
@@ -399,9 +400,9 @@ def main():
                         "note": "dfbsim total of the chosen placement on the measured profile"},
         "roofline": {"bound": "hbm", "achieved": gv["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": gv["gbs"] / peaks["hbm_gbs"],
-                     "traffic": ncu_traffic(f"gemv_kernel<SILU{', ECT' if ect_dec else ''}> gate|up "
+                     "traffic": ncu_traffic(f"{'gemv_ect_kernel' if ect_dec else 'gemv_kernel'}<SILU> gate|up "
                                             f"{2 * cfg.lm_ffn}x{cfg.lm_d}"),
-                     "kernel": f"gemv_kernel<SILU{', ECT pages' if ect_dec else ''}> gate|up "
+                     "kernel": f"{'gemv_ect_kernel<SILU> (ECT pages)' if ect_dec else 'gemv_kernel<SILU>'} gate|up "
                                f"{2 * cfg.lm_ffn}x{cfg.lm_d} bf16 ({gv['bytes']} algorithmic B/launch, "
                                f"{gv['ms'] * 1e3:.1f} us)",
                      "plain_equivalent_gbs": gv["plain_equiv_gbs"],

@@ -10,7 +10,7 @@ timeout 1200 python bench.py --dump $OUT > $OUT/bench.json 2> $OUT/bench.err; ec
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?"; cat $OUT/bench_ref.json
 PROF=$OUT/profile_alpamayo-r1-10b-shape.json
 if [ -f "$PROF" ] && [ -z "$SKIP_NCU" ]; then
-  KRE='regex:gemv_kernel|gemm_kernel|flash_kernel|decode_attn|rmsnorm|layernorm|qk_norm|embed_rows|add_rows|argmax_to|time_embed|action_|silu_kernel|fill_u64|ecf'
+  KRE='regex:gemv_kernel|gemv_ect_kernel|gemm_kernel|flash_kernel|decode_attn|rmsnorm|layernorm|qk_norm|embed_rows|add_rows|argmax_to|time_embed|action_|silu_kernel|fill_u64|ecf'
   N=$(python tools/profile_step.py --profile $PROF --runs 1 2>/dev/null | sed -n "s/.*kernel_launches.: \([0-9]*\).*/\1/p" | head -1)
   echo "launches per inference: $N"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -s $N -c $N --csv \
@@ -18,7 +18,7 @@ if [ -f "$PROF" ] && [ -z "$SKIP_NCU" ]; then
   python tools/ncu_summary.py $OUT/launches.csv > $OUT/launches_summary.txt 2>&1; head -30 $OUT/launches_summary.txt
   # the dominant decode kernel as launched in the step: gate|up GEMV over ECT pages
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-      -k 'regex:gemv_kernel<.int.2, .bool.1' -s 40 -c 1 -o $OUT/gemv_silu_ect python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_gemv.log 2>&1
+      -k 'regex:gemv_ect_kernel<.int.2' -s 40 -c 1 -o $OUT/gemv_silu_ect python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_gemv.log 2>&1
   ncu -i $OUT/gemv_silu_ect.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > $OUT/gemv_silu_ect_dram.csv 2>&1
   cat $OUT/gemv_silu_ect_dram.csv | tail -3
   python tools/ncu_kv.py $OUT/gemv_silu_ect.ncu-rep > $OUT/gemv_silu_ect_summary.txt 2>&1
