@@ -154,8 +154,8 @@ def gemv_microbench(torch, device, n, k, reps=30, ect_pages=False):
         e1.record(s)
     s.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    # ECT: 12 KiB page + 64 B escape mask per 16 KiB tile (the bytes the kernel moves)
-    w_bytes = n * k * 2 * 3 // 4 + (n * k * 2 // 16384) * 64 if ect_pages else n * k * 2
+    # ECT: 12 KiB page + 16 B escape mask per 16 KiB tile (the bytes the kernel moves)
+    w_bytes = n * k * 2 * 3 // 4 + (n * k * 2 // 16384) * 16 if ect_pages else n * k * 2
     algo_bytes = w_bytes + k * 4 + k * 2 + (n // 2) * 4
     return {"bytes": algo_bytes, "ms": ms, "gbs": algo_bytes / (ms * 1e6),
             "plain_equiv_gbs": (n * k * 2) / (ms * 1e6)}

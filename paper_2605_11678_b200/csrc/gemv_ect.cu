@@ -2,7 +2,7 @@
 // residency / streaming form, ect.py): 12 KiB pages are decoded in registers
 // and fed to mma.sync, never expanded in memory.
 //
-// Roofline: HBM.  Moved bytes per launch = n_pages * (12288 + 64) (pages +
+// Roofline: HBM.  Moved bytes per launch = n_pages * (12288 + 16) (pages +
 // escape masks) + K*4 + N*4; the plain-equivalent figure divides N*K*2 by
 // the same time.  The kernel is bound by the consumers' integer issue rate
 // (~2.4 ALU/FMA ops per decoded word), so everything around the decode is
@@ -10,9 +10,9 @@
 //   * chunks of up to 4 pages (never straddling an m-tile) are one ring slot:
 //     one bulk copy of the pages (contiguous in the blob) + one of their
 //     escape masks, one mbarrier wait and one arrive per warp per chunk;
-//   * the per-page escape mask (64 B: one bit per lane and warp region) says
-//     which lanes hold a code-15 word, so the per-code escape test and the
-//     patch run only for those lanes (~0.2 % of lane-pages for BF16 weights);
+//   * the per-page escape mask (16 B: one bit per 64 words = 4 lanes of a warp)
+//     says where code-15 words are, so the per-code escape test and the patch
+//     run only for those lanes (~1 % of lane groups for BF16 weights);
 //   * same stream-K split, fix-up and fused epilogues as gemv.cu (shared
 //     gemv_common.cuh), so plain and ECT launches give bit-identical results.
 #include "common.cuh"
@@ -26,7 +26,7 @@ constexpr int kWarps = 16;                 // 8 row blocks x 2 k-parts of every 
 constexpr int kConsumers = kWarps * 32;
 constexpr int kThreads = kConsumers + 32;  // + producer warp
 constexpr int kChunk = 4;                  // pages per ring slot
-constexpr int kMaskBytes = 64;             // escape mask per page
+constexpr int kMaskBytes = 16;             // escape mask per page (1 bit per 64 words)
 constexpr int kSlotBytes = kChunk * (kEctPageBytes + kMaskBytes);
 constexpr int kMaxSlots = 4;
 constexpr int kSmemBudget = 227 * 1024;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
 
   const int g = lane >> 2, t4 = lane & 3;
   const int rb = warp & 7, kh = warp >> 3;  // row block, k-part (k-steps 2 kh, 2 kh + 1)
-  const int wreg = rb * 2 + kh;             // escape-mask word of this warp
+  const int wreg = rb * 2 + kh;             // warp region: page words [512 wreg, +512)
   const int f0 = (wreg * 32 + lane) * 2;    // this lane's two fragments in a page
   // B words: column g = 0 -> hi, 1 -> lo; columns g >= 2 repeat them and only
   // reach C columns >= 2, which lanes t4 != 0 hold and the flush ignores
@@ -134,9 +134,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   // without a mask section every lane takes the escape test (the slot's mask
   // area then holds stale bytes, overridden by no_mask)
   const uint32_t no_mask = has_mask ? 0u : 0xffffffffu;
+  const int esh = 8 * (wreg & 3) + (lane >> 2);  // mask bit of this lane's 64-word group
   auto lane_esc = [&](const uint8_t* st, int q) -> bool {
-    const uint32_t m = *reinterpret_cast<const uint32_t*>(st + kChunk * kEctPageBytes + q * kMaskBytes + wreg * 4);
-    return ((m | no_mask) >> lane) & 1u;
+    const uint32_t m = *reinterpret_cast<const uint32_t*>(st + kChunk * kEctPageBytes + q * kMaskBytes + (wreg >> 2) * 4);
+    return ((m | no_mask) >> esh) & 1u;
   };
 
   int kb = static_cast<int>(t0 % a.n_kb), mt = static_cast<int>(t0 / a.n_kb), s = 0;

@@ -22,10 +22,9 @@ Blob (all offsets 16-byte aligned, csrc/kernels.h EctHeader):
                    its 8192 words in mma.sync A-fragment order (page_order())
     tail           the layer's vectors (norm weights, biases), raw
     exc_off        (n_pages + 1) x u32, prefix offsets of each page's escapes
-    escmask        n_pages x 16 x u32: word r bit l <=> page words
-                   [16 (32 r + l), +16) hold an escape (code 15), so a decoder
-                   skips the per-code escape test for the (~99.8 % of) 16-word
-                   groups without one
+    escmask        n_pages x 16 B: bit b <=> page words [64 b, 64 b + 64) hold
+                   an escape (code 15), so a decoder skips the per-code escape
+                   test for the (~99 % of) 64-word groups without one
     exc            n_exc x u32 = (word index in page << 8) | exponent
 The code window is contiguous: code c < 15 means exponent e0 + c, where
 [e0, e0 + 14] is the 15-exponent window holding the most words, so decoding
@@ -114,7 +113,7 @@ def compress(buf: torch.Tensor, mat_bytes: int) -> torch.Tensor:
     off_tail = _a16(off_pages + n_pages * PAGE_BYTES)
     off_excoff = _a16(off_tail + tail)
     off_escmask = _a16(off_excoff + 4 * (n_pages + 1))
-    off_exc = _a16(off_escmask + 64 * n_pages)
+    off_exc = _a16(off_escmask + 16 * n_pages)
     size = _a16(off_exc + 4 * n_exc)
     cb = [e0 + c for c in range(15)] + [0]
     head = struct.pack(_HDR_FMT, MAGIC, n_pages, total, mat_bytes, off_pages, off_tail, off_excoff,
@@ -126,18 +125,19 @@ def compress(buf: torch.Tensor, mat_bytes: int) -> torch.Tensor:
     if tail:
         blob[off_tail:off_tail + tail] = buf[mat_bytes:]
     blob[off_excoff:off_excoff + 4 * (n_pages + 1)] = exc_off.to(torch.int32).view(torch.uint8)
-    blob[off_escmask:off_escmask + 64 * n_pages] = escape_mask(code.view(n_pages, PAGE_WORDS)).view(-1).view(torch.uint8)
+    blob[off_escmask:off_escmask + 16 * n_pages] = escape_mask(code.view(n_pages, PAGE_WORDS)).view(-1).view(torch.uint8)
     if n_exc:
         blob[off_exc:off_exc + 4 * n_exc] = exc.view(torch.uint8)
     return blob
 
 
 def escape_mask(code: torch.Tensor) -> torch.Tensor:
-    """[n_pages, 8192] codes (page order) -> int32 [n_pages, 16]: word r of a
-    page, bit l set when page words [16 (32 r + l), +16) -- the two fragments
-    decode-GEMV lane l of warp region r owns -- hold an escape (code 15)."""
+    """[n_pages, 8192] codes (page order) -> int32 [n_pages, 4] (128 bits per
+    page): bit b set when page words [64 b, 64 b + 64) -- the 16-word groups
+    of decode-GEMV lanes 4 (b % 8) .. +3 of warp region b // 8 -- hold an
+    escape (code 15)."""
     n = code.shape[0]
-    esc = (code == 15).view(n, 16, 32, 16).any(dim=3).to(torch.int64)
+    esc = (code == 15).view(n, 4, 32, 64).any(dim=3).to(torch.int64)
     bits = (esc << torch.arange(32, device=code.device)).sum(dim=2)
     return (bits - ((bits >> 31) & 1) * (1 << 32)).to(torch.int32)
 

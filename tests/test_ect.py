@@ -29,27 +29,25 @@ def test_cpu_roundtrip_ratio_and_escapes():
 
 
 def test_escape_region_mask_matches_codes():
-    """escmask word r bit l of page p <=> a code-15 nibble among page words
-    [16 (32 r + l), +16) -- the 16 words decode-GEMV lane l of warp region r
-    decodes -- so the GEMV tests codes only where the mask says so."""
+    """escmask bit b of page p <=> a code-15 nibble among page words
+    [64 b, 64 b + 64) (decode-GEMV lanes 4 (b % 8) .. +3 of warp region b // 8),
+    so the GEMV tests codes only where the mask says so."""
     buf, mat = _layer(6, 0, seed=3)
     blob = ect.compress(buf, mat)
     h = ect.header(blob)
     n = h["n_pages"]
-    assert h["off_escmask"] % 16 == 0 and h["off_exc"] >= h["off_escmask"] + 64 * n
+    assert h["off_escmask"] % 16 == 0 and h["off_exc"] >= h["off_escmask"] + 16 * n
     pages = blob[h["off_pages"]:h["off_pages"] + n * ect.PAGE_BYTES].view(n, ect.PAGE_BYTES)
     nib = pages[:, ect.PAGE_WORDS:].to(torch.int64)
     code = torch.stack([nib & 0xF, nib >> 4], 2).reshape(n, ect.PAGE_WORDS)
-    mask = blob[h["off_escmask"]:h["off_escmask"] + 64 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    mask = mask.view(n, 16)
+    mask = blob[h["off_escmask"]:h["off_escmask"] + 16 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    mask = mask.view(n, 4)
     for p in range(n):
-        for r in range(16):
-            for lane in range(32):
-                w0 = 16 * (32 * r + lane)
-                want = bool((code[p, w0:w0 + 16] == 15).any())
-                assert bool((mask[p, r] >> lane) & 1) == want, (p, r, lane)
+        for b in range(128):
+            want = bool((code[p, 64 * b:64 * (b + 1)] == 15).any())
+            assert bool((mask[p, b // 32] >> (b % 32)) & 1) == want, (p, b)
     assert int(mask[0, 0]) & 1  # the zero padding rows escape (exponent 0)
-    assert int(mask.sum()) < n * 16 * 0xFFFFFFFF  # most groups are escape-free
+    assert int(mask.sum()) < n * 4 * 0xFFFFFFFF  # most groups are escape-free
 
 
 def test_cpu_roundtrip_no_tail_and_single_page():
