@@ -1253,6 +1253,9 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
           if (ecf_src) {
             KL(launch_ecf_decode(ecf_src, const_cast<char*>(w), e->nsm, e->ss));
             ++e->launches;  // decode + exception patch
+            // the layer's kernels request weights before their pdl_wait: they must
+            // not start before the decoded layer is complete
+            e->pdl_ok = false;
           }
           CtView ct;
           if (m.ct && e->ct_fused) {

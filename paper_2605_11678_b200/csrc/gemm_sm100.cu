@@ -38,7 +38,7 @@ struct GemmCfg {
   static constexpr int kDecWarps = CT ? 16 : 0;
   static constexpr int kThreads = 192 + 32 * kDecWarps;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * (kStageBytes + kPBytes) +
-                                  128 * 17 * 4 + (3 * kStages + 4) * 8 + 16;
+                                  128 * 17 * 4 + (4 * kStages + 4) * 8 + 16;
 };
 
 // Persistent: grid = min(#tiles, #SMs); CTA c takes tiles c, c+grid, ...  Tiles
@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_f + 128 * 17);
   uint64_t* empty = full + Cfg::kStages;
   uint64_t* dec = empty + Cfg::kStages;          // CT: A tile decoded (kDecWarps arrivals)
-  uint64_t* acc_full = dec + Cfg::kStages;     // [2]
+  uint64_t* bfull = dec + Cfg::kStages;          // B (activation) tile landed
+  uint64_t* acc_full = bfull + Cfg::kStages;   // [2]
   uint64_t* acc_empty = acc_full + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
       mbar_init(&dec[s], Cfg::kDecWarps > 0 ? Cfg::kDecWarps : 1);
+      mbar_init(&bfull[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -91,21 +93,38 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
+      constexpr int kWBytes = CT ? kEctPageBytes : kTileBytes;
+      // weights (A / ECT page, full[s]) and activations (B, bfull[s]) complete
+      // on separate barriers: the first kStages weight tiles do not depend on
+      // the previous kernel and are requested before pdl_wait, so they stream
+      // (and, CT, get decoded) while the previous launch drains
+      auto a_load = [&](int s, int mt, int kb) {
+        mbar_arrive_expect_tx(&full[s], kWBytes);
+        bulk_g2s(CT ? spg + s * Cfg::kPBytes : sa + s * Cfg::kABytes,
+                 a.w + (static_cast<long>(mt) * n_kb + kb) * kWBytes, kWBytes, &full[s]);
+      };
+      int pre = 0;
+#ifndef LS_GEMM_NOPRE  // diagnostic build: every weight tile after pdl_wait
+      for (int t = blockIdx.x; t < n_tiles && pre < Cfg::kStages; t += gridDim.x) {
+        const int tile = t / ks, sp = t % ks, mt = tile / n_nt;
+        const int kb1 = (sp + 1) * n_kb / ks;
+        for (int kb = sp * n_kb / ks; kb < kb1 && pre < Cfg::kStages; ++kb) a_load(pre++, mt, kb);
+      }
+#endif
       pdl_wait();  // activations of the previous kernel
-      int s = 0;
+      int s = 0, i = 0;
       uint32_t round = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int tile = t / ks, sp = t % ks;
         const int mt = tile / n_nt, n0 = (tile % n_nt) * BN;
-        constexpr int kWBytes = CT ? kEctPageBytes : kTileBytes;
-        const uint8_t* wt = a.w + static_cast<long>(mt) * n_kb * kWBytes;
         const int kb1 = (sp + 1) * n_kb / ks;
-        for (int kb = sp * n_kb / ks; kb < kb1; ++kb) {
-          if (round) mbar_wait(&empty[s], (round - 1) & 1);
-          mbar_arrive_expect_tx(&full[s], kWBytes + Cfg::kBBytes);
-          bulk_g2s(CT ? spg + s * Cfg::kPBytes : sa + s * Cfg::kABytes,
-                   wt + static_cast<long>(kb) * kWBytes, kWBytes, &full[s]);
-          tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &full[s]);
+        for (int kb = sp * n_kb / ks; kb < kb1; ++kb, ++i) {
+          if (i >= pre) {
+            if (round) mbar_wait(&empty[s], (round - 1) & 1);
+            a_load(s, mt, kb);
+          }
+          mbar_arrive_expect_tx(&bfull[s], Cfg::kBBytes);
+          tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &bfull[s]);
           if (++s == Cfg::kStages) {
             s = 0;
             ++round;
@@ -127,8 +146,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
         const uint32_t acc = tmem + b * Cfg::kAccCols;
         const int sp = t % ks, kb0 = sp * n_kb / ks, kb1 = (sp + 1) * n_kb / ks;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[s], round & 1);
-          if constexpr (CT) mbar_wait(&dec[s], round & 1);
+          if constexpr (CT) mbar_wait(&dec[s], round & 1);  // decoders waited for the page
+          else mbar_wait(&full[s], round & 1);
+          mbar_wait(&bfull[s], round & 1);
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
           const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
@@ -170,7 +190,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
         uint32_t* ta = reinterpret_cast<uint32_t*>(sa + s * Cfg::kABytes);
         const uint32_t page = static_cast<uint32_t>(mt * n_kb + kb);
 #pragma unroll
-        for (int it = 0; it < 1024 / (32 * Cfg::kDecWarps); ++it) {
+        for (int it = 0; it < (Cfg::kDecWarps ? 1024 / (32 * Cfg::kDecWarps) : 0); ++it) {
           const uint32_t f = it * 32 * Cfg::kDecWarps + dt;  // fragment
           const uint2 sm = *reinterpret_cast<const uint2*>(pg + f * 8);
           const uint32_t nib = *reinterpret_cast<const uint32_t*>(pg + kEctPageWords + f * 4);

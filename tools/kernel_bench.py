@@ -81,7 +81,7 @@ def bench_gemv_ect(n, k, epi=K.GEMV_F32, copies=4):
                ct_blob=b)
     ms = timed(run)
     plain = n * k * 2
-    moved = plain * 3 // 4 + k * 6 + n * 4
+    moved = plain * 3 // 4 + plain // 16384 * 16 + k * 6 + n * 4
     return {"kernel": f"gemv_ect epi={epi} {n}x{k}", "us": ms * 1e3, "GBps_moved": moved / (ms * 1e6),
             "plain_equiv_GBps": plain / (ms * 1e6)}
 
@@ -181,6 +181,10 @@ def main():
         res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
         res.append(bench_gemv_ect(6144, 4096, K.GEMV_F32))
         res.append(bench_ect_decode())
+    if args.only == "overhead":  # fixed per-launch cost: tiny and mid shapes, ECT and plain
+        for n, k in ((18944, 64), (18944, 256), (18944, 1024), (6144, 4096), (24576, 4096)):
+            res.append(bench_gemv_ect(n, k, K.GEMV_F32))
+            res.append(bench_gemv(n, k, K.GEMV_F32))
     if args.only in ("all", "attn"):
         for s in (16, 9):
             res.append(bench_decode_attn(n_split=s))
