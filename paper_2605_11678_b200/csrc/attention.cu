@@ -306,31 +306,57 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   }
 
   // K/V block loader: cp.async 16-byte chunks (zero-filled past the end), one
-  // commit group per block, so block j+1 streams in while block j is computed
+  // commit group per block, so block j+1 streams in while block j is computed.
+  // A thread always copies chunk column c of rows r0, r0 + 128 / (DK / 8), ...:
+  // its per-segment base pointers are fixed, a row costs one multiply-add.
+  constexpr int CPR = DK / 8;          // 16-byte chunks per (padded) row
+  constexpr int RSTEP = 128 / CPR;     // rows between a thread's chunks
+  const int lc = threadIdx.x % CPR, lr0 = threadIdx.x / CPR;
+  const bool col_ok = lc < CH;
+  const long hoff1 = static_cast<long>(kvh) * a.k1_head_stride + lc * 8;
+  const long hoff2 = static_cast<long>(kvh) * a.k2_head_stride + lc * 8;
+  auto load_row = [&](bf16* kd, bf16* vd, int j, bool ok) {
+    const bf16 *kp = a.k1, *vp = a.v1;
+    if (ok) {
+      const long off = j < a.len1 ? hoff1 + static_cast<long>(j) * a.k1_tok_stride
+                                  : hoff2 + static_cast<long>(j - a.len1) * a.k2_tok_stride;
+      kp = (j < a.len1 ? a.k1 : a.k2) + off;
+      vp = (j < a.len1 ? a.v1 : a.v2) + off;
+    }
+    cp_async16(kd, kp, ok);
+    cp_async16(vd, vp, ok);
+  };
   auto load_kv = [&](int buf, int j0) {
-    bf16* kd = ks_buf + buf * BN * LD;
-    bf16* vd = vs_buf + buf * BN * LD;
-    for (int i = threadIdx.x; i < BN * (DK / 8); i += 128) {
-      const int r = i / (DK / 8), c = i % (DK / 8);
-      const int j = j0 + r;
-      const bool ok = j < k_end && c < CH;
-      const bf16 *kp = a.k1, *vp = a.v1;
-      if (ok) {
-        if (j < a.len1) {
-          const long off = static_cast<long>(j) * a.k1_tok_stride + static_cast<long>(kvh) * a.k1_head_stride + c * 8;
-          kp = a.k1 + off;
-          vp = a.v1 + off;
-        } else {
-          const long off = static_cast<long>(j - a.len1) * a.k2_tok_stride + static_cast<long>(kvh) * a.k2_head_stride + c * 8;
-          kp = a.k2 + off;
-          vp = a.v2 + off;
+    bf16* kb = ks_buf + buf * BN * LD;
+    bf16* vb = vs_buf + buf * BN * LD;
+    if constexpr (128 % CPR == 0) {
+#pragma unroll
+      for (int r = lr0; r < BN; r += RSTEP)
+        load_row(kb + r * LD + lc * 8, vb + r * LD + lc * 8, j0 + r, col_ok && j0 + r < k_end);
+    } else {  // chunk count per row does not divide the CTA (head dim 72)
+      for (int i = threadIdx.x; i < BN * CPR; i += 128) {
+        const int r = i / CPR, c = i % CPR, j = j0 + r;
+        const long hc = (c - lc) * 8;  // load_row's bases are for column lc
+        bf16* kd = kb + r * LD + c * 8;
+        bf16* vd = vb + r * LD + c * 8;
+        const bool ok = c < CH && j < k_end;
+        const bf16 *kp = a.k1, *vp = a.v1;
+        if (ok) {
+          const long off = (j < a.len1 ? hoff1 + static_cast<long>(j) * a.k1_tok_stride
+                                       : hoff2 + static_cast<long>(j - a.len1) * a.k2_tok_stride) + hc;
+          kp = (j < a.len1 ? a.k1 : a.k2) + off;
+          vp = (j < a.len1 ? a.v1 : a.v2) + off;
         }
+        cp_async16(kd, kp, ok);
+        cp_async16(vd, vp, ok);
       }
-      cp_async16(kd + r * LD + c * 8, kp, ok);
-      cp_async16(vd + r * LD + c * 8, vp, ok);
     }
     cp_async_commit();
   };
+  // ldmatrix source row / column of this lane for K^T fragments: matrices
+  // 0..3 = dims +0, +8, +16, +24 of a k-step pair, rows = the 8 keys of n-tile
+  const int kl_row = lane & 7, kl_col = (lane >> 3) * 8;
+  const int q_lo = q0 + a.q_offset;  // smallest query position of the tile (causal)
   if (k_begin < k_end) load_kv(0, k_begin);
   int buf = 0;
   for (int j0 = k_begin; j0 < k_end; j0 += BN, buf ^= 1) {
@@ -343,38 +369,50 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
     __syncthreads();
     const bf16* ks = ks_buf + buf * BN * LD;
     const bf16* vs = vs_buf + buf * BN * LD;
-    // S = Q K^T  (16 x 64 per warp)
+    // S = Q K^T  (16 x 64 per warp); K^T fragments by ldmatrix (two k-steps per x4)
     float s[BN / 8][4];
 #pragma unroll
     for (int nt = 0; nt < BN / 8; ++nt) {
       s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-      const bf16* kr = ks + (nt * 8 + g) * LD;
+      const bf16* kr = ks + (nt * 8 + kl_row) * LD + kl_col;
 #pragma unroll
-      for (int kk = 0; kk < DK / 16; ++kk) {
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 2 * t4);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8 + 2 * t4);
+      for (int kk = 0; kk + 1 < DK / 16; kk += 2) {
+        uint32_t b[4];
+        ldsm_x4(b, kr + kk * 16);
+        mma_bf16_16816(s[nt], qf[kk], b[0], b[1]);
+        mma_bf16_16816(s[nt], qf[kk + 1], b[2], b[3]);
+      }
+      if constexpr ((DK / 16) & 1) {  // odd k-step count (head dim 72 -> 80)
+        constexpr int kk = DK / 16 - 1;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(ks + (nt * 8 + g) * LD + kk * 16 + 2 * t4);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(ks + (nt * 8 + g) * LD + kk * 16 + 8 + 2 * t4);
         mma_bf16_16816(s[nt], qf[kk], b0, b1);
       }
     }
-    // mask + online softmax (rows g and g+8 of this warp)
+    // masks only where a block can hold masked keys: the range end, causal diagonal
+    const bool edge = j0 + BN > k_end || (a.causal && j0 + BN - 1 > q_lo);
+    if (edge) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int nt = 0; nt < BN / 8; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = j0 + nt * 8 + 2 * t4 + e;
+            bool ok = j < k_end;
+            if (a.causal) ok = ok && (j <= qi[r] + a.q_offset);
+            if (!ok) s[nt][2 * r + e] = -INFINITY;
+          }
+    }
+    // online softmax (rows g and g+8 of this warp), log2 domain: p = 2^(s sl2 - m)
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       float mx = -INFINITY;
 #pragma unroll
-      for (int nt = 0; nt < BN / 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = j0 + nt * 8 + 2 * t4 + e;
-          float v = s[nt][2 * r + e] * sl2;
-          bool ok = j < k_end && qi[r] < a.Tq;
-          if (a.causal) ok = ok && (j <= qi[r] + a.q_offset);
-          v = ok ? v : -INFINITY;
-          s[nt][2 * r + e] = v;
-          mx = fmaxf(mx, v);
-        }
+      for (int nt = 0; nt < BN / 8; ++nt) mx = fmaxf(mx, fmaxf(s[nt][2 * r], s[nt][2 * r + 1]));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float mnew = fmaxf(mrow[r], mx);
+      const float mnew = fmaxf(mrow[r], mx * sl2);
       const float base = mnew == -INFINITY ? 0.f : mnew;
       const float corr = exp2f(mrow[r] - base);
       float rs = 0.f;
@@ -382,7 +420,7 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
       for (int nt = 0; nt < BN / 8; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const float p = exp2f(s[nt][2 * r + e] - base);
+          const float p = exp2f(fmaf(s[nt][2 * r + e], sl2, -base));
           s[nt][2 * r + e] = p;
           rs += p;
         }

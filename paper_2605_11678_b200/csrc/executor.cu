@@ -277,6 +277,9 @@ struct ls_exec {
   uint64_t gen = 0;  // bumped whenever resident pointers or the layout change
   cudaGraphExec_t gexec = nullptr;
   uint64_t gkey[12] = {};
+  // diagnostics only (tools/layer_breakdown.py): kernels of the expert layer
+  // to leave out -- results are wrong, the timing difference is the cost
+  uint32_t diag_skip = 0;
   std::vector<RunRec> grecs;  // invocation-span records of the captured run
   cudaEvent_t join_ev = nullptr, fork_ev = nullptr;
   uint64_t h2d_bytes = 0;
@@ -558,9 +561,10 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   bf16* ek = e->ex_kv;
   bf16* ev = e->ex_kv + static_cast<long>(d.ex_hkv) * T * d.ex_hd;
   const long shift = static_cast<long>(e->ctx) * d.ex_hd;  // store index t, RoPE position ctx + t
-  KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(4), e->ex_norm, T, D, d.lm_eps, e->ss));
-  RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0)));
-  KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
+  const uint32_t skip = e->diag_skip;
+  if (!(skip & 1)) KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(4), e->ex_norm, T, D, d.lm_eps, e->ss));
+  if (!(skip & 8)) RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0)));
+  if (!(skip & 2)) KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
                          (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], e->ctx, e->ex_q,
                          ek - shift, ev - shift, T * d.ex_hd, e->ss));
   FlashArgs f = flash_base(T, d.ex_hq, d.ex_hkv, d.ex_hd);
@@ -583,12 +587,13 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   f.kv_splits = e->ex_kv_splits;
   f.ws = e->flash_ws;
   f.counters = e->flash_cnt;
-  KL(launch_flash_attention(f, e->ss));
-  RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h, nullptr, cb, pg(1)));
-  KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
-  RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.ex_ffn, D, T, e->m_ex_norm, e->ex_mlp, d.ex_ffn,
-          nullptr, d.ex_ffn, cb, pg(2)));
-  RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, nullptr, cb, pg(3)));
+  if (!(skip & 4)) KL(launch_flash_attention(f, e->ss));
+  if (!(skip & 16)) RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h, nullptr, cb, pg(1)));
+  if (!(skip & 1)) KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
+  if (!(skip & 32))
+    RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.ex_ffn, D, T, e->m_ex_norm, e->ex_mlp, d.ex_ffn,
+            nullptr, d.ex_ffn, cb, pg(2)));
+  if (!(skip & 64)) RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, nullptr, cb, pg(3)));
   return LS_OK;
 }
 
@@ -1110,6 +1115,12 @@ int ls_exec_stats(ls_exec* e, int64_t out[3]) {
   out[0] = e->launches;    // kernels launched by the last run
   out[1] = e->h2d_copies;  // streamed-layer transfers of the last run
   out[2] = static_cast<int64_t>(e->h2d_bytes);
+  return LS_OK;
+}
+
+int ls_exec_set_diag_skip(ls_exec* e, uint32_t mask) {
+  e->diag_skip = mask;
+  ++e->gen;  // re-capture
   return LS_OK;
 }
 

@@ -60,6 +60,7 @@ def _bind():
         "ls_exec_streams": [vp, C.POINTER(vp), C.POINTER(vp)],
         "ls_exec_stats": [vp, C.POINTER(C.c_int64)],
         "ls_exec_enqueue_us": [vp, C.POINTER(C.c_double)],
+        "ls_exec_set_diag_skip": [vp, C.c_uint32],
         "ls_exec_run": [vp, C.POINTER(RunIO), C.POINTER(RunOpts), C.POINTER(_native.Event),
                         C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                         C.POINTER(C.c_double)],

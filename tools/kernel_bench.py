@@ -151,6 +151,30 @@ def bench_decode_attn(ctx=1045, hq=32, hkv=8, hd=128, n_split=18):
     return {"kernel": f"decode_attn ctx={ctx} split={n_split}", "us": ms * 1e3, "GBps": b / (ms * 1e6)}
 
 
+def bench_flash_expert(kv_splits, ctx=1045, T=64, hq=32, hkv=8, hd=128, max_ctx=1280):
+    """Action-expert attention: 64 queries x (VLM cache prefix + own 64 keys)."""
+    dev = "cuda"
+    q = torch.randn(T, hq, hd, device=dev).to(torch.bfloat16)
+    kc = torch.randn(hkv, max_ctx, hd, device=dev).to(torch.bfloat16)
+    vc = torch.randn(hkv, max_ctx, hd, device=dev).to(torch.bfloat16)
+    k2 = torch.randn(hkv, T, hd, device=dev).to(torch.bfloat16)
+    v2 = torch.randn(hkv, T, hd, device=dev).to(torch.bfloat16)
+    out = torch.empty(T, hq, hd, device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(1 << 22, device=dev)
+    cnt = torch.zeros(4096, dtype=torch.int32, device=dev)
+    a = K.FlashArgs(q=q.data_ptr(), q_tok_stride=q.stride(0), q_head_stride=q.stride(1),
+                    k1=kc.data_ptr(), v1=vc.data_ptr(), k1_tok_stride=hd, k1_head_stride=max_ctx * hd,
+                    len1=ctx, k2=k2.data_ptr(), v2=v2.data_ptr(), k2_tok_stride=hd,
+                    k2_head_stride=T * hd, len2=T, out=out.data_ptr(), o_tok_stride=out.stride(0),
+                    o_head_stride=out.stride(1), Tq=T, hq=hq, hkv=hkv, hd=hd, causal=0, q_offset=0,
+                    seg_len=0, scale=1 / math.sqrt(hd), kv_splits=kv_splits, ws=ws.data_ptr(),
+                    counters=cnt.data_ptr())
+    ms = timed(lambda: K.flash_attention(a))
+    flops = 4.0 * T * hq * (ctx + T) * hd
+    return {"kernel": f"flash expert T={T} keys={ctx + T} kv_splits={kv_splits}", "us": ms * 1e3,
+            "TFLOPs": flops / (ms * 1e9)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="all")
@@ -181,6 +205,9 @@ def main():
         res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
         res.append(bench_gemv_ect(6144, 4096, K.GEMV_F32))
         res.append(bench_ect_decode())
+    if args.only == "flash":
+        for sp in (1, 2, 4, 8):
+            res.append(bench_flash_expert(sp))
     if args.only == "overhead":  # fixed per-launch cost: tiny and mid shapes, ECT and plain
         for n, k in ((18944, 64), (18944, 256), (18944, 1024), (6144, 4096), (24576, 4096)):
             res.append(bench_gemv_ect(n, k, K.GEMV_F32))

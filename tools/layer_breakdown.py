@@ -1,0 +1,58 @@
+"""In-context cost of each expert-layer kernel (subtractive): run the planned
+Alpamayo-shaped inference with one kernel kind left out of every expert layer
+(ls_exec_set_diag_skip; results are wrong, only the timing is used) and report
+the latency difference per expert layer invocation.
+
+    python tools/layer_breakdown.py [--profile profiles/r1_profile_alpamayo_ect.json] [--runs 3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+MASKS = {"rmsnorm x2": 1, "qk_norm_rope": 2, "attention": 4, "qkv gemm": 8, "o gemm": 16,
+         "gate|up gemm": 32, "down gemm": 64, "all": 127}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--profile", default="profiles/r1_profile_alpamayo_ect.json")
+    ap.add_argument("--runs", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import paper_2605_11678_b200 as ls
+    from paper_2605_11678_b200 import model as M
+    from paper_2605_11678_b200.engine import DemandLayeringEngine
+    cfg = M.PRESETS["alpamayo-r1-10b-shape"]
+    prof = ls.load_profile(args.profile)
+    plan = ls.plan_for_budget(prof, prof.hardware.vram_mb)
+    eng = DemandLayeringEngine(cfg, vram_cap_mb=prof.hardware.vram_mb)
+    inputs = M.synthetic_inputs(cfg, 0)
+    n_inv = cfg.layers_of(M.KIND_EXPERT) * cfg.euler_steps
+
+    def run(mask):
+        eng.lib.ls_exec_set_diag_skip(eng.handle, mask)
+        eng.execute(plan.placement, inputs=inputs, record_timeline=False)
+        return statistics.fmean(eng.execute(plan.placement, inputs=inputs, record_timeline=False).total_ms
+                                for _ in range(args.runs))
+
+    base = run(0)
+    res = {"base_ms": base, "expert_layer_invocations": n_inv, "per_layer_us": {}}
+    for name, m in MASKS.items():
+        ms = run(m)
+        res["per_layer_us"][name] = (base - ms) * 1e3 / n_inv
+        print(f"{name:14s} {ms:8.2f} ms  -> {res['per_layer_us'][name]:7.2f} us per expert layer", flush=True)
+    run(0)
+    eng.close()
+    print(json.dumps(res))
+    if args.out:
+        Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
