@@ -21,15 +21,49 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 }
 
 // RMSNorm over rows of an fp32 [T x D] residual stream -> bf16 GEMM operand.
+// Rows with D % 1024 == 0 and D <= 4096 (every hidden size here): a thread
+// holds its float4 groups in registers -- x is read once, in one round trip,
+// and the norm weights are fetched before pdl_wait.
+constexpr int kNormMaxV = 4;  // float4 per thread (256 threads -> D <= 4096)
+
 __global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, int D, float eps) {
   pdl_trigger();
-  pdl_wait();
   __shared__ float sh[32];
   const float* xr = x + static_cast<long>(blockIdx.x) * D;
+  bf16* o = out + static_cast<long>(blockIdx.x) * D;
+  if (D % 1024 == 0 && D <= 1024 * kNormMaxV) {
+    const int nv = D / 1024;
+    uint2 wv[kNormMaxV];
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v < nv) wv[v] = reinterpret_cast<const uint2*>(w)[v * 256 + threadIdx.x];
+    pdl_wait();
+    float4 xv[kNormMaxV];
+    float ss = 0.f;
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v < nv) {
+        xv[v] = reinterpret_cast<const float4*>(xr)[v * 256 + threadIdx.x];
+        ss = fmaf(xv[v].x, xv[v].x, ss);
+        ss = fmaf(xv[v].y, xv[v].y, ss);
+        ss = fmaf(xv[v].z, xv[v].z, ss);
+        ss = fmaf(xv[v].w, xv[v].w, ss);
+      }
+    const float rstd = rsqrtf(block_sum(ss, sh) / D + eps);
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v < nv) {
+        uint2 r;
+        r.x = pack_bf16x2(xv[v].x * rstd * bf16_lo(wv[v].x), xv[v].y * rstd * bf16_hi(wv[v].x));
+        r.y = pack_bf16x2(xv[v].z * rstd * bf16_lo(wv[v].y), xv[v].w * rstd * bf16_hi(wv[v].y));
+        reinterpret_cast<uint2*>(o)[v * 256 + threadIdx.x] = r;
+      }
+    return;
+  }
+  pdl_wait();
   float ss = 0.f;
   for (int i = threadIdx.x; i < D; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
   const float rstd = rsqrtf(block_sum(ss, sh) / D + eps);
-  bf16* o = out + static_cast<long>(blockIdx.x) * D;
   for (int i = threadIdx.x; i < D; i += blockDim.x) o[i] = f2bf(xr[i] * rstd * bf2f(w[i]));
 }
 
@@ -112,11 +146,77 @@ __global__ void qk_norm_rope_kernel(const bf16* qkv, int hq, int hkv, int hd, co
   }
 }
 
+// Head dim 128: lane l holds dims 2l, 2l+1 and 64+2l, 64+2l+1 -- the RoPE pairs
+// (d, d + 64) never leave the lane -- and a warp issues every load of its heads
+// (x, norm weights, cos/sin; the tables before pdl_wait) before computing.
+constexpr int kQkMaxHeadsPerWarp = 8;
+
+__global__ void qk_norm_rope128_kernel(const bf16* qkv, int hq, int hkv, const bf16* qn_w,
+                                       const bf16* kn_w, float eps, const float2* rope, int pos0,
+                                       bf16* q_out, bf16* k_cache, bf16* v_cache, int cache_head_stride) {
+  constexpr int hd = 128;
+  pdl_trigger();
+  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int nh = hq + 2 * hkv;
+  const int pos = pos0 + t;
+  const float4 cs = reinterpret_cast<const float4*>(rope + static_cast<long>(pos) * (hd / 2))[lane];
+  uint32_t wq[2] = {0x3f803f80u, 0x3f803f80u}, wk[2] = {0x3f803f80u, 0x3f803f80u};  // bf16 1.0
+  if (qn_w) { wq[0] = reinterpret_cast<const uint32_t*>(qn_w)[lane]; wq[1] = reinterpret_cast<const uint32_t*>(qn_w)[32 + lane]; }
+  if (kn_w) { wk[0] = reinterpret_cast<const uint32_t*>(kn_w)[lane]; wk[1] = reinterpret_cast<const uint32_t*>(kn_w)[32 + lane]; }
+  pdl_wait();
+  const uint32_t* row = reinterpret_cast<const uint32_t*>(qkv + static_cast<long>(t) * nh * hd);
+  uint32_t xa[kQkMaxHeadsPerWarp], xb[kQkMaxHeadsPerWarp];
+#pragma unroll
+  for (int i = 0; i < kQkMaxHeadsPerWarp; ++i) {
+    const int head = warp + i * nw;
+    if (head < nh) {
+      xa[i] = row[head * (hd / 2) + lane];
+      xb[i] = row[head * (hd / 2) + 32 + lane];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kQkMaxHeadsPerWarp; ++i) {
+    const int head = warp + i * nw;
+    if (head >= nh) break;
+    uint32_t* dst;
+    if (head >= hq + hkv) {  // V: straight into the cache
+      dst = reinterpret_cast<uint32_t*>(v_cache + static_cast<long>(head - hq - hkv) * cache_head_stride +
+                                        static_cast<long>(pos) * hd);
+      dst[lane] = xa[i];
+      dst[32 + lane] = xb[i];
+      continue;
+    }
+    const bool is_q = head < hq;
+    const bf16* nwp = is_q ? qn_w : kn_w;
+    const uint32_t w0 = is_q ? wq[0] : wk[0], w1 = is_q ? wq[1] : wk[1];
+    const float v0 = bf16_lo(xa[i]), v1 = bf16_hi(xa[i]), v2 = bf16_lo(xb[i]), v3 = bf16_hi(xb[i]);
+    float rstd = 1.0f;
+    if (nwp) {
+      float ss = fmaf(v0, v0, 0.f);
+      ss = fmaf(v1, v1, ss);
+      ss = fmaf(v2, v2, ss);
+      ss = fmaf(v3, v3, ss);
+      rstd = rsqrtf(warp_sum(ss) / hd + eps);
+    }
+    const float n0 = v0 * rstd * bf16_lo(w0), n1 = v1 * rstd * bf16_hi(w0);
+    const float n2 = v2 * rstd * bf16_lo(w1), n3 = v3 * rstd * bf16_hi(w1);
+    dst = is_q ? reinterpret_cast<uint32_t*>(q_out + (static_cast<long>(t) * hq + head) * hd)
+               : reinterpret_cast<uint32_t*>(k_cache + static_cast<long>(head - hq) * cache_head_stride +
+                                             static_cast<long>(pos) * hd);
+    dst[lane] = pack_bf16x2(n0 * cs.x - n2 * cs.y, n1 * cs.z - n3 * cs.w);
+    dst[32 + lane] = pack_bf16x2(n2 * cs.x + n0 * cs.y, n3 * cs.z + n1 * cs.w);
+  }
+}
+
 cudaError_t launch_qk_norm_rope(const bf16* qkv, int T, int hq, int hkv, int hd, const bf16* qn_w,
                                 const bf16* kn_w, float eps, const float2* rope, int pos0,
                                 bf16* q_out, bf16* k_cache, bf16* v_cache, int cache_head_stride,
                                 cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
+  if (hd == 128 && hq + 2 * hkv <= 8 * kQkMaxHeadsPerWarp)
+    return launch_k(qk_norm_rope128_kernel, dim3(T), dim3(256), 0, st, qkv, hq, hkv, qn_w, kn_w, eps, rope,
+                    pos0, q_out, k_cache, v_cache, cache_head_stride);
   return launch_k(qk_norm_rope_kernel, dim3(T), dim3(256), 0, st, qkv, hq, hkv, hd, qn_w, kn_w, eps, rope, pos0, q_out,
                                          k_cache, v_cache, cache_head_stride);
 }

@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
     fence_barrier_init();
   }
   __syncthreads();
+#if defined(LS_GEMV_EXP) && (LS_GEMV_EXP & 32)  // diagnostic: launch + setup only
+  return;
+#endif
 
   if (warp == kWarps) {  // ---- producer warp: one chunk (<= 4 pages + masks) per slot ----
     if (lane == 0) {
@@ -108,7 +111,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_excoff) + a.ct_page0;
   const uint32_t* exc = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_exc);
   const bool has_mask = h->off_escmask != 0;
+#if defined(LS_GEMV_EXP) && (LS_GEMV_EXP & 16)  // diagnostic: no x prologue (wrong results)
+  pdl_wait();
+#else
   gemv_stage_x<kConsumers>(a, xq, scratch, K, tid, lane, warp);
+#endif
   named_bar(1, kConsumers);
 
   const int g = lane >> 2, t4 = lane & 3;

@@ -276,9 +276,10 @@ def test_flash_two_segments_expert(kv_splits):
     _close(out, _attn_ref(q, kk, vv, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
 
 
-def test_qk_norm_rope_prefill_kernel():
+@pytest.mark.parametrize("T,hq,hkv,hd", [(50, 8, 2, 32), (64, 32, 8, 128)])
+def test_qk_norm_rope_prefill_kernel(T, hq, hkv, hd):
+    """hd 128 takes the register path (RoPE pairs inside a lane), others the generic one."""
     torch.manual_seed(11)
-    T, hq, hkv, hd = 50, 8, 2, 32
     qkv = torch.randn(T, (hq + 2 * hkv) * hd, device=DEV).to(torch.bfloat16)
     qn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
     kn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
@@ -373,3 +374,15 @@ def test_gemm_ect_pages_bit_identical(epi, T, n, k, splitk, page0):
     K.gemm(epi, None, n, k, x, b, n_valid=ncol, splitk=splitk, ct_blob=blob, ct_page0=page0)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("T,D", [(64, 2048), (7, 4096), (5, 1152)])
+def test_rmsnorm_rows_kernel(T, D):
+    """fp32 rows -> bf16 RMSNorm(x) * w; D % 1024 == 0 uses the register path."""
+    torch.manual_seed(12)
+    x = torch.randn(T, D, device=DEV) * 3
+    w = (1 + 0.1 * torch.randn(D, device=DEV)).to(torch.bfloat16)
+    out = torch.empty(T, D, dtype=torch.bfloat16, device=DEV)
+    K.rmsnorm_rows(x, w, out, 1e-6)
+    ref = x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6) * w.float()
+    _close(out, ref, rel=1e-2, abs_=1e-2)

@@ -208,6 +208,9 @@ def main():
     if args.only == "flash":
         for sp in (1, 2, 4, 8):
             res.append(bench_flash_expert(sp))
+    if args.only == "overhead_ect":
+        for n, k in ((18944, 64), (18944, 1024), (6144, 4096), (4096, 4096)):
+            res.append(bench_gemv_ect(n, k, K.GEMV_F32))
     if args.only == "overhead":  # fixed per-launch cost: tiny and mid shapes, ECT and plain
         for n, k in ((18944, 64), (18944, 256), (18944, 1024), (6144, 4096), (24576, 4096)):
             res.append(bench_gemv_ect(n, k, K.GEMV_F32))
