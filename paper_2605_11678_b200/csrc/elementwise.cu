@@ -21,9 +21,9 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 }
 
 // RMSNorm over rows of an fp32 [T x D] residual stream -> bf16 GEMM operand.
-// Rows with D % 1024 == 0 and D <= 4096 (every hidden size here): a thread
-// holds its float4 groups in registers -- x is read once, in one round trip,
-// and the norm weights are fetched before pdl_wait.
+// Rows with D % 4 == 0 and D <= 4096 (every hidden size here): a thread holds
+// its float4 groups (group v * 256 + tid) in registers -- x is read once, in
+// one round trip, and the norm weights are fetched before pdl_wait.
 constexpr int kNormMaxV = 4;  // float4 per thread (256 threads -> D <= 4096)
 
 __global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, int D, float eps) {
@@ -31,18 +31,18 @@ __global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, in
   __shared__ float sh[32];
   const float* xr = x + static_cast<long>(blockIdx.x) * D;
   bf16* o = out + static_cast<long>(blockIdx.x) * D;
-  if (D % 1024 == 0 && D <= 1024 * kNormMaxV) {
-    const int nv = D / 1024;
+  const int ng = D / 4;
+  if (D % 4 == 0 && ng <= 256 * kNormMaxV) {
     uint2 wv[kNormMaxV];
 #pragma unroll
     for (int v = 0; v < kNormMaxV; ++v)
-      if (v < nv) wv[v] = reinterpret_cast<const uint2*>(w)[v * 256 + threadIdx.x];
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) wv[v] = reinterpret_cast<const uint2*>(w)[v * 256 + threadIdx.x];
     pdl_wait();
     float4 xv[kNormMaxV];
     float ss = 0.f;
 #pragma unroll
     for (int v = 0; v < kNormMaxV; ++v)
-      if (v < nv) {
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) {
         xv[v] = reinterpret_cast<const float4*>(xr)[v * 256 + threadIdx.x];
         ss = fmaf(xv[v].x, xv[v].x, ss);
         ss = fmaf(xv[v].y, xv[v].y, ss);
@@ -52,7 +52,7 @@ __global__ void rmsnorm_rows_kernel(const float* x, const bf16* w, bf16* out, in
     const float rstd = rsqrtf(block_sum(ss, sh) / D + eps);
 #pragma unroll
     for (int v = 0; v < kNormMaxV; ++v)
-      if (v < nv) {
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) {
         uint2 r;
         r.x = pack_bf16x2(xv[v].x * rstd * bf16_lo(wv[v].x), xv[v].y * rstd * bf16_hi(wv[v].x));
         r.y = pack_bf16x2(xv[v].z * rstd * bf16_lo(wv[v].y), xv[v].w * rstd * bf16_hi(wv[v].y));
@@ -76,9 +76,52 @@ cudaError_t launch_rmsnorm_rows(const float* x, const bf16* w, bf16* out, int T,
 __global__ void layernorm_rows_kernel(const float* x, const bf16* w, const bf16* b, bf16* out,
                                       int D, long ld_out, float eps) {
   pdl_trigger();
-  pdl_wait();
   __shared__ float sh[32];
   const float* xr = x + static_cast<long>(blockIdx.x) * D;
+  const int ng = D / 4;
+  if (D % 4 == 0 && ng <= 256 * kNormMaxV && ld_out % 4 == 0) {  // register path (see rmsnorm)
+    uint2 wv[kNormMaxV], bv[kNormMaxV];
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) {
+        wv[v] = reinterpret_cast<const uint2*>(w)[v * 256 + threadIdx.x];
+        bv[v] = reinterpret_cast<const uint2*>(b)[v * 256 + threadIdx.x];
+      }
+    pdl_wait();
+    float4 xv[kNormMaxV];
+    float s1 = 0.f;
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) {
+        xv[v] = reinterpret_cast<const float4*>(xr)[v * 256 + threadIdx.x];
+        s1 += xv[v].x + xv[v].y + xv[v].z + xv[v].w;
+      }
+    const float mean = block_sum(s1, sh) / D;
+    float v2 = 0.f;
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) {
+        const float d0 = xv[v].x - mean, d1 = xv[v].y - mean, d2 = xv[v].z - mean, d3 = xv[v].w - mean;
+        v2 = fmaf(d0, d0, v2);
+        v2 = fmaf(d1, d1, v2);
+        v2 = fmaf(d2, d2, v2);
+        v2 = fmaf(d3, d3, v2);
+      }
+    const float rstd = rsqrtf(block_sum(v2, sh) / D + eps);
+    bf16* o = out + static_cast<long>(blockIdx.x) * ld_out;
+#pragma unroll
+    for (int v = 0; v < kNormMaxV; ++v)
+      if (v * 256 + static_cast<int>(threadIdx.x) < ng) {
+        uint2 r;
+        r.x = pack_bf16x2((xv[v].x - mean) * rstd * bf16_lo(wv[v].x) + bf16_lo(bv[v].x),
+                          (xv[v].y - mean) * rstd * bf16_hi(wv[v].x) + bf16_hi(bv[v].x));
+        r.y = pack_bf16x2((xv[v].z - mean) * rstd * bf16_lo(wv[v].y) + bf16_lo(bv[v].y),
+                          (xv[v].w - mean) * rstd * bf16_hi(wv[v].y) + bf16_hi(bv[v].y));
+        reinterpret_cast<uint2*>(o)[v * 256 + threadIdx.x] = r;
+      }
+    return;
+  }
+  pdl_wait();
   float s = 0.f;
   for (int i = threadIdx.x; i < D; i += blockDim.x) s += xr[i];
   const float mean = block_sum(s, sh) / D;

@@ -386,3 +386,18 @@ def test_rmsnorm_rows_kernel(T, D):
     K.rmsnorm_rows(x, w, out, 1e-6)
     ref = x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6) * w.float()
     _close(out, ref, rel=1e-2, abs_=1e-2)
+
+
+@pytest.mark.parametrize("T,D,ld", [(9, 1152, 1152), (4, 1152, 1280), (3, 1000, 1000)])
+def test_layernorm_rows_kernel(T, D, ld):
+    """fp32 rows -> bf16 LayerNorm(x) * w + b into a row pitch ld (ViT); register path for D % 4 == 0."""
+    torch.manual_seed(13)
+    x = torch.randn(T, D, device=DEV) * 2 + 0.5
+    w = (1 + 0.1 * torch.randn(D, device=DEV)).to(torch.bfloat16)
+    b = (0.1 * torch.randn(D, device=DEV)).to(torch.bfloat16)
+    buf = torch.zeros(T, ld, dtype=torch.bfloat16, device=DEV)
+    out = buf[:, :D]
+    K.layernorm_rows(x, w, b, out, 1e-6)
+    ref = torch.nn.functional.layer_norm(x, (D,), eps=1e-6) * w.float() + b.float()
+    _close(out, ref, rel=1e-2, abs_=1e-2)
+    assert not buf[:, D:].any()
