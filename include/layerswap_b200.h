@@ -261,7 +261,7 @@ int ls_exec_stats(ls_exec* e, int64_t out[3]);
 /* Host wall time (us) the last ls_exec_run spent enqueueing work, i.e. before
    its final stream synchronisation (enqueue-bound when close to the device time). */
 int ls_exec_enqueue_us(ls_exec* e, double* us);
-/* Diagnostics: leave out kernels of the expert layer (bit mask; results are
+/* Diagnostics: leave out kernels of the expert / LM decode layer (bit mask; results are
  * wrong -- timing only, tools/layer_breakdown.py).  0 = normal. */
 int ls_exec_set_diag_skip(ls_exec* e, uint32_t mask);
 

@@ -277,8 +277,8 @@ struct ls_exec {
   uint64_t gen = 0;  // bumped whenever resident pointers or the layout change
   cudaGraphExec_t gexec = nullptr;
   uint64_t gkey[12] = {};
-  // diagnostics only (tools/layer_breakdown.py): kernels of the expert layer
-  // to leave out -- results are wrong, the timing difference is the cost
+  // diagnostics only (tools/layer_breakdown.py): kernels of the expert /
+  // LM decode layer to leave out -- results are wrong, the timing difference is the cost
   uint32_t diag_skip = 0;
   std::vector<RunRec> grecs;  // invocation-span records of the captured run
   cudaEvent_t join_ev = nullptr, fork_ev = nullptr;
@@ -530,7 +530,8 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   q.k_cache = e->kc(l);
   q.v_cache = e->vc(l);
   q.cache_head_stride = e->cache_stride();
-  RC(gemv(e, GEMV_QKV, e->gp_qkv, part(0), e->dec_h, e->dec_q, part(4), nullptr, -1, &q, cb, pg(0)));
+  const uint32_t skip = e->diag_skip;
+  if (!(skip & 256)) RC(gemv(e, GEMV_QKV, e->gp_qkv, part(0), e->dec_h, e->dec_q, part(4), nullptr, -1, &q, cb, pg(0)));
   DecodeAttnArgs a{};
   a.q = e->dec_q;
   a.k_cache = e->kc(l);
@@ -543,11 +544,12 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.scale = 1.0f / std::sqrt(static_cast<float>(d.lm_hd));
   a.out = e->dec_attn;
   a.n_split = decode_attn_splits(pos + 1);  // one cluster of <= 16 CTAs, merged over DSMEM
-  KL(launch_decode_attention(a, e->ss));
-  RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h, cb, pg(1)));
-  RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn, nullptr,
-          cb, pg(2)));
-  RC(resid_gemv(e, e->gp_down, part(3), e->dec_mlp, e->dec_h, cb, pg(3)));
+  if (!(skip & 128)) KL(launch_decode_attention(a, e->ss));
+  if (!(skip & 512)) RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h, cb, pg(1)));
+  if (!(skip & 1024))
+    RC(gemv(e, GEMV_SILU, e->gp_gu, part(2), e->dec_h, e->dec_mlp, part(5), nullptr, d.lm_ffn, nullptr,
+            cb, pg(2)));
+  if (!(skip & 2048)) RC(resid_gemv(e, e->gp_down, part(3), e->dec_mlp, e->dec_h, cb, pg(3)));
   return LS_OK;
 }
 

@@ -1,7 +1,7 @@
 """In-context cost of each expert-layer kernel (subtractive): run the planned
 Alpamayo-shaped inference with one kernel kind left out of every expert layer
 (ls_exec_set_diag_skip; results are wrong, only the timing is used) and report
-the latency difference per expert layer invocation.
+the latency difference per expert layer invocation / LM decode layer-step.
 
     python tools/layer_breakdown.py [--profile profiles/r1_profile_alpamayo_ect.json] [--runs 3]
 """
@@ -17,6 +17,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 MASKS = {"rmsnorm x2": 1, "qk_norm_rope": 2, "attention": 4, "qkv gemm": 8, "o gemm": 16,
          "gate|up gemm": 32, "down gemm": 64, "all": 127}
+# LM decode layer (bits 7..11), reported per decode layer-step
+DEC_MASKS = {"dec attention": 128, "dec qkv gemv": 256, "dec o gemv": 512, "dec gate|up gemv": 1024,
+             "dec down gemv": 2048, "dec all": 128 | 256 | 512 | 1024 | 2048}
 
 
 def main():
@@ -47,6 +50,11 @@ def main():
         ms = run(m)
         res["per_layer_us"][name] = (base - ms) * 1e3 / n_inv
         print(f"{name:14s} {ms:8.2f} ms  -> {res['per_layer_us'][name]:7.2f} us per expert layer", flush=True)
+    n_dec = cfg.layers_of(M.KIND_LM) * cfg.decode_steps
+    for name, m in DEC_MASKS.items():
+        ms = run(m)
+        res["per_layer_us"][name] = (base - ms) * 1e3 / n_dec
+        print(f"{name:16s} {ms:8.2f} ms  -> {res['per_layer_us'][name]:7.2f} us per decode layer-step", flush=True)
     run(0)
     eng.close()
     print(json.dumps(res))
