@@ -55,16 +55,28 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
   // peers may write our shared memory only once we run: announce it now, wait
   // for everyone's announcement right before the first remote store
   if (a.n_split > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  pdl_wait();
   const int chunk = (a.n_ctx + a.n_split - 1) / a.n_split;
   const int p0 = split * chunk, p1 = min(a.n_ctx, p0 + chunk);
   const int np = max(p1 - p0, 0);
+  // positions < n_ctx - 1 were cached by earlier steps: their bulk copies go out
+  // before griddepcontrol.wait; only the newest position (appended by the QKV
+  // GEMV this kernel follows) waits for it
+  const int n_old = max(min(p1, a.n_ctx - 1) - p0, 0);
+  const long off = static_cast<long>(kh) * a.cache_head_stride + static_cast<long>(p0) * HD;
   if (threadIdx.x == 0 && np > 0) {
-    const uint32_t bytes = static_cast<uint32_t>(np * HD * 2);
-    mbar_arrive_expect_tx(&bar, 2 * bytes);
-    const long off = static_cast<long>(kh) * a.cache_head_stride + static_cast<long>(p0) * HD;
-    bulk_g2s(ks, a.k_cache + off, bytes, &bar);
-    bulk_g2s(vs, a.v_cache + off, bytes, &bar);
+    mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(2 * np * HD * 2));
+    if (n_old > 0) {
+      const uint32_t bytes = static_cast<uint32_t>(n_old * HD * 2);
+      bulk_g2s(ks, a.k_cache + off, bytes, &bar);
+      bulk_g2s(vs, a.v_cache + off, bytes, &bar);
+    }
+  }
+  pdl_wait();
+  if (threadIdx.x == 0 && np > n_old) {
+    const uint32_t bytes = static_cast<uint32_t>((np - n_old) * HD * 2);
+    const long o2 = off + static_cast<long>(n_old) * HD;
+    bulk_g2s(ks + n_old * HD, a.k_cache + o2, bytes, &bar);
+    bulk_g2s(vs + n_old * HD, a.v_cache + o2, bytes, &bar);
   }
   const float sl2 = a.scale * 1.4426950408889634f;
   for (int i = threadIdx.x; i < G * HD; i += 128) qs[i] = a.q[kh * G * HD + i] * sl2;
@@ -253,7 +265,6 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   bf16* ks_buf = qs + BM * LD;          // [2][BN][LD]: double-buffered K and V blocks
   bf16* vs_buf = ks_buf + 2 * BN * LD;
   pdl_trigger();
-  pdl_wait();
 
   const int h = blockIdx.y, kvh = h / (a.hq / a.hkv);
   const int q0 = blockIdx.x * BM;
@@ -261,30 +272,6 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   const int g = lane >> 2, t4 = lane & 3;
   const float sl2 = a.scale * 1.4426950408889634f;
 
-  // ---- Q tile -> smem (zero padded) ----
-  for (int i = threadIdx.x; i < BM * (DK / 8); i += 128) {
-    const int r = i / (DK / 8), c = i % (DK / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (q0 + r < a.Tq && c < CH)
-      v = *reinterpret_cast<const uint4*>(a.q + static_cast<long>(q0 + r) * a.q_tok_stride +
-                                          static_cast<long>(h) * a.q_head_stride + c * 8);
-    *reinterpret_cast<uint4*>(qs + r * LD + c * 8) = v;
-  }
-  __syncthreads();
-  uint32_t qf[DK / 16][4];
-  {
-    const bf16* qr = qs + (warp * 16) * LD;
-#pragma unroll
-    for (int kk = 0; kk < DK / 16; ++kk) {
-      qf[kk][0] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 2 * t4);
-      qf[kk][1] = *reinterpret_cast<const uint32_t*>(qr + (g + 8) * LD + kk * 16 + 2 * t4);
-      qf[kk][2] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 8 + 2 * t4);
-      qf[kk][3] = *reinterpret_cast<const uint32_t*>(qr + (g + 8) * LD + kk * 16 + 8 + 2 * t4);
-    }
-  }
-  float o[ND][4];
-#pragma unroll
-  for (int j = 0; j < ND; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const int qi[2] = {q0 + warp * 16 + g, q0 + warp * 16 + g + 8};
 
@@ -357,7 +344,36 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   // 0..3 = dims +0, +8, +16, +24 of a k-step pair, rows = the 8 keys of n-tile
   const int kl_row = lane & 7, kl_col = (lane >> 3) * 8;
   const int q_lo = q0 + a.q_offset;  // smallest query position of the tile (causal)
-  if (k_begin < k_end) load_kv(0, k_begin);
+  // the first K/V block is requested before griddepcontrol.wait when it lies in
+  // a segment the previous kernel did not write (the expert over the VLM cache)
+  const bool early = a.k1_ready && k_begin < k_end && k_begin + BN <= a.len1;
+  if (early) load_kv(0, k_begin);
+  pdl_wait();
+  // ---- Q tile -> smem (zero padded), after griddepcontrol.wait ----
+  for (int i = threadIdx.x; i < BM * (DK / 8); i += 128) {
+    const int r = i / (DK / 8), c = i % (DK / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (q0 + r < a.Tq && c < CH)
+      v = *reinterpret_cast<const uint4*>(a.q + static_cast<long>(q0 + r) * a.q_tok_stride +
+                                          static_cast<long>(h) * a.q_head_stride + c * 8);
+    *reinterpret_cast<uint4*>(qs + r * LD + c * 8) = v;
+  }
+  __syncthreads();
+  uint32_t qf[DK / 16][4];
+  {
+    const bf16* qr = qs + (warp * 16) * LD;
+#pragma unroll
+    for (int kk = 0; kk < DK / 16; ++kk) {
+      qf[kk][0] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 2 * t4);
+      qf[kk][1] = *reinterpret_cast<const uint32_t*>(qr + (g + 8) * LD + kk * 16 + 2 * t4);
+      qf[kk][2] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 8 + 2 * t4);
+      qf[kk][3] = *reinterpret_cast<const uint32_t*>(qr + (g + 8) * LD + kk * 16 + 8 + 2 * t4);
+    }
+  }
+  float o[ND][4];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  if (!early && k_begin < k_end) load_kv(0, k_begin);
   int buf = 0;
   for (int j0 = k_begin; j0 < k_end; j0 += BN, buf ^= 1) {
     if (j0 + BN < k_end) {

@@ -587,6 +587,7 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   f.o_tok_stride = AH;
   f.o_head_stride = d.ex_hd;
   f.kv_splits = e->ex_kv_splits;
+  f.k1_ready = 1;  // the VLM cache was written before the expert runs
   f.ws = e->flash_ws;
   f.counters = e->flash_cnt;
   if (!(skip & 4)) KL(launch_flash_attention(f, e->ss));

@@ -132,6 +132,9 @@ struct FlashArgs {
   int kv_splits;   // <= 1: off
   float* ws;
   int* counters;
+  // 1: segment 1 was not written by the previous kernel (the expert reading the
+  // VLM cache) -- its first K/V block is requested before griddepcontrol.wait
+  int k1_ready;
 };
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st);
 // kv_splits the launcher will use for (Tq, hq, keys) given num_sms, and the

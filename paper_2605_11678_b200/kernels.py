@@ -42,7 +42,8 @@ class FlashArgs(C.Structure):
                 ("out", _vp), ("o_tok_stride", C.c_int64), ("o_head_stride", C.c_int64),
                 ("Tq", C.c_int32), ("hq", C.c_int32), ("hkv", C.c_int32), ("hd", C.c_int32),
                 ("causal", C.c_int32), ("q_offset", C.c_int32), ("seg_len", C.c_int32),
-                ("scale", C.c_float), ("kv_splits", C.c_int32), ("ws", _vp), ("counters", _vp)]
+                ("scale", C.c_float), ("kv_splits", C.c_int32), ("ws", _vp), ("counters", _vp),
+                ("k1_ready", C.c_int32)]
 
 
 GEMV_F32, GEMV_RESID, GEMV_SILU, GEMV_QKV, GEMV_ARGMAX = range(5)

@@ -216,7 +216,7 @@ def _attn_ref(q, k, v, mask, scale):
     return (torch.softmax(s, -1) @ vv).permute(1, 0, 2)
 
 
-def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0, kv_splits=0):
+def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0, kv_splits=0, k1_ready=0):
     a = K.FlashArgs(q=q.data_ptr(), q_tok_stride=q.stride(0), q_head_stride=q.stride(1),
                     k1=k1.data_ptr(), v1=v1.data_ptr(), k1_tok_stride=k1.stride(0),
                     k1_head_stride=k1.stride(1), len1=k1.shape[0],
@@ -229,6 +229,7 @@ def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0,
                     Tq=q.shape[0], hq=hq, hkv=hkv, hd=hd, causal=causal, q_offset=q_offset,
                     seg_len=seg_len, scale=1 / math.sqrt(hd))
     a.kv_splits = kv_splits  # > 1: one thread-block cluster per (q tile, head), DSMEM merge
+    a.k1_ready = k1_ready    # first K/V block of segment 1 requested before griddepcontrol.wait
     K.flash_attention(a)
 
 
@@ -269,7 +270,7 @@ def test_flash_two_segments_expert(kv_splits):
     out = torch.empty(Tq, hq, hd, dtype=torch.bfloat16, device=DEV)
     k1v = cache_k.permute(1, 0, 2)  # strided view [pos][head][d]
     v1v = cache_v.permute(1, 0, 2)
-    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd, kv_splits=kv_splits)
+    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd, kv_splits=kv_splits, k1_ready=1)
     kk = torch.cat([k1v[:L1], k2], 0)
     vv = torch.cat([v1v[:L1], v2], 0)
     mask = torch.ones(Tq, L1 + Tq, dtype=torch.bool, device=DEV)

@@ -168,7 +168,7 @@ def bench_flash_expert(kv_splits, ctx=1045, T=64, hq=32, hkv=8, hd=128, max_ctx=
                     k2_head_stride=T * hd, len2=T, out=out.data_ptr(), o_tok_stride=out.stride(0),
                     o_head_stride=out.stride(1), Tq=T, hq=hq, hkv=hkv, hd=hd, causal=0, q_offset=0,
                     seg_len=0, scale=1 / math.sqrt(hd), kv_splits=kv_splits, ws=ws.data_ptr(),
-                    counters=cnt.data_ptr())
+                    counters=cnt.data_ptr(), k1_ready=1)
     ms = timed(lambda: K.flash_attention(a))
     flops = 4.0 * T * hq * (ctx + T) * hd
     return {"kernel": f"flash expert T={T} keys={ctx + T} kv_splits={kv_splits}", "us": ms * 1e3,
