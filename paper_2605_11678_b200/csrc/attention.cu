@@ -18,7 +18,7 @@ namespace lsb {
 
 // ------------------------------- decode ---------------------------------------
 //
-// grid (hkv, n_split) launched as clusters of n_split CTAs (<= 16) along y, 128
+// grid (hkv, n_split) launched as clusters of n_split CTAs (<= 16) along y, kDecThreads
 // threads.  Each CTA owns <= kDecChunk consecutive positions of one KV head:
 // its K and V rows are contiguous in the cache, so two 1-D bulk copies (TMA
 // engine) land them in shared memory with one mbarrier wait.  Scores: one
@@ -29,10 +29,11 @@ namespace lsb {
 // reading every peer's partial over DSMEM, in split order (deterministic).
 
 constexpr int kDecChunk = 128;
+constexpr int kDecThreads = 256;  // 2 scores / 1 output pair per thread per head group
 constexpr int kDecMaxSplits = 16;
 
 template <int HD, int G>
-__global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a) {
+__global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAttnArgs a) {
   namespace cg = cooperative_groups;
   constexpr int HP = HD / 2;  // bf16 pairs per row
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -79,11 +80,11 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
     bulk_g2s(vs + n_old * HD, a.v_cache + o2, bytes, &bar);
   }
   const float sl2 = a.scale * 1.4426950408889634f;
-  for (int i = threadIdx.x; i < G * HD; i += 128) qs[i] = a.q[kh * G * HD + i] * sl2;
+  for (int i = threadIdx.x; i < G * HD; i += kDecThreads) qs[i] = a.q[kh * G * HD + i] * sl2;
   __syncthreads();
   if (np > 0) mbar_wait(&bar, 0);
   // ---- scores (log2 domain) ----
-  for (int idx = threadIdx.x; idx < G * kDecChunk; idx += 128) {
+  for (int idx = threadIdx.x; idx < G * kDecChunk; idx += kDecThreads) {
     const int g = idx / kDecChunk, p = idx % kDecChunk;
     float sc = -INFINITY;
     if (p < np) {
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
   }
   __syncthreads();
   // ---- softmax per head: warp g (strided) ----
-  for (int g = warp; g < G; g += 4) {
+  for (int g = warp; g < G; g += kDecThreads / 32) {
     float mx = -INFINITY;
     for (int p = lane; p < kDecChunk; p += 32) mx = fmaxf(mx, ps[g * kDecChunk + p]);
     mx = warp_max(mx);
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
 #pragma unroll
     for (int g = 0; g < 2 * G; ++g) dst[g] = sm_ml[g];
   }
-  for (int idx = threadIdx.x; idx < G * HP; idx += 128) {
+  for (int idx = threadIdx.x; idx < G * HP; idx += kDecThreads) {
     const int g = idx / HP, dp = idx % HP;
     const uint32_t* vc = reinterpret_cast<const uint32_t*>(vs) + dp;
     const float* pg = ps + g * kDecChunk;
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeAttnArgs a
   cg::cluster_group cluster = cg::this_cluster();
   cluster.sync();
   const int lo = split * GHD / S, hi = (split + 1) * GHD / S;
-  for (int i = lo + threadIdx.x; i < hi; i += 128) {
+  for (int i = lo + threadIdx.x; i < hi; i += kDecThreads) {
     const int g = i / HD;
     float M = -INFINITY;
     for (int z = 0; z < S; ++z) M = fmaxf(M, recv_ml[z * 2 * G + g]);
@@ -206,7 +207,7 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.hkv, a.n_split);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(kDecThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute la[2];
