@@ -148,22 +148,22 @@ __device__ inline void gemv_epilogue_any(int epi, const GemvArgs& a, int mt, con
 // Consumer prologue shared by the decode GEMVs: x (fp32, optional fused
 // RMSNorm) -> the (hi, lo) bf16 B-word layout in shared memory.  Contains the
 // kernel's pdl_wait.  Ends without a barrier (callers sync the NC consumers).
-template <int NC>
+template <int NC, int RP = kXRegPairs>
 __device__ __forceinline__ void gemv_stage_x(const GemvArgs& a, uint32_t* xq, float* scratch, int K, int tid,
                                              int lane, int warp) {
+  constexpr int kXRegPairs = RP;  // register pairs per thread on the one-round-trip path
   // x pairs i = tid + j * consumers live in registers between the load, the
   // RMSNorm reduction and the scatter (one global round trip after pdl_wait);
   // the norm weights do not come from the previous kernel and load before it.
   const int KP = K / 2;
   if (KP <= kXRegPairs * NC) {
     float2 xv[kXRegPairs];
-    float2 nv[kXRegPairs];
+    uint32_t nv[kXRegPairs];  // bf16 pairs (norm weights do not come from the previous kernel)
 #pragma unroll
     for (int j = 0; j < kXRegPairs; ++j) {
       const int i = tid + j * NC;
-      nv[j] = make_float2(1.f, 1.f);
-      if (a.norm_w && i < KP)
-        nv[j] = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(a.norm_w)[i]);
+      nv[j] = 0x3f803f80u;  // (1, 1)
+      if (a.norm_w && i < KP) nv[j] = reinterpret_cast<const uint32_t*>(a.norm_w)[i];
     }
     pdl_wait();  // x, workspace and outputs belong to the previous kernel until here
 #pragma unroll
@@ -190,7 +190,7 @@ __device__ __forceinline__ void gemv_stage_x(const GemvArgs& a, uint32_t* xq, fl
 #pragma unroll
     for (int j = 0; j < kXRegPairs; ++j) {
       const int i = tid + j * NC;
-      if (i < KP) gemv_stage_pair(xq, i, xv[j].x * rstd * nv[j].x, xv[j].y * rstd * nv[j].y);
+      if (i < KP) gemv_stage_pair(xq, i, xv[j].x * rstd * bf16_lo(nv[j]), xv[j].y * rstd * bf16_hi(nv[j]));
     }
   } else {
     pdl_wait();

@@ -111,12 +111,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   const uint32_t* exc_off = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_excoff) + a.ct_page0;
   const uint32_t* exc = reinterpret_cast<const uint32_t*>(a.ct_blob + h->off_exc);
   const bool has_mask = h->off_escmask != 0;
-#if defined(LS_GEMV_EXP) && (LS_GEMV_EXP & 16)  // diagnostic: no x prologue (wrong results)
-  pdl_wait();
-#else
-  gemv_stage_x<kConsumers>(a, xq, scratch, K, tid, lane, warp);
-#endif
-  named_bar(1, kConsumers);
 
   const int g = lane >> 2, t4 = lane & 3;
   const int rb = warp & 7, kh = warp >> 3;  // row block, k-part (k-steps 2 kh, 2 kh + 1)
@@ -151,33 +145,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
   int rem = static_cast<int>(t1 - t0), par = 0;
   uint32_t t = static_cast<uint32_t>(t0), round = 0;
   const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
-  while (rem > 0) {
-    const int np = min(min(kChunk, a.n_kb - kb), rem);
-    const uint8_t* st = slots + s * kSlotBytes;
-    mbar_wait_u32(full0 + 8 * s, round & 1);
-    if (np == kChunk) {
-      uint4 bw[kChunk];
+  // K <= 4096 (QKV, O, gate|up): the first chunk's pages do not depend on the
+  // previous kernel -- decode them into registers while it drains, then stage x
+  uint32_t fr0[kChunk][2][4];
+  bool have0 = false;
+  if (K <= 8 * kConsumers && min(min(kChunk, a.n_kb - kb), rem) == kChunk) {
+    mbar_wait_u32(full0, 0);
 #pragma unroll
-      for (int q = 0; q < kChunk; ++q)
-        bw[q] = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
-      uint32_t fr[kChunk][2][4];
-#pragma unroll
-      for (int q = 0; q < kChunk; ++q)
-        frags(st + q * kEctPageBytes, t + q, lane_esc(st, q), fr[q]);
-#pragma unroll
-      for (int q = 0; q < kChunk; ++q) {
-        mma_bf16_16816(acc, fr[q][0], bw[q].x, bw[q].y);
-        mma_bf16_16816(acc, fr[q][1], bw[q].z, bw[q].w);
-      }
-    } else {
-      for (int q = 0; q < np; ++q) {
-        const uint4 bw = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
-        uint32_t fr[2][4];
-        frags(st + q * kEctPageBytes, t + q, lane_esc(st, q), fr);
-        mma_bf16_16816(acc, fr[0], bw.x, bw.y);
-        mma_bf16_16816(acc, fr[1], bw.z, bw.w);
-      }
-    }
+    for (int q = 0; q < kChunk; ++q) frags(slots + q * kEctPageBytes, t + q, lane_esc(slots, q), fr0[q]);
+    have0 = true;
+  }
+#if defined(LS_GEMV_EXP) && (LS_GEMV_EXP & 16)  // diagnostic: no x prologue (wrong results)
+  pdl_wait();
+#else
+  if (K <= 8 * kConsumers) gemv_stage_x<kConsumers, 4>(a, xq, scratch, K, tid, lane, warp);
+  else gemv_stage_x<kConsumers>(a, xq, scratch, K, tid, lane, warp);
+#endif
+  named_bar(1, kConsumers);
+  auto advance = [&](int np) {
     __syncwarp();
     if (lane == 0) mbar_arrive_u32(empty0 + 8 * s);
     if (++s == NQ) {
@@ -192,6 +177,45 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
       kb = 0;
       ++mt;
     }
+  };
+  if (have0) {  // the chunk decoded before x was staged
+#pragma unroll
+    for (int q = 0; q < kChunk; ++q) {
+      const uint4 bw = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
+      mma_bf16_16816(acc, fr0[q][0], bw.x, bw.y);
+      mma_bf16_16816(acc, fr0[q][1], bw.z, bw.w);
+    }
+    advance(kChunk);
+  }
+  while (rem > 0) {
+    const int np = min(min(kChunk, a.n_kb - kb), rem);
+    const uint8_t* st = slots + s * kSlotBytes;
+    if (np == kChunk) {
+      uint4 bw[kChunk];
+#pragma unroll
+      for (int q = 0; q < kChunk; ++q)
+        bw[q] = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
+      uint32_t fr[kChunk][2][4];
+      mbar_wait_u32(full0 + 8 * s, round & 1);
+#pragma unroll
+      for (int q = 0; q < kChunk; ++q)
+        frags(st + q * kEctPageBytes, t + q, lane_esc(st, q), fr[q]);
+#pragma unroll
+      for (int q = 0; q < kChunk; ++q) {
+        mma_bf16_16816(acc, fr[q][0], bw[q].x, bw[q].y);
+        mma_bf16_16816(acc, fr[q][1], bw[q].z, bw[q].w);
+      }
+    } else {
+      mbar_wait_u32(full0 + 8 * s, round & 1);
+      for (int q = 0; q < np; ++q) {
+        const uint4 bw = *reinterpret_cast<const uint4*>(xb + (kb + q) * 64);
+        uint32_t fr[2][4];
+        frags(st + q * kEctPageBytes, t + q, lane_esc(st, q), fr);
+        mma_bf16_16816(acc, fr[0], bw.x, bw.y);
+        mma_bf16_16816(acc, fr[1], bw.z, bw.w);
+      }
+    }
+    advance(np);
   }
   if (kb != 0) gemv_flush<EPI, kConsumers, 2>(a, acc, red, par, flag, mt, G, T, c, tid, g, t4, rb, kh);
 }
