@@ -20,7 +20,10 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
                                                          int with_tail, uint8_t* __restrict__ out) {
   __shared__ __align__(16) uint32_t tile[kTileBytes / 4];
   pdl_trigger();
-  pdl_wait();  // `out` (the decode scratch) is read by the previous layer's kernels
+  // pages never depend on the previous kernel, but `out` (the decode scratch) is
+  // read by it: the first page is loaded and decoded before griddepcontrol.wait,
+  // every store comes after it
+  bool waited = false;
   const EctHeader* h = reinterpret_cast<const EctHeader*>(blob);
   const uint32_t e0p = (h->e0 << 7) | (h->e0 << 23);
   const uint8_t* pages = blob + h->off_pages + static_cast<uint64_t>(page0) * kEctPageBytes;
@@ -60,12 +63,17 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
       }
       if (e_hi > e_lo) __syncthreads();
     }
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
     uint4* dst = reinterpret_cast<uint4*>(out + static_cast<uint64_t>(page) * kTileBytes);
 #pragma unroll
     for (int it = 0; it < 4; ++it)
       dst[it * 256 + threadIdx.x] = reinterpret_cast<const uint4*>(tile)[it * 256 + threadIdx.x];
     __syncthreads();
   }
+  if (!waited) pdl_wait();
   if (!with_tail) return;
   // raw tail (vectors), whole 16-byte chunks
   const uint64_t tail = (h->total - h->mat_bytes + 15) / 16;

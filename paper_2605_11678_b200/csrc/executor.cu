@@ -352,10 +352,11 @@ int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensor
     // several token tiles would each re-decode every page inside the GEMM: expand
     // this matrix's pages once into the decode scratch and run the plain GEMM on it
     // (the GEMM then must not prefetch weights before the decode has finished)
-    KL(launch_ect_decode_pages(reinterpret_cast<const uint8_t*>(ct_blob), static_cast<uint32_t>(ct_page0),
-                               static_cast<uint32_t>(n_mt(n)) * static_cast<uint32_t>(n_kb(k)), false,
-                               e->scratch, e->nsm, e->ss));
-    e->pdl_ok = false;
+    if (!(e->diag_skip & (1u << 12)))
+      KL(launch_ect_decode_pages(reinterpret_cast<const uint8_t*>(ct_blob), static_cast<uint32_t>(ct_page0),
+                                 static_cast<uint32_t>(n_mt(n)) * static_cast<uint32_t>(n_kb(k)), false,
+                                 e->scratch, e->nsm, e->ss));
+    a.w_dep = 1;  // PDL-chained after the decode, weights only after griddepcontrol.wait
     w = e->scratch;
     ct_blob = nullptr;
   }
@@ -484,7 +485,8 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   const char* cb = ct.blob;
   auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
   KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(4), e->lm_norm, S, D, d.lm_eps, e->ss));
-  RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN, nullptr, -1, cb, pg(0)));
+  const uint32_t skip = e->diag_skip;
+  if (!(skip & (1u << 14))) RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN, nullptr, -1, cb, pg(0)));
   KL(launch_qk_norm_rope(e->lm_qkv, S, d.lm_hq, d.lm_hkv, d.lm_hd, (const bf16*)part(6),
                          (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], 0, e->lm_q,
                          e->kc(l), e->vc(l), e->cache_stride(), e->ss));
@@ -501,12 +503,13 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   f.o_tok_stride = AH;
   f.o_head_stride = d.lm_hd;
   f.causal = 1;
-  KL(launch_flash_attention(f, e->ss));
-  RC(resid_gemm(e, part(1), D, AH, S, e->m_lm_attn, e->lm_h, nullptr, cb, pg(1)));
+  if (!(skip & (1u << 13))) KL(launch_flash_attention(f, e->ss));
+  if (!(skip & (1u << 15))) RC(resid_gemm(e, part(1), D, AH, S, e->m_lm_attn, e->lm_h, nullptr, cb, pg(1)));
   KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(5), e->lm_norm, S, D, d.lm_eps, e->ss));
-  RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.lm_ffn, D, S, e->m_lm_norm, e->lm_mlp, d.lm_ffn,
-          nullptr, d.lm_ffn, cb, pg(2)));
-  RC(resid_gemm(e, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h, nullptr, cb, pg(3)));
+  if (!(skip & (1u << 16)))
+    RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.lm_ffn, D, S, e->m_lm_norm, e->lm_mlp, d.lm_ffn,
+            nullptr, d.lm_ffn, cb, pg(2)));
+  if (!(skip & (1u << 17))) RC(resid_gemm(e, part(3), D, d.lm_ffn, S, e->m_lm_mlp, e->lm_h, nullptr, cb, pg(3)));
   return LS_OK;
 }
 

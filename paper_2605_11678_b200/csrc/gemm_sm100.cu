@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
       };
       int pre = 0;
 #ifndef LS_GEMM_NOPRE  // diagnostic build: every weight tile after pdl_wait
-      for (int t = blockIdx.x; t < n_tiles && pre < Cfg::kStages; t += gridDim.x) {
+      for (int t = blockIdx.x; !a.w_dep && t < n_tiles && pre < Cfg::kStages; t += gridDim.x) {
         const int tile = t / ks, sp = t % ks, mt = tile / n_nt;
         const int kb1 = (sp + 1) * n_kb / ks;
         for (int kb = sp * n_kb / ks; kb < kb1 && pre < Cfg::kStages; ++kb) a_load(pre++, mt, kb);

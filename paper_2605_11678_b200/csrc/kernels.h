@@ -88,6 +88,9 @@ struct GemmArgs {
   // ECT weights (see GemvArgs): w = the matrix's first page, tile t = page ct_page0 + t
   const uint8_t* ct_blob;
   int ct_page0;
+  // 1: w was written by the previous kernel (ECT decode scratch) -- no weight
+  // tile is requested before griddepcontrol.wait
+  int w_dep;
 };
 
 int gemm_block_n(int T);

@@ -55,6 +55,14 @@ def main():
         ms = run(m)
         res["per_layer_us"][name] = (base - ms) * 1e3 / n_dec
         print(f"{name:16s} {ms:8.2f} ms  -> {res['per_layer_us'][name]:7.2f} us per decode layer-step", flush=True)
+    n_pre = cfg.layers_of(M.KIND_LM)
+    for name, m in {"prefill ECT scratch decodes (all layers)": 1 << 12, "prefill attention": 1 << 13,
+                    "prefill qkv gemm": 1 << 14, "prefill o gemm": 1 << 15, "prefill gate|up gemm": 1 << 16,
+                    "prefill down gemm": 1 << 17}.items():
+        ms = run(m)
+        per = (base - ms) * 1e3 / n_pre
+        res["per_layer_us"][name] = per
+        print(f"{name:16s} {ms:8.2f} ms  -> {per:7.2f} us per prefill layer", flush=True)
     run(0)
     eng.close()
     print(json.dumps(res))
