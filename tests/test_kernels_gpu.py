@@ -300,10 +300,14 @@ def test_qk_norm_rope_prefill_kernel(T, hq, hkv, hd):
     assert torch.equal(vc[:, 5:5 + T].permute(1, 0, 2), qkv.view(T, -1, hd)[:, hq + hkv:])
 
 
-@pytest.mark.parametrize("n,k,page0", [(384, 256, 0), (6144, 4096, 0), (4096, 12288, 3)])
+@pytest.mark.parametrize("n,k,page0", [(384, 256, 0), (6144, 4096, 0), (4096, 12288, 3),
+                                       (320, 1152, 1),     # 18 k-blocks: chunks 4,4,4,4,2; ragged n
+                                       (128, 16384, 0),    # one m-tile over every CTA; x staged by the loop path
+                                       (2048, 64, 2)])     # one page per m-tile
 def test_gemv_ect_pages_bit_identical(n, k, page0):
-    """Decode GEMV over ECT pages (decoded in registers) == plain-tile GEMV, bit
-    for bit, including escaped exponents; pages may start mid-blob (page0)."""
+    """Decode GEMV over ECT pages (decoded in registers, 4-page chunks, escape
+    masks) == plain-tile GEMV, bit for bit, including escaped exponents; pages
+    may start mid-blob (page0); partial chunks, many-contributor fix-ups."""
     from paper_2605_11678_b200 import ect
     torch.manual_seed(7)
     w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
@@ -315,7 +319,7 @@ def test_gemv_ect_pages_bit_identical(n, k, page0):
     assert ect.header(blob)["n_exc"] > 0
     x = torch.randn(k, device=DEV)
     nw = (1 + 0.1 * torch.randn(k, device=DEV)).to(torch.bfloat16)
-    ws = K.GemvWorkspace(DEV)
+    ws = K.GemvWorkspace(DEV, max_contrib=160)  # (128, 16384): all 148 CTAs on one m-tile
     a = torch.empty(n, device=DEV)
     b = torch.empty(n, device=DEV)
     K.gemv(K.GEMV_F32, tiled, n, k, x, a, ws, norm_w=nw)
@@ -402,3 +406,26 @@ def test_layernorm_rows_kernel(T, D, ld):
     ref = torch.nn.functional.layer_norm(x, (D,), eps=1e-6) * w.float() + b.float()
     _close(out, ref, rel=1e-2, abs_=1e-2)
     assert not buf[:, D:].any()
+
+
+@pytest.mark.parametrize("epi", [1, 2])
+def test_gemv_ect_fused_epilogues_bit_identical(epi):
+    """RESID and SiLU*up epilogues (fused RMSNorm prologue) over ECT pages equal
+    the plain-tile launches bit for bit."""
+    from paper_2605_11678_b200 import ect
+    torch.manual_seed(17)
+    n, k = 2048, 4096
+    w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
+    tiled = K.pack_tiled(w)
+    flat = tiled.view(torch.uint8).reshape(-1)
+    blob = ect.compress(flat, flat.numel())
+    x = torch.randn(k, device=DEV)
+    nw = (1 + 0.1 * torch.randn(k, device=DEV)).to(torch.bfloat16)
+    ws = K.GemvWorkspace(DEV)
+    nv = n // 2 if epi == K.GEMV_SILU else n
+    base = torch.randn(nv, device=DEV)
+    a, b = base.clone(), base.clone()
+    K.gemv(epi, tiled, n, k, x, a, ws, norm_w=nw, n_valid=nv)
+    K.gemv(epi, None, n, k, x, b, ws, norm_w=nw, n_valid=nv, ct_blob=blob)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
