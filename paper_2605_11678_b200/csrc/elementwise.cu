@@ -136,9 +136,65 @@ __global__ void layernorm_rows_kernel(const float* x, const bf16* w, const bf16*
     o[i] = f2bf((xr[i] - mean) * rstd * bf2f(w[i]) + bf2f(b[i]));
 }
 
+// Narrow rows (ViT: D = 1152): one warp per row, the row in registers (<= 12
+// float4 per lane), shuffles only -- no block barriers, 8 rows per CTA.
+constexpr int kLnWarpMaxV = 12;
+__global__ void __launch_bounds__(256) layernorm_rows_warp_kernel(const float* x, const bf16* w, const bf16* b,
+                                                                  bf16* out, int T, int D, long ld_out,
+                                                                  float eps) {
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int ng = D / 4;
+  uint2 wv[kLnWarpMaxV], bv[kLnWarpMaxV];
+#pragma unroll
+  for (int v = 0; v < kLnWarpMaxV; ++v)
+    if (v * 32 + lane < ng) {
+      wv[v] = reinterpret_cast<const uint2*>(w)[v * 32 + lane];
+      bv[v] = reinterpret_cast<const uint2*>(b)[v * 32 + lane];
+    }
+  pdl_wait();
+  if (row >= T) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long>(row) * D);
+  float4 xv[kLnWarpMaxV];
+  float s1 = 0.f;
+#pragma unroll
+  for (int v = 0; v < kLnWarpMaxV; ++v)
+    if (v * 32 + lane < ng) {
+      xv[v] = xr[v * 32 + lane];
+      s1 += xv[v].x + xv[v].y + xv[v].z + xv[v].w;
+    }
+  const float mean = warp_sum(s1) / D;
+  float v2 = 0.f;
+#pragma unroll
+  for (int v = 0; v < kLnWarpMaxV; ++v)
+    if (v * 32 + lane < ng) {
+      const float d0 = xv[v].x - mean, d1 = xv[v].y - mean, d2 = xv[v].z - mean, d3 = xv[v].w - mean;
+      v2 = fmaf(d0, d0, v2);
+      v2 = fmaf(d1, d1, v2);
+      v2 = fmaf(d2, d2, v2);
+      v2 = fmaf(d3, d3, v2);
+    }
+  const float rstd = rsqrtf(warp_sum(v2) / D + eps);
+  uint2* o = reinterpret_cast<uint2*>(out + static_cast<long>(row) * ld_out);
+#pragma unroll
+  for (int v = 0; v < kLnWarpMaxV; ++v)
+    if (v * 32 + lane < ng) {
+      uint2 r;
+      r.x = pack_bf16x2((xv[v].x - mean) * rstd * bf16_lo(wv[v].x) + bf16_lo(bv[v].x),
+                        (xv[v].y - mean) * rstd * bf16_hi(wv[v].x) + bf16_hi(bv[v].x));
+      r.y = pack_bf16x2((xv[v].z - mean) * rstd * bf16_lo(wv[v].y) + bf16_lo(bv[v].y),
+                        (xv[v].w - mean) * rstd * bf16_hi(wv[v].y) + bf16_hi(bv[v].y));
+      o[v * 32 + lane] = r;
+    }
+}
+
 cudaError_t launch_layernorm_rows(const float* x, const bf16* w, const bf16* b, bf16* out, int T,
                                   int D, long ld_out, float eps, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
+  if (D % 4 == 0 && D / 4 <= 32 * kLnWarpMaxV && ld_out % 4 == 0)
+    return launch_k(layernorm_rows_warp_kernel, dim3((T + 7) / 8), dim3(256), 0, st, x, w, b, out, T, D, ld_out,
+                    eps);
   return launch_k(layernorm_rows_kernel, dim3(T), dim3(256), 0, st, x, w, b, out, D, ld_out, eps);
 }
 

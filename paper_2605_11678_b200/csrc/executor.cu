@@ -451,9 +451,11 @@ int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L, const CtView&
   auto part = [&](int i) { return ct.blob ? ct.part(L, i) : w + L.offset[i]; };
   const char* cb = ct.blob;
   auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
-  KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(8), (const bf16*)part(9), e->vit_ln, T, D, D,
-                           d.vit_eps, e->ss));
-  RC(gemm(e, GEMM_BF16, part(0), 3 * H, D, T, e->m_vit_ln, e->vit_qkv, 3 * H, part(4), -1, cb, pg(0)));
+  const uint32_t skip = e->diag_skip;
+  if (!(skip & (1u << 18)))
+    KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(8), (const bf16*)part(9), e->vit_ln, T, D, D,
+                             d.vit_eps, e->ss));
+  if (!(skip & (1u << 19))) RC(gemm(e, GEMM_BF16, part(0), 3 * H, D, T, e->m_vit_ln, e->vit_qkv, 3 * H, part(4), -1, cb, pg(0)));
   FlashArgs f = flash_base(T, d.vit_heads, d.vit_heads, d.vit_hd);
   f.q = e->vit_qkv;
   f.q_tok_stride = 3 * H;
@@ -467,13 +469,15 @@ int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L, const CtView&
   f.o_tok_stride = H;
   f.o_head_stride = d.vit_hd;
   f.seg_len = d.vit_tokens_per_image;
-  KL(launch_flash_attention(f, e->ss));
-  RC(resid_gemm(e, part(1), D, H, T, e->m_vit_attn, e->vit_h, part(5), cb, pg(1)));
-  KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(10), (const bf16*)part(11), e->vit_ln, T, D,
-                           D, d.vit_eps, e->ss));
-  RC(gemm(e, GEMM_BF16_GELU, part(2), F, D, T, e->m_vit_ln, e->vit_fc1, e->vit_ffn_pad, part(6), F, cb,
-          pg(2)));
-  RC(resid_gemm(e, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, part(7), cb, pg(3)));
+  if (!(skip & (1u << 20))) KL(launch_flash_attention(f, e->ss));
+  if (!(skip & (1u << 21))) RC(resid_gemm(e, part(1), D, H, T, e->m_vit_attn, e->vit_h, part(5), cb, pg(1)));
+  if (!(skip & (1u << 18)))
+    KL(launch_layernorm_rows(e->vit_h, (const bf16*)part(10), (const bf16*)part(11), e->vit_ln, T, D,
+                             D, d.vit_eps, e->ss));
+  if (!(skip & (1u << 22)))
+    RC(gemm(e, GEMM_BF16_GELU, part(2), F, D, T, e->m_vit_ln, e->vit_fc1, e->vit_ffn_pad, part(6), F, cb,
+            pg(2)));
+  if (!(skip & (1u << 23))) RC(resid_gemm(e, part(3), D, e->vit_ffn_pad, T, e->m_vit_fc1, e->vit_h, part(7), cb, pg(3)));
   return LS_OK;
 }
 

@@ -63,6 +63,13 @@ def main():
         per = (base - ms) * 1e3 / n_pre
         res["per_layer_us"][name] = per
         print(f"{name:16s} {ms:8.2f} ms  -> {per:7.2f} us per prefill layer", flush=True)
+    n_vit = cfg.layers_of(M.KIND_VIT)
+    for name, m in {"vit layernorm x2": 1 << 18, "vit qkv gemm": 1 << 19, "vit attention": 1 << 20,
+                    "vit proj gemm": 1 << 21, "vit fc1 gemm": 1 << 22, "vit fc2 gemm": 1 << 23}.items():
+        ms = run(m)
+        per = (base - ms) * 1e3 / n_vit
+        res["per_layer_us"][name] = per
+        print(f"{name:16s} {ms:8.2f} ms  -> {per:7.2f} us per vit layer", flush=True)
     run(0)
     eng.close()
     print(json.dumps(res))
