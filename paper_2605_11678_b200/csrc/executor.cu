@@ -24,6 +24,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -881,6 +882,7 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       OV(gemm_ws, 4ull * e->gemm_ws_floats);
       OV(gemm_cnt, 4ull * e->gemm_cnt_n);
       e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq, e->ctx + Te, e->nsm);
+      if (const char* ov = std::getenv("LS_DIAG_EX_KV_SPLITS")) e->ex_kv_splits = std::atoi(ov);  // diagnostics
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
     e->tp_world = std::max(1, d.tp_world);
