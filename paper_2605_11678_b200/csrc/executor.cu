@@ -281,6 +281,7 @@ struct ls_exec {
   // diagnostics only (tools/layer_breakdown.py): kernels of the expert /
   // LM decode layer to leave out -- results are wrong, the timing difference is the cost
   uint32_t diag_skip = 0;
+  int diag_dec_splits = 0;  // LS_DIAG_DEC_SPLITS: decode-attention split count override
   std::vector<RunRec> grecs;  // invocation-span records of the captured run
   cudaEvent_t join_ev = nullptr, fork_ev = nullptr;
   uint64_t h2d_bytes = 0;
@@ -552,6 +553,7 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.scale = 1.0f / std::sqrt(static_cast<float>(d.lm_hd));
   a.out = e->dec_attn;
   a.n_split = decode_attn_splits(pos + 1);  // one cluster of <= 16 CTAs, merged over DSMEM
+  if (e->diag_dec_splits > a.n_split && e->diag_dec_splits <= 16) a.n_split = e->diag_dec_splits;
   if (!(skip & 128)) KL(launch_decode_attention(a, e->ss));
   if (!(skip & 512)) RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h, cb, pg(1)));
   if (!(skip & 1024))
@@ -883,6 +885,7 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       OV(gemm_cnt, 4ull * e->gemm_cnt_n);
       e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq, e->ctx + Te, e->nsm);
       if (const char* ov = std::getenv("LS_DIAG_EX_KV_SPLITS")) e->ex_kv_splits = std::atoi(ov);  // diagnostics
+      if (const char* ov = std::getenv("LS_DIAG_DEC_SPLITS")) e->diag_dec_splits = std::atoi(ov);
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
     e->tp_world = std::max(1, d.tp_world);
