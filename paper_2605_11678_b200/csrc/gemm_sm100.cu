@@ -15,6 +15,7 @@
 //   * mbarrier full/empty ring, tcgen05.commit releases smem stages.
 #include <dlfcn.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -415,6 +416,11 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   GemmArgs b = a;
   b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n, CT) : 1;
+  static const int ks_cap = [] {  // LS_DIAG_GEMM_KS: split-K cap (diagnostics)
+    const char* v = std::getenv("LS_DIAG_GEMM_KS");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (ks_cap > 0 && b.ks > ks_cap) b.ks = ks_cap;
   const int units = a.n_mt * ((a.T + BN - 1) / BN) * b.ks;
   dim3 grid(units < nsm ? units : nsm);
   return launch_k(gemm_kernel<BN, EPI, CT>, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, map, b);
