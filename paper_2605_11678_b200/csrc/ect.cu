@@ -8,6 +8,8 @@
 // both sides; the 16-entry exponent table lives in shared memory.  Escapes
 // (~1.5e-4 of words on N(0, 0.02) weights) take a divergent slow path that
 // scans the page's short exception list.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -86,7 +88,11 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
 
 cudaError_t launch_ect_decode_pages(const uint8_t* blob, uint32_t page0, uint32_t n_pages,
                                     bool with_tail, void* out, int num_sms, cudaStream_t st) {
-  return launch_k(ect_decode_kernel, dim3(6 * num_sms), dim3(256), 0, st, blob, page0, n_pages,
+  static const int per_sm = [] {  // LS_DIAG_ECT_DEC_PER_SM: CTAs per SM (diagnostics)
+    const char* v = std::getenv("LS_DIAG_ECT_DEC_PER_SM");
+    return v ? std::atoi(v) : 8;  // 8 x 256 threads fill an SM; measured 3: +4.2 ms, 4: +2.2, 6: 0, 8: -1.1 ms
+  }();
+  return launch_k(ect_decode_kernel, dim3(per_sm * num_sms), dim3(256), 0, st, blob, page0, n_pages,
                   with_tail ? 1 : 0, static_cast<uint8_t*>(out));
 }
 
