@@ -25,10 +25,16 @@ namespace {
 constexpr int kWarps = 16;                 // 8 row blocks x 2 k-parts of every page
 constexpr int kConsumers = kWarps * 32;
 constexpr int kThreads = kConsumers + 32;  // + producer warp
-constexpr int kChunk = 4;                  // pages per ring slot
+#ifndef LS_GEMV_CHUNK
+#define LS_GEMV_CHUNK 4
+#endif
+#ifndef LS_GEMV_SLOTS
+#define LS_GEMV_SLOTS 4
+#endif
+constexpr int kChunk = LS_GEMV_CHUNK;      // pages per ring slot
 constexpr int kMaskBytes = 16;             // escape mask per page (1 bit per 64 words)
 constexpr int kSlotBytes = kChunk * (kEctPageBytes + kMaskBytes);
-constexpr int kMaxSlots = 4;
+constexpr int kMaxSlots = LS_GEMV_SLOTS;
 constexpr int kSmemBudget = 227 * 1024;
 
 __host__ __device__ inline int ect_slots(int n_kb) {
