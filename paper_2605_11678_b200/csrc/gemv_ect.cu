@@ -13,8 +13,14 @@
 //   * the per-page escape mask (16 B: one bit per 64 words = 4 lanes of a warp)
 //     says where code-15 words are, so the per-code escape test and the patch
 //     run only for those lanes (~1 % of lane groups for BF16 weights);
-//   * same stream-K split, fix-up and fused epilogues as gemv.cu (shared
+//   * pages never depend on the previous kernel: the producer fills the ring
+//     and (K <= 4096) the consumers decode the first chunk before
+//     griddepcontrol.wait / x staging;
+//   * same stream-K split, fix-up (one all-consumer barrier per m-tile, the
+//     rest on warps 0-3) and fused epilogues as gemv.cu (shared
 //     gemv_common.cuh), so plain and ECT launches give bit-identical results.
+// LS_GEMV_CHUNK / LS_GEMV_SLOTS are tuning knobs (4 x 4 measured best,
+// DESIGN.md §8c).
 #include "common.cuh"
 #include "gemv_common.cuh"
 #include "kernels.h"
