@@ -260,25 +260,29 @@ struct FlashCfg {
   static constexpr int kBM = 64, kBN = 64;
 };
 
-template <int HD>
-__global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
+// G > 1 (GQA packing): one CTA = G query heads of one KV head, 4 warps per head,
+// so each K/V block is loaded once for all G heads.
+template <int HD, int G = 1>
+__global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   using Cfg = FlashCfg<HD>;
+  constexpr int NT = 128 * G;
   constexpr int DK = Cfg::kDK, LD = Cfg::kLd, ND = Cfg::kND, BM = Cfg::kBM, BN = Cfg::kBN;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(16) uint8_t fsm[];
   bf16* qs = reinterpret_cast<bf16*>(fsm);
-  bf16* ks_buf = qs + BM * LD;          // [2][BN][LD]: double-buffered K and V blocks
+  bf16* ks_buf = qs + G * BM * LD;      // [2][BN][LD]: double-buffered K and V blocks
   bf16* vs_buf = ks_buf + 2 * BN * LD;
   pdl_trigger();
 
-  const int h = blockIdx.y, kvh = h / (a.hq / a.hkv);
-  const int q0 = blockIdx.x * BM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw = warp >> 2, wr = warp & 3;  // head of this warp within the CTA, row block
+  const int h = static_cast<int>(blockIdx.y) * G + hw, kvh = static_cast<int>(blockIdx.y) * G / (a.hq / a.hkv);
+  const int q0 = blockIdx.x * BM;
   const int g = lane >> 2, t4 = lane & 3;
   const float sl2 = a.scale * 1.4426950408889634f;
 
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-  const int qi[2] = {q0 + warp * 16 + g, q0 + warp * 16 + g + 8};
+  const int qi[2] = {q0 + wr * 16 + g, q0 + wr * 16 + g + 8};
 
   const int n_keys = a.len1 + a.len2;
   int k_begin = 0, k_end = n_keys;
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   // A thread always copies chunk column c of rows r0, r0 + 128 / (DK / 8), ...:
   // its per-segment base pointers are fixed, a row costs one multiply-add.
   constexpr int CPR = DK / 8;          // 16-byte chunks per (padded) row
-  constexpr int RSTEP = 128 / CPR;     // rows between a thread's chunks
+  constexpr int RSTEP = NT / CPR;      // rows between a thread's chunks
   const int lc = threadIdx.x % CPR, lr0 = threadIdx.x / CPR;
   const bool col_ok = lc < CH;
   const long hoff1 = static_cast<long>(kvh) * a.k1_head_stride + lc * 8;
@@ -321,12 +325,12 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   auto load_kv = [&](int buf, int j0) {
     bf16* kb = ks_buf + buf * BN * LD;
     bf16* vb = vs_buf + buf * BN * LD;
-    if constexpr (128 % CPR == 0) {
+    if constexpr (NT % CPR == 0) {
 #pragma unroll
       for (int r = lr0; r < BN; r += RSTEP)
         load_row(kb + r * LD + lc * 8, vb + r * LD + lc * 8, j0 + r, col_ok && j0 + r < k_end);
     } else {  // chunk count per row does not divide the CTA (head dim 72)
-      for (int i = threadIdx.x; i < BN * CPR; i += 128) {
+      for (int i = threadIdx.x; i < BN * CPR; i += NT) {
         const int r = i / CPR, c = i % CPR, j = j0 + r;
         const long hc = (c - lc) * 8;  // load_row's bases are for column lc
         bf16* kd = kb + r * LD + c * 8;
@@ -355,18 +359,19 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   if (early) load_kv(0, k_begin);
   pdl_wait();
   // ---- Q tile -> smem (zero padded), after griddepcontrol.wait ----
-  for (int i = threadIdx.x; i < BM * (DK / 8); i += 128) {
-    const int r = i / (DK / 8), c = i % (DK / 8);
+  for (int i = threadIdx.x; i < G * BM * (DK / 8); i += NT) {
+    const int hh = i / (BM * (DK / 8)), rc = i % (BM * (DK / 8));
+    const int r = rc / (DK / 8), c = rc % (DK / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (q0 + r < a.Tq && c < CH)
       v = *reinterpret_cast<const uint4*>(a.q + static_cast<long>(q0 + r) * a.q_tok_stride +
-                                          static_cast<long>(h) * a.q_head_stride + c * 8);
-    *reinterpret_cast<uint4*>(qs + r * LD + c * 8) = v;
+                                          static_cast<long>(blockIdx.y * G + hh) * a.q_head_stride + c * 8);
+    *reinterpret_cast<uint4*>(qs + (hh * BM + r) * LD + c * 8) = v;
   }
   __syncthreads();
   uint32_t qf[DK / 16][4];
   {
-    const bf16* qr = qs + (warp * 16) * LD;
+    const bf16* qr = qs + (hw * BM + wr * 16) * LD;
 #pragma unroll
     for (int kk = 0; kk < DK / 16; ++kk) {
       qf[kk][0] = *reinterpret_cast<const uint32_t*>(qr + g * LD + kk * 16 + 2 * t4);
@@ -481,11 +486,12 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     constexpr int W = HD + 2;
-    float* rec = reinterpret_cast<float*>(fsm);  // [BM][W]: o unnormalised, m, l
+    constexpr int RT = G * BM;                   // merged rows (G heads x BM queries)
+    float* rec = reinterpret_cast<float*>(fsm);  // [RT][W]: o unnormalised, m, l
     __syncthreads();                             // K/V buffers are free
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const int row = warp * 16 + g + 8 * r;
+      const int row = hw * BM + wr * 16 + g + 8 * r;
 #pragma unroll
       for (int dt = 0; dt < ND; ++dt) {
         rec[row * W + dt * 8 + 2 * t4] = o[dt][2 * r];
@@ -498,9 +504,9 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
     }
     cluster.sync();
     const int z = static_cast<int>(cluster.block_rank());
-    const int r_lo = z * BM / splits, r_hi = (z + 1) * BM / splits;
-    __shared__ float wz[BM / 2 + 1][kMaxKvSplits + 1];  // merge weights, then 1/L
-    for (int row = r_lo + threadIdx.x; row < r_hi; row += 128) {
+    const int r_lo = z * RT / splits, r_hi = (z + 1) * RT / splits;
+    __shared__ float wz[RT / 2 + 1][kMaxKvSplits + 1];  // merge weights, then 1/L
+    for (int row = r_lo + threadIdx.x; row < r_hi; row += NT) {
       float mz[kMaxKvSplits], M = -INFINITY;
 #pragma unroll
       for (int p = 0; p < kMaxKvSplits; ++p) {
@@ -517,7 +523,7 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
       wz[row - r_lo][kMaxKvSplits] = L > 0.f ? 1.0f / L : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < (r_hi - r_lo) * (HD / 2); i += 128) {
+    for (int i = threadIdx.x; i < (r_hi - r_lo) * (HD / 2); i += NT) {
       const int rr = i / (HD / 2), d = 2 * (i % (HD / 2)), row = r_lo + rr;
       float v0 = 0.f, v1 = 0.f;
 #pragma unroll
@@ -528,10 +534,10 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
           v1 = fmaf(pv.y, wz[rr][p], v1);
         }
       }
-      const int qrow = q0 + row;
+      const int qrow = q0 + row % BM, hrow = static_cast<int>(blockIdx.y) * G + row / BM;
       if (qrow < a.Tq) {
         const float inv = wz[rr][kMaxKvSplits];
-        bf16* op = a.out + static_cast<long>(qrow) * a.o_tok_stride + static_cast<long>(h) * a.o_head_stride;
+        bf16* op = a.out + static_cast<long>(qrow) * a.o_tok_stride + static_cast<long>(hrow) * a.o_head_stride;
         *reinterpret_cast<uint32_t*>(op + d) = pack_bf16x2(v0 * inv, v1 * inv);
       }
     }
@@ -551,25 +557,25 @@ __global__ void __launch_bounds__(128) flash_kernel(const FlashArgs a) {
   }
 }
 
-template <int HD>
+template <int HD, int G = 1>
 static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   using Cfg = FlashCfg<HD>;
-  const size_t smem = static_cast<size_t>(Cfg::kBM + 4 * Cfg::kBN) * Cfg::kLd * 2;
+  const size_t smem = static_cast<size_t>(G * Cfg::kBM + 4 * Cfg::kBN) * Cfg::kLd * 2;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int splits = a.kv_splits > 1 ? a.kv_splits : 1;
-  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq, splits);
+  dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq / G, splits);
   if (splits > kMaxKvSplits || (splits > 1 && a.seg_len > 0) ||
-      static_cast<size_t>(Cfg::kBM) * (HD + 2) * 4 > smem)
+      static_cast<size_t>(G * Cfg::kBM) * (HD + 2) * 4 > smem || a.hq % G || (a.hq / a.hkv) % G)
     return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(128 * G);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute la[2];
@@ -581,7 +587,7 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   la[1].val.clusterDim.z = static_cast<unsigned>(splits);
   cfg.attrs = la;
   cfg.numAttrs = splits > 1 ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, flash_kernel<HD>, a);
+  return cudaLaunchKernelEx(&cfg, flash_kernel<HD, G>, a);
 }
 
 int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms) {
@@ -606,7 +612,7 @@ cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {
     case 32: return flash_hd<32>(a, st);
     case 64: return flash_hd<64>(a, st);
     case 72: return flash_hd<72>(a, st);
-    case 128: return flash_hd<128>(a, st);
+    case 128: return a.g_pack == 2 ? flash_hd<128, 2>(a, st) : flash_hd<128>(a, st);
   }
   return cudaErrorInvalidValue;
 }

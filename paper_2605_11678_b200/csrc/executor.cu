@@ -257,6 +257,7 @@ struct ls_exec {
   long gemm_ws_floats = 0;
   int gemm_cnt_n = 0;
   int ex_kv_splits = 1;
+  int ex_g_pack = 1;  // expert flash GQA packing (query heads per CTA)
   unsigned long long* amax = nullptr;
   CUtensorMap m_patches, m_vit_ln, m_vit_attn, m_vit_fc1, m_merge_in, m_merger_mid, m_lm_norm,
       m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
@@ -599,6 +600,7 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   f.o_head_stride = d.ex_hd;
   f.kv_splits = e->ex_kv_splits;
   f.k1_ready = 1;  // the VLM cache was written before the expert runs
+  f.g_pack = e->ex_g_pack;
   f.ws = e->flash_ws;
   f.counters = e->flash_cnt;
   if (!(skip & 4)) KL(launch_flash_attention(f, e->ss));
@@ -892,7 +894,12 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       e->gemm_cnt_n = e->nsm;
       OV(gemm_ws, 4ull * e->gemm_ws_floats);
       OV(gemm_cnt, 4ull * e->gemm_cnt_n);
-      e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq, e->ctx + Te, e->nsm);
+      // GQA packing (2 query heads per CTA) measured slower in context (31.8-33.5 vs
+      // 22.7 us per expert layer): off unless LS_DIAG_EX_GPACK=2
+      e->ex_g_pack = 1;
+      if (const char* ov = std::getenv("LS_DIAG_EX_GPACK"))
+        e->ex_g_pack = (std::atoi(ov) == 2 && d.ex_hd == 128 && (d.ex_hq / d.ex_hkv) % 2 == 0) ? 2 : 1;
+      e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq / e->ex_g_pack, e->ctx + Te, e->nsm);
       if (const char* ov = std::getenv("LS_DIAG_EX_KV_SPLITS")) e->ex_kv_splits = std::atoi(ov);  // diagnostics
       if (const char* ov = std::getenv("LS_DIAG_DEC_SPLITS")) e->diag_dec_splits = std::atoi(ov);
     }

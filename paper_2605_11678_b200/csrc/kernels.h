@@ -138,6 +138,9 @@ struct FlashArgs {
   // 1: segment 1 was not written by the previous kernel (the expert reading the
   // VLM cache) -- its first K/V block is requested before griddepcontrol.wait
   int k1_ready;
+  // 2: GQA packing -- one CTA per (q tile, 2 query heads of one KV head), 8 warps;
+  // hd 128, (hq / hkv) % 2 == 0; kv_splits counts CTAs per (q tile, head pair)
+  int g_pack;
 };
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st);
 // kv_splits the launcher will use for (Tq, hq, keys) given num_sms, and the

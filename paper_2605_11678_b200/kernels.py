@@ -43,7 +43,7 @@ class FlashArgs(C.Structure):
                 ("Tq", C.c_int32), ("hq", C.c_int32), ("hkv", C.c_int32), ("hd", C.c_int32),
                 ("causal", C.c_int32), ("q_offset", C.c_int32), ("seg_len", C.c_int32),
                 ("scale", C.c_float), ("kv_splits", C.c_int32), ("ws", _vp), ("counters", _vp),
-                ("k1_ready", C.c_int32)]
+                ("k1_ready", C.c_int32), ("g_pack", C.c_int32)]
 
 
 GEMV_F32, GEMV_RESID, GEMV_SILU, GEMV_QKV, GEMV_ARGMAX = range(5)

@@ -216,7 +216,8 @@ def _attn_ref(q, k, v, mask, scale):
     return (torch.softmax(s, -1) @ vv).permute(1, 0, 2)
 
 
-def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0, kv_splits=0, k1_ready=0):
+def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0, kv_splits=0, k1_ready=0,
+           g_pack=1):
     a = K.FlashArgs(q=q.data_ptr(), q_tok_stride=q.stride(0), q_head_stride=q.stride(1),
                     k1=k1.data_ptr(), v1=v1.data_ptr(), k1_tok_stride=k1.stride(0),
                     k1_head_stride=k1.stride(1), len1=k1.shape[0],
@@ -230,6 +231,7 @@ def _flash(q, k1, v1, k2, v2, out, hq, hkv, hd, causal=0, q_offset=0, seg_len=0,
                     seg_len=seg_len, scale=1 / math.sqrt(hd))
     a.kv_splits = kv_splits  # > 1: one thread-block cluster per (q tile, head), DSMEM merge
     a.k1_ready = k1_ready    # first K/V block of segment 1 requested before griddepcontrol.wait
+    a.g_pack = g_pack        # 2: one CTA per pair of query heads of a KV head
     K.flash_attention(a)
 
 
@@ -258,8 +260,8 @@ def test_flash_vit_block_diagonal_hd72():
     _close(out, _attn_ref(q, k, v, mask, 1 / math.sqrt(hd)), rel=0, abs_=2e-2)
 
 
-@pytest.mark.parametrize("kv_splits", [0, 3, 8])
-def test_flash_two_segments_expert(kv_splits):
+@pytest.mark.parametrize("kv_splits,g_pack", [(0, 1), (3, 1), (8, 1), (0, 2), (4, 2), (8, 2)])
+def test_flash_two_segments_expert(kv_splits, g_pack):
     torch.manual_seed(10)
     Tq, L1, hq, hkv, hd = 64, 530, 32, 8, 128
     q = torch.randn(Tq, hq, hd, device=DEV).to(torch.bfloat16)
@@ -270,7 +272,7 @@ def test_flash_two_segments_expert(kv_splits):
     out = torch.empty(Tq, hq, hd, dtype=torch.bfloat16, device=DEV)
     k1v = cache_k.permute(1, 0, 2)  # strided view [pos][head][d]
     v1v = cache_v.permute(1, 0, 2)
-    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd, kv_splits=kv_splits, k1_ready=1)
+    _flash(q, k1v[:L1], v1v[:L1], k2, v2, out, hq, hkv, hd, kv_splits=kv_splits, k1_ready=1, g_pack=g_pack)
     kk = torch.cat([k1v[:L1], k2], 0)
     vv = torch.cat([v1v[:L1], v2], 0)
     mask = torch.ones(Tq, L1 + Tq, dtype=torch.bool, device=DEV)
