@@ -246,9 +246,13 @@ int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* hos
                                 const uint64_t* bytes, int32_t n);
 /* ECT-compressed host blobs (exponent-coded tiles, ect.py) of one module: the
    module is then stored compact everywhere -- DFB slots and resident blocks
-   hold blobs (resident footprint = largest blob, 256-aligned), and every EXE
-   decodes the blob before the layer's kernels.  Re-lays out the slot ring and
-   drops resident layers (call ls_exec_set_placement afterwards). */
+   hold blobs (resident footprint = largest blob, 256-aligned).  Blob layout:
+   128-byte header (magic 'ECT1', page count, section offsets, exponent window,
+   off_escmask), 12 KiB pages, raw vector tail, per-page exception offsets,
+   16-byte per-page escape masks, exception list.  Decode GEMVs and 64-token
+   GEMMs read the pages directly; multi-token-tile GEMMs expand one matrix
+   into the decode scratch first.  Re-lays out the slot ring and drops
+   resident layers (call ls_exec_set_placement afterwards). */
 int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host_ptrs,
                                const uint64_t* bytes, int32_t n);
 /* Upload resident layers for a placement mask (module order vit, lm, expert). */
