@@ -1,3 +1,10 @@
+"""Diagnostic: k-block timeline of CTA 0 of the 64-token ECT gate|up GEMM.
+Needs a variant library built from gemm_sm100.cu with clock64 stamps
+(`__device__ long long g_trace[8][128]`, TRACE(event, k-block) at: decoder
+start / empty ok / full ok / decoded / fenced, MMA dec ok / bfull ok, epilogue
+acc ok) and `extern "C" int ls_gemm_trace_read(void*)` copying g_trace out;
+run with LS_LIB_PATH pointing at it.  Results: DESIGN.md section 8b.
+"""
 import ctypes as C, sys, os
 sys.path.insert(0, os.getcwd())
 import torch
