@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAt
   }
 }
 
+int decode_attn_max_ctx() { return kDecMaxSplits * kDecChunk; }
+
 int decode_attn_splits(int n_ctx) {
   // >= 64 positions per split, <= kDecChunk: measured in context (the PDL chain
   // QKV GEMV -> attention -> O GEMV) at ctx 1045, 16 x 66 positions beat 9 x 117
@@ -198,8 +200,8 @@ template <int HD, int G>
 static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   const size_t smem = 2ull * kDecChunk * HD * 2 +
                       4ull * (G * (HD + kDecChunk) + G * HD + kDecMaxSplits + kDecMaxSplits * 2 * G);
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -207,7 +209,7 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
     e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.hkv, a.n_split);
@@ -561,12 +563,12 @@ template <int HD, int G = 1>
 static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   using Cfg = FlashCfg<HD>;
   const size_t smem = static_cast<size_t>(G * Cfg::kBM + 4 * Cfg::kBN) * Cfg::kLd * 2;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark();
   }
   const int splits = a.kv_splits > 1 ? a.kv_splits : 1;
   dim3 grid((a.Tq + Cfg::kBM - 1) / Cfg::kBM, a.hq / G, splits);

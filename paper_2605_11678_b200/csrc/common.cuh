@@ -7,6 +7,20 @@
 #include <stdint.h>
 
 #include <utility>
+#include <atomic>
+
+// cudaFuncSetAttribute applies to the CURRENT device only, so a launcher's
+// "attributes already set" flag is kept per device (bit d = done on device d).
+struct DeviceFlags {
+  std::atomic<uint64_t> bits{0};
+  static int cur() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+  }
+  bool done() const { return (bits.load(std::memory_order_acquire) >> cur()) & 1ull; }
+  void mark() { bits.fetch_or(1ull << cur(), std::memory_order_release); }
+};
 
 namespace lsb {
 

@@ -303,6 +303,7 @@ GemvPlan plan_gemv(int n, int k, int nsm) {
 }
 
 int alloc_into(ls_exec* e, void* dst_ptr, uint64_t bytes, uint64_t* counter) {
+  const uint64_t before = e->ar.used;
   char* p = e->ar.alloc(bytes ? bytes : 16);
   if (!p)
     return set_error(LS_ERR_CAP,
@@ -311,7 +312,9 @@ int alloc_into(ls_exec* e, void* dst_ptr, uint64_t bytes, uint64_t* counter) {
                      static_cast<unsigned long long>(e->ar.used),
                      static_cast<unsigned long long>(e->ar.cap));
   *static_cast<char**>(dst_ptr) = p;
-  if (counter) *counter += bytes;
+  // count what the arena actually consumed (alignment padding included), so the
+  // profile's always-resident / overhead terms match the arena exactly
+  if (counter) *counter += e->ar.used - before;
   return LS_OK;
 }
 
@@ -761,6 +764,11 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     return fail(set_error(LS_ERR_VALUE, "expert KV heads must match the LM's (joint attention)"));
   e->S = prompt_len(d);
   e->ctx = ctx_len(d);
+  if (e->ctx > decode_attn_max_ctx())
+    return fail(set_error(LS_ERR_VALUE,
+                          "context of %d tokens (prompt %d + %d decode steps) exceeds the decode "
+                          "attention limit of %d positions",
+                          e->ctx, e->S, d.decode_steps, decode_attn_max_ctx()));
   e->Tv = d.has_vit ? d.vit_images * d.vit_tokens_per_image : 0;
   e->Te = d.has_expert ? d.ex_tokens : 0;
   e->vit_ffn_pad = n_kb(d.vit_ffn) * 64 > n_mt(d.vit_ffn) * 128 ? n_kb(d.vit_ffn) * 64 : n_mt(d.vit_ffn) * 128;
@@ -1082,8 +1090,18 @@ int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host
       if (!host_ptrs[i] || bytes[i] < sizeof(EctHeader))
         return set_error(LS_ERR_VALUE, "ECT blob %d of module kind %d is missing or truncated", i, kind);
       const EctHeader* h = static_cast<const EctHeader*>(host_ptrs[i]);
-      if (h->magic != 0x31544345u || h->total != m.lay.total ||
-          h->mat_bytes != static_cast<uint64_t>(h->n_pages) * 16384ull)
+      // the kernels derive page and tail offsets from the layout: the blob must
+      // cover exactly the layout's tiled matrices (parts 0..3) and its sections
+      // must lie inside the blob
+      const uint64_t mat = m.lay.offset[3] + m.lay.bytes[3];
+      const uint64_t tail = h->total - h->mat_bytes;
+      if (h->magic != 0x31544345u || h->total != m.lay.total || h->mat_bytes != mat ||
+          h->mat_bytes != static_cast<uint64_t>(h->n_pages) * 16384ull ||
+          h->off_pages + static_cast<uint64_t>(h->n_pages) * 12288ull > bytes[i] ||
+          h->off_tail + tail > bytes[i] ||
+          h->off_excoff + 4ull * (h->n_pages + 1ull) > bytes[i] ||
+          h->off_exc + 4ull * h->n_exc > bytes[i] ||
+          (h->off_escmask && h->off_escmask + 16ull * h->n_pages > bytes[i]))
         return set_error(LS_ERR_VALUE, "ECT blob %d of module kind %d does not match the layer layout",
                          i, kind);
       worst = std::max<uint64_t>(worst, bytes[i]);
@@ -1106,28 +1124,42 @@ int ls_exec_set_placement(ls_exec* e, const uint8_t* mask, int64_t n) {
                                    static_cast<long long>(n), static_cast<long long>(total));
   CK(cudaStreamSynchronize(e->ss));
   CK(cudaStreamSynchronize(e->cs));
-  ++e->gen;
+  ++e->gen;  // invalidates any captured graph (it holds the old resident pointers)
   e->ar.used = e->mark;
+  for (auto& m : e->mods) std::fill(m.resident.begin(), m.resident.end(), nullptr);
+  // all-or-nothing: on any failure no module keeps a pointer into the rewound
+  // arena and no resident copy is left in flight -- every layer is streamed
+  auto fail = [&](int rc) {
+    cudaStreamSynchronize(e->cs);
+    for (auto& m : e->mods) std::fill(m.resident.begin(), m.resident.end(), nullptr);
+    e->ar.used = e->mark;
+    return rc;
+  };
   int64_t off = 0;
   for (auto& m : e->mods) {
     for (int l = 0; l < m.layers; ++l) {
-      m.resident[l] = nullptr;
       if (!mask[off + l]) continue;
-      if (!m.host_of(l)) return set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind);
+      if (!m.host_of(l))
+        return fail(set_error(LS_ERR_VALUE, "host layer %d of module kind %d not set", l, m.kind));
       const uint64_t foot = m.ct ? m.ct_stride : m.lay.total;
       char* p = e->ar.alloc(foot, 256);
       if (!p)
-        return set_error(LS_ERR_CAP,
-                         "resident layers exceed the emulated VRAM cap (%llu bytes used of %llu)",
-                         static_cast<unsigned long long>(e->ar.used),
-                         static_cast<unsigned long long>(e->ar.cap));
-      CK(cudaMemcpyAsync(p, m.host_of(l), m.ct ? m.ct_bytes[l] : m.lay.total, cudaMemcpyHostToDevice,
-                         e->cs));
+        return fail(set_error(LS_ERR_CAP,
+                              "resident layers exceed the emulated VRAM cap (%llu bytes used of %llu)",
+                              static_cast<unsigned long long>(e->ar.used),
+                              static_cast<unsigned long long>(e->ar.cap)));
+      cudaError_t ce = cudaMemcpyAsync(p, m.host_of(l), m.ct ? m.ct_bytes[l] : m.lay.total,
+                                       cudaMemcpyHostToDevice, e->cs);
+      if (ce != cudaSuccess)
+        return fail(set_error(LS_ERR_CUDA, "cudaMemcpyAsync (resident layer): %s",
+                              cudaGetErrorString(ce)));
       m.resident[l] = p;
     }
     off += m.layers;
   }
-  CK(cudaStreamSynchronize(e->cs));
+  cudaError_t ce = cudaStreamSynchronize(e->cs);
+  if (ce != cudaSuccess)
+    return fail(set_error(LS_ERR_CUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(ce)));
   return LS_OK;
 }
 

@@ -404,13 +404,13 @@ int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_
 template <int BN, int EPI, bool CT>
 static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
   using Cfg = GemmCfg<BN, CT>;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI, CT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark();
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);

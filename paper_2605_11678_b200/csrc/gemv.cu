@@ -321,12 +321,12 @@ static size_t gemv_smem(int n_kb) {
 
 template <int EPI, bool CT, int NW>
 static cudaError_t launch_t(const GemvArgs& a, int grid, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceFlags attr_set;
+  if (!attr_set.done()) {
     cudaError_t e = cudaFuncSetAttribute(gemv_kernel<EPI, CT, NW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.mark();
   }
   return launch_k(gemv_kernel<EPI, CT, NW>, dim3(grid), dim3(GemvShape<NW>::kThreads),
                   gemv_smem<CT>(a.n_kb), st, a);

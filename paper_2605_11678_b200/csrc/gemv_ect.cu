@@ -234,12 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a)
 
 template <int EPI>
 static cudaError_t launch_ect_t(const GemvArgs& a, int grid, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceFlags attr_set;
+  if (!attr_set.done()) {
     cudaError_t e =
         cudaFuncSetAttribute(gemv_ect_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.mark();
   }
   return launch_k(gemv_ect_kernel<EPI>, dim3(grid), dim3(kThreads), ect_smem(a.n_kb), st, a);
 }

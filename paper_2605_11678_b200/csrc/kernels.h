@@ -117,6 +117,7 @@ struct DecodeAttnArgs {
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
 // splits (one cluster of <= 16 CTAs per KV head, <= 128 positions per CTA)
 int decode_attn_splits(int n_ctx);
+int decode_attn_max_ctx();  // positions one decode-attention launch covers
 
 struct FlashArgs {
   const bf16* q;  long q_tok_stride, q_head_stride;   // q[t, h, d]

@@ -112,13 +112,19 @@ class DemandLayeringEngine:
 
     def __init__(self, cfg: M.ModelConfig = M.ALPAMAYO, *, device: int = 0,
                  vram_cap_mb: float = 16000.0, n_slots: int = 2, seed: int = 0,
-                 keep_logical: bool = False, ecf: bool = True, compact: bool = True,
+                 init_device=None, ecf: bool = True, compact: bool = True,
                  tp_world: int = 1,
                  tp_rank: int = 0, tp_id: bytes | None = None, tp_force: bool = False) -> None:
         """tp_world > 1: this engine is rank `tp_rank` of a tensor-parallel group;
         it holds and streams only its shard of every layer (model.tp_config /
         shard_layer_tensors) and all-reduces row-parallel outputs with NCCL
         (`tp_id` = the 128-byte id from `nccl_unique_id()` on rank 0).
+
+        init_device: where the seeded weight generator, tile packing and ECT
+        compression run (default: the engine's GPU).  "cpu" keeps the setup
+        off the GPU entirely (small configs: the first kernels the process
+        launches are then the executor's own).  The generator device selects
+        the random stream, so an oracle must regenerate on the same device.
 
         compact=True stores every module as ECT blobs (ect.py: exponent-coded
         tiles, lossless, 75 % of the bytes) in the host arena, the DFB slots
@@ -140,6 +146,7 @@ class DemandLayeringEngine:
         self.cfg = cfg
         self.device = device
         self.dev = torch.device("cuda", device)
+        self.init_dev = torch.device(init_device) if init_device is not None else self.dev
         self.vram_cap_mb = vram_cap_mb
         self.n_slots = n_slots
         self.seed = seed
@@ -157,7 +164,6 @@ class DemandLayeringEngine:
             _native.check(self.lib.ls_exec_set_tp(self.handle, idbuf), RuntimeError)
         self.kinds = cfg.kinds
         self.layouts = {k: M.layer_layout(cfg, k) for k in self.kinds}
-        self.logical: dict | None = {"layers": {}, "globals": {}} if keep_logical else None
         self.arenas: dict = {}
         self._placement_key = None
         self._init_globals()
@@ -170,7 +176,7 @@ class DemandLayeringEngine:
         return p.value
 
     def _init_globals(self) -> None:
-        tensors = M.global_tensors(self.cfg, self.seed, self.dev)
+        tensors = M.global_tensors(self.cfg, self.seed, self.init_dev)
         for gid, t in tensors.items():
             raw = M.global_bytes_of(gid, t)
             if gid == M.G_EMBED and self.cfg.embed_on_host:
@@ -183,8 +189,6 @@ class DemandLayeringEngine:
                 size = M.global_size(self.cfg, gid)
                 assert raw.numel() == size, (gid, raw.numel(), size)
                 _copy_to_device_ptr(self._global_ptr(gid), raw)
-            if self.logical is not None:
-                self.logical["globals"][gid] = t.float().cpu()
         torch.cuda.synchronize()
 
     def _init_layers(self) -> None:
@@ -227,13 +231,10 @@ class DemandLayeringEngine:
         torch.cuda.synchronize()
 
     def _packed_layer(self, kind: int, layer: int) -> torch.Tensor:
-        """This rank's packed (tiled, flat) bytes of one layer, on the GPU."""
-        t = M.layer_tensors(self.full_cfg, kind, layer, self.seed, self.dev)
+        """This rank's packed (tiled, flat) bytes of one layer (on init_dev)."""
+        t = M.layer_tensors(self.full_cfg, kind, layer, self.seed, self.init_dev)
         shard = M.shard_layer_tensors(self.full_cfg, kind, t, self.tp_world, self.tp_rank)
-        buf = M.pack_layer(self.cfg, kind, shard)
-        if self.logical is not None:
-            self.logical["layers"][(kind, layer)] = {k: v.float().cpu() for k, v in t.items()}
-        return buf
+        return M.pack_layer(self.cfg, kind, shard)
 
     def _blob_arena(self, key, blobs: list, setter, kind: int) -> None:
         n = len(blobs)
@@ -326,6 +327,7 @@ class DemandLayeringEngine:
                                      f"out-of-range layer index {i} (valid 0..{n - 1})")
                 mask[off + i] = 1
             off += n
+        self._placement_key = None  # a failed call leaves every layer streamed (all-or-nothing)
         _native.check(self.lib.ls_exec_set_placement(self.handle, mask, total))
         self._placement_key = key
 

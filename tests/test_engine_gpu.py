@@ -21,7 +21,7 @@ import paper_2605_11678_b200 as ls  # noqa: E402
 from paper_2605_11678_b200 import model as M  # noqa: E402
 
 if cuda_available():
-    from oracle.model_fp32 import FP32Model
+    from oracle.model_fp32 import FP32Model, OracleWeights
     from paper_2605_11678_b200.engine import DemandLayeringEngine
 
 SLACK_MS = 2e-3  # event-timestamp resolution slack
@@ -29,20 +29,20 @@ SLACK_MS = 2e-3  # event-timestamp resolution slack
 
 @pytest.fixture(scope="module")
 def tiny_lm():
-    eng = DemandLayeringEngine(M.TINY_LM, vram_cap_mb=512, n_slots=3, keep_logical=True)
+    eng = DemandLayeringEngine(M.TINY_LM, vram_cap_mb=512, n_slots=3)
     yield eng
     eng.close()
 
 
 @pytest.fixture(scope="module")
 def tiny_alp():
-    eng = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=3, keep_logical=True)
+    eng = DemandLayeringEngine(M.TINY_ALPAMAYO, vram_cap_mb=1024, n_slots=3)
     yield eng
     eng.close()
 
 
 def _check_numerics(eng, res, inputs):
-    ref = FP32Model(eng.cfg, eng.logical)
+    ref = FP32Model(eng.cfg, OracleWeights(eng.cfg, eng.seed, gen_device=eng.init_dev))
     got_tokens = res.tokens.cpu()
     tokens, logits, actions = ref.run({k: v.cpu() for k, v in inputs.items()},
                                       teacher_tokens=got_tokens[:-1])
