@@ -237,13 +237,6 @@ int ls_exec_set_tp(ls_exec* e, const uint8_t id[128]);
 int ls_exec_set_global_host(ls_exec* e, int32_t id, void* host_ptr);
 /* Pinned host buffers of every layer of one module (streamed source). */
 int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_ptrs, int32_t n);
-/* ECF-compressed host blobs of one module's layers: streamed layers of that
- * module are transferred compressed (bytes[i] each) into the tail of their
- * DFB slot and decoded on the GPU into the slot head.  Only accepted when
- * layer bytes + blob bytes fit in one slot, so the VRAM accounting is
- * unchanged (slots = slot_count x largest layer, dfbsim.py:266). */
-int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* host_ptrs,
-                                const uint64_t* bytes, int32_t n);
 /* ECT-compressed host blobs (exponent-coded tiles, ect.py) of one module: the
    module is then stored compact everywhere -- DFB slots and resident blocks
    hold blobs (resident footprint = largest blob, 256-aligned).  Blob layout:
@@ -321,8 +314,6 @@ int ls_k_gemm_ws(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, c
 int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64_t ws_floats,
                    int32_t cnt_n);
 int ls_k_decode_attention(const void* args, void* stream);
-/* Lossless exponent-coded BF16 (ECF) blob -> BF16 words (decode + exception patch). */
-int ls_k_ecf_decode(const void* blob, void* out, void* stream);
 /* Diagnostic: `grid` CTAs each stream `per_cta` bytes from src through a ring of
    `stages` x `stage_bytes` TMA bulk copies (per-SM streaming bandwidth probe). */
 int ls_probe_bulk_stream(const void* src, uint64_t per_cta, int32_t stage_bytes, int32_t stages,

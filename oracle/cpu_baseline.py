@@ -1,151 +1,181 @@
-"""ORACLE / CPU BASELINE -- test & benchmark infrastructure only.
+"""ORACLE / CPU BASELINE -- benchmark infrastructure only.
 
 The reference arm of bench.py (`--impl reference`) and the `cpu_baseline`
-object of our own bench line.  The reference (`layerswap`) has no executor: its
-hot path is a pure-Python schedule model and planner (README.md:21).
-This module times, on the box's host cores, the two CPU-side pieces of the
-path:
+object of our own bench line.  Everything here is MEASURED, nothing is
+extrapolated:
 
-  1. the model inference itself, restated in fp32 PyTorch on the host
-     (oracle/model_fp32.py) -- a BOUNDED sample: one layer of each kind
-     (ViT block over all image tokens, LM prefill over the prompt, LM decode
-     at full context, expert denoise step over the action tokens), the merger
-     and one lm-head row, extrapolated to the full Alpamayo inference as
-     sum(R * L * t_layer) + non-layer parts;
-  2. the reference's policy/predictor path (oracle/dfb_oracle.py: simulate +
-     plan + predict on a profile built from those CPU layer times).
-
-Weights are random fp32 tensors of the real shapes (timing does not depend
-on values).
+  1. `full_inference`: the whole Alpamayo-shaped inference (ViT over every
+     image token -> merger -> 36-layer LM prefill -> 21 greedy decode steps ->
+     10 Euler steps of the 36-layer expert) in fp32 PyTorch on the host cores
+     (oracle/model_fp32.py, the numeric oracle), every layer executed, each
+     timed step one complete inference.  The weights are the product's own
+     (same seeded generator, regenerated in logical form; generation and the
+     host fp32 upcast are setup, outside the timed region), so the CPU greedy
+     tokens are comparable with the GPU arm's.
+  2. `policy_path`: the reference's own policy / predictor path -- `simulate`,
+     `plan_for_budget`, `sweep(vlm, 0..35)`, `predict` + `validate` -- on the
+     measured B200 profile (fixtures/b200_alpamayo.json), pinned to ONE core
+     (the reference is single-threaded, dfbsim.py:43-44), run by the real
+     reference package when it is installed (baseline/_ref, `pip install
+     --target`) and otherwise by the oracle restatement (oracle/dfb_oracle.py),
+     with the native C++ implementation's timings of the same calls beside it.
 """
 from __future__ import annotations
 
 import os
+import statistics
+import sys
 import time
+from pathlib import Path
 
 import torch
 
-from oracle import dfb_oracle as O
-from oracle.model_fp32 import (G_EX_FINAL_NORM, G_EX_OUT_B, G_EX_OUT_W, G_FINAL_NORM, G_LM_HEAD,
-                               G_MERGE_FC1, G_MERGE_FC1_B, G_MERGE_FC2, G_MERGE_FC2_B,
-                               G_MERGE_LN_B, G_MERGE_LN_W, G_ROPE, KIND_EXPERT, KIND_LM, KIND_VIT,
-                               FP32Model)
+ROOT = Path(__file__).resolve().parent.parent
+B200_PROFILE = ROOT / "paper_2605_11678_b200" / "fixtures" / "b200_alpamayo.json"
 
 
-def _rand(*shape, std=0.02, mean=0.0):
-    return torch.randn(*shape) * std + mean
-
-
-def _layer_weights(cfg, kind):
-    if kind == KIND_VIT:
-        d, h, hd, f = cfg.vit_d, cfg.vit_heads, cfg.vit_hd, cfg.vit_ffn
-        return {"qkv": _rand(3 * h * hd, d), "proj": _rand(d, h * hd), "fc1": _rand(f, d),
-                "fc2": _rand(d, f), "qkv_b": _rand(3 * h * hd), "proj_b": _rand(d),
-                "fc1_b": _rand(f), "fc2_b": _rand(d), "ln1_w": _rand(d, mean=1.0),
-                "ln1_b": _rand(d), "ln2_w": _rand(d, mean=1.0), "ln2_b": _rand(d)}
-    if kind == KIND_LM:
-        d, hq, hkv, hd, f = cfg.lm_d, cfg.lm_hq, cfg.lm_hkv, cfg.lm_hd, cfg.lm_ffn
-    else:
-        d, hq, hkv, hd, f = cfg.ex_d, cfg.ex_hq, cfg.ex_hkv, cfg.ex_hd, cfg.ex_ffn
-    return {"q": _rand(hq * hd, d), "k": _rand(hkv * hd, d), "v": _rand(hkv * hd, d),
-            "o": _rand(d, hq * hd), "gate": _rand(f, d), "up": _rand(f, d), "down": _rand(d, f),
-            "attn_norm": _rand(d, mean=1.0), "mlp_norm": _rand(d, mean=1.0),
-            "q_norm": _rand(hd, mean=1.0), "k_norm": _rand(hd, mean=1.0)}
-
-
-def _timed(fn, reps):
-    best = float("inf")
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        fn()
-        best = min(best, time.perf_counter() - t0)
-    return best
-
-
+# ------------------------------------------------------------ inference ------
 @torch.no_grad()
-def estimate(cfg, threads: int | None = None, budget_mb: float = 16000.0) -> dict:
-    """Extrapolated CPU latency (s) of one full inference + the sample used."""
+def full_inference(cfg, steps: int = 1, warmup: int = 0, threads: int | None = None,
+                   budget_s: float = 150.0, seed: int = 0) -> dict:
+    """Time complete fp32 inferences on the host.  Runs `warmup` untimed
+    inferences, then timed ones until `steps` are done or the timed total
+    would exceed `budget_s` (at least one).  Returns per-step seconds."""
+    from oracle.model_fp32 import FP32Model, OracleWeights
+    from paper_2605_11678_b200.model import synthetic_inputs
+
     threads = threads or os.cpu_count() or 1
     torch.set_num_threads(threads)
-    torch.manual_seed(0)
-    t_start = time.perf_counter()
-    S = cfg.prompt_len
-    ctx = S + cfg.decode_steps
-    rows = ctx + 1 + (cfg.ex_tokens if cfg.has_expert else 0)
-    inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, cfg.lm_hd, 2, dtype=torch.float64) / cfg.lm_hd))
-    ang = torch.arange(rows, dtype=torch.float64)[:, None] * inv[None, :]
-    g = {G_ROPE: torch.stack([ang.cos(), ang.sin()], -1).float(),
-         G_FINAL_NORM: _rand(cfg.lm_d, mean=1.0), G_LM_HEAD: _rand(cfg.vocab, cfg.lm_d)}
-    layers = {(KIND_LM, 0): _layer_weights(cfg, KIND_LM)}
-    if cfg.has_vit:
-        layers[(KIND_VIT, 0)] = _layer_weights(cfg, KIND_VIT)
-        md = 4 * cfg.vit_d
-        g.update({G_MERGE_LN_W: _rand(cfg.vit_d, mean=1.0), G_MERGE_LN_B: _rand(cfg.vit_d),
-                  G_MERGE_FC1: _rand(md, md), G_MERGE_FC1_B: _rand(md),
-                  G_MERGE_FC2: _rand(cfg.lm_d, md), G_MERGE_FC2_B: _rand(cfg.lm_d)})
-    if cfg.has_expert:
-        layers[(KIND_EXPERT, 0)] = _layer_weights(cfg, KIND_EXPERT)
-        g.update({G_EX_FINAL_NORM: _rand(cfg.ex_d, mean=1.0),
-                  G_EX_OUT_W: _rand(cfg.action_dim, cfg.ex_d), G_EX_OUT_B: _rand(cfg.action_dim)})
-    m = FP32Model(cfg, {"globals": g, "layers": layers})
-    t = {}
-    h = _rand(S, cfg.lm_d, std=1.0)
-    pos = torch.arange(S)
-    t["lm_prefill_layer"] = _timed(lambda: m._layer(KIND_LM, 0, h, pos), 2)
-    kv = (_rand(ctx - 1, cfg.lm_hkv, cfg.lm_hd, std=1.0), _rand(ctx - 1, cfg.lm_hkv, cfg.lm_hd, std=1.0))
-    x1 = _rand(1, cfg.lm_d, std=1.0)
-    t["lm_decode_layer"] = _timed(lambda: m._layer(KIND_LM, 0, x1, torch.tensor([ctx - 1]),
-                                                   kv_prefix=kv), 3)
-    t["lm_head_row"] = _timed(lambda: m._head(x1[0]), 3)
-    est = (cfg.lm_layers * t["lm_prefill_layer"] + cfg.decode_steps * cfg.lm_layers * t["lm_decode_layer"]
-           + (cfg.decode_steps + 1) * t["lm_head_row"])
-    if cfg.has_vit:
-        Tv = cfg.vit_images * cfg.vit_tokens_per_image
-        hv = _rand(Tv, cfg.vit_d, std=1.0)
-        mask = m.vit_mask(Tv)
-        t["vit_layer"] = _timed(lambda: m.vit_layer(0, hv, mask), 2)
-        t["merger"] = _timed(lambda: m.merge(hv), 1)
-        est += cfg.vit_layers * t["vit_layer"] + t["merger"]
-    if cfg.has_expert:
-        xe = _rand(cfg.ex_tokens, cfg.ex_d, std=1.0)
-        kvp = (kv[0][:ctx - 1], kv[1][:ctx - 1])
-        pe = torch.arange(ctx, ctx + cfg.ex_tokens)
-        t["expert_layer"] = _timed(lambda: m._layer(KIND_EXPERT, 0, xe, pe, kv_prefix=kvp,
-                                                    causal=False), 3)
-        est += cfg.euler_steps * cfg.ex_layers * t["expert_layer"]
-    # the reference's policy path on a CPU-cost profile (schedule model + plan + predict)
-    doc = _cpu_profile_doc(cfg, t, budget_mb)
+    gen = "cuda" if torch.cuda.is_available() else "cpu"
     t0 = time.perf_counter()
-    placement, _ = O.plan(doc, budget_mb)
-    _, sim_total = O.schedule(doc, placement)
-    vlm = next(mm for mm in doc["modules"] if mm["name"] == "vlm")
-    O.predict(O.intercept(doc)[0], O.slope(vlm), range(0, cfg.lm_layers))
-    t["policy_oracle_s"] = time.perf_counter() - t0
-    est += t["policy_oracle_s"]
-    sample = ", ".join(f"{k}={v * 1e3:.1f}ms" for k, v in t.items())
-    return {"value": est, "unit": "s", "cores": threads, "kind": "port",
-            "sample": (f"fp32 torch on {threads} host threads: one layer of each kind timed "
-                       f"({sample}); extrapolated as sum(R*L*t_layer) over the "
-                       f"{cfg.name} inference + reference policy path (dfb_oracle plan/simulate/"
-                       f"predict)"),
-            "sample_wall_s": time.perf_counter() - t_start, "per_layer_s": t}
+    W = OracleWeights(cfg, seed, gen_device=gen, device="cpu", store="fp32")
+    W.materialize()
+    setup_s = time.perf_counter() - t0
+    model = FP32Model(cfg, W)
+    inputs = synthetic_inputs(cfg, 0)
+    for _ in range(warmup):
+        model.run(inputs)
+    times, tokens = [], None
+    while len(times) < max(1, steps):
+        t = time.perf_counter()
+        tokens, _, _ = model.run(inputs)
+        times.append(time.perf_counter() - t)
+        if sum(times) + statistics.fmean(times) > budget_s:
+            break
+    del model, W
+    return {"step_s": times, "value": statistics.fmean(times), "cores": threads,
+            "setup_s": setup_s, "tokens": tokens.tolist(), "weights_generated_on": gen,
+            "sample": (f"{len(times)} complete fp32 inference(s) of {cfg.name} on {threads} host "
+                       f"threads (torch {torch.__version__}), every layer executed: ViT "
+                       f"{cfg.vit_layers if cfg.has_vit else 0} x {cfg.vit_images * cfg.vit_tokens_per_image if cfg.has_vit else 0} tokens, "
+                       f"LM {cfg.lm_layers} layers prefill {cfg.prompt_len} + {cfg.decode_steps} "
+                       f"greedy decode steps, expert {cfg.ex_layers if cfg.has_expert else 0} layers x "
+                       f"{cfg.euler_steps if cfg.has_expert else 0} Euler steps; no extrapolation")}
 
 
-def _cpu_profile_doc(cfg, t, budget_mb):
-    mods = []
-    lm_mb = 2 * (4 * cfg.lm_d * cfg.lm_d + 3 * cfg.lm_d * cfg.lm_ffn) / 2 ** 20
-    if cfg.has_vit:
-        mods.append({"name": "vit", "layers": cfg.vit_layers, "layer_mem_mb": 29.1,
-                     "phases": [{"name": "encode", "repetitions": 1, "dma_ms": 1e-3,
-                                 "exe_ms": t["vit_layer"] * 1e3}]})
-    mods.append({"name": "vlm", "layers": cfg.lm_layers, "layer_mem_mb": lm_mb,
-                 "phases": [{"name": "prefill", "repetitions": 1, "dma_ms": 1e-3,
-                             "exe_ms": t["lm_prefill_layer"] * 1e3},
-                            {"name": "decode", "repetitions": cfg.decode_steps, "dma_ms": 1e-3,
-                             "exe_ms": t["lm_decode_layer"] * 1e3}]})
-    if cfg.has_expert:
-        mods.append({"name": "expert", "layers": cfg.ex_layers, "layer_mem_mb": 120.8,
-                     "phases": [{"name": "denoise", "repetitions": cfg.euler_steps, "dma_ms": 1e-3,
-                                 "exe_ms": t["expert_layer"] * 1e3}]})
-    return {"hardware": {"name": "cpu", "vram_mb": budget_mb, "h2d_gbps": 0.0, "overhead_mb": 0.0},
-            "always_resident_mb": 0.0, "modules": mods}
+# ---------------------------------------------------------- policy path ------
+def _time(fn, reps: int) -> dict:
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t)
+    return {"min_ms": min(ts) * 1e3, "median_ms": statistics.median(ts) * 1e3, "reps": reps}
+
+
+def _reference_pkg():
+    """The installed reference (baseline/_ref), else None."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "layerswap" / "__init__.py").exists():
+        if str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        try:
+            import layerswap
+            if Path(layerswap.__file__).resolve().is_relative_to(ref.resolve()):
+                return layerswap
+        except Exception:
+            return None
+    return None
+
+
+def _calls(pkg, prof, budget_mb: float):
+    """The four policy-path calls on one package with the reference API
+    (the reference `layerswap` or this repo's native-backed mirror)."""
+    vlm = next(m for m in prof.modules if m.name == "vlm")
+    ks = list(range(0, vlm.layers))
+    cfg = pkg.SimConfig()
+
+    def sweep():
+        return pkg.sweep(prof, "vlm", ks, cfg)
+
+    pts = sweep()
+    measured = [(p.k, p.simulated_total_ms / 1e3) for p in pts]
+
+    def validate():
+        preds = pkg.predict(prof.calibration_total_s, pkg.slope_from_profile(vlm), ks)
+        return pkg.validate(preds, measured)
+
+    plan = pkg.plan_for_budget(prof, budget_mb, cfg, include_simulated=True)
+    return {
+        "simulate_full_offload": lambda: pkg.simulate(prof, pkg.Placement.empty(), cfg),
+        "simulate_plan": lambda: pkg.simulate(prof, plan.placement, cfg),
+        "simulated_total_plan": lambda: pkg.simulated_total(prof, plan.placement, cfg),
+        "plan_for_budget": lambda: pkg.plan_for_budget(prof, budget_mb, cfg, include_simulated=True),
+        "sweep_vlm_0_35": sweep,
+        "predict_validate": validate,
+    }, plan
+
+
+def policy_path(profile_path: Path = B200_PROFILE, budget_mb: float = 16000.0,
+                reps: int = 20) -> dict:
+    """Reference policy path on one core, with the native implementation beside it."""
+    import paper_2605_11678_b200 as native
+
+    ref = _reference_pkg()
+    kind = "reference" if ref is not None else "port"
+    try:
+        affinity = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(affinity)})
+        pinned = True
+    except (AttributeError, OSError):
+        affinity, pinned = None, False
+    try:
+        out = {"kind": kind, "cores": 1, "pinned_single_core": pinned, "nproc": os.cpu_count(),
+               "profile": str(Path(profile_path).relative_to(ROOT)), "budget_mb": budget_mb,
+               "calls": {}}
+        if ref is not None:
+            prof = ref.load_profile(profile_path)
+            calls, plan = _calls(ref, prof, budget_mb)
+            ref_plan = {m: sorted(v) for m, v in plan.placement.resident.items()}
+            out["reference_plan_counts"] = {m: len(v) for m, v in ref_plan.items()}
+            for name, fn in calls.items():
+                out["calls"][name] = {"reference": _time(fn, max(3, reps // 4) if "sweep" in name
+                                                         else reps)}
+        else:
+            from oracle import dfb_oracle as O
+            import json
+            doc = json.loads(Path(profile_path).read_text())
+            ks = range(0, 36)
+            calls = {"simulate_full_offload": lambda: O.schedule(doc, {}),
+                     "plan_for_budget": lambda: O.plan(doc, budget_mb),
+                     "sweep_vlm_0_35": lambda: O.sweep(doc, "vlm", ks)}
+            for name, fn in calls.items():
+                out["calls"][name] = {"reference": _time(fn, reps)}
+        nprof = native.load_profile(profile_path)
+        ncalls, nplan = _calls(native, nprof, budget_mb)
+        native_plan = {m: sorted(v) for m, v in nplan.placement.resident.items()}
+        out["native_plan_counts"] = {m: len(v) for m, v in native_plan.items()}
+        if ref is not None:
+            out["plans_identical"] = native_plan == ref_plan
+        for name, fn in ncalls.items():
+            if name in out["calls"]:
+                out["calls"][name]["native"] = _time(fn, reps)
+                r, n = out["calls"][name]["reference"], out["calls"][name]["native"]
+                n["speedup_vs_reference"] = r["median_ms"] / max(n["median_ms"], 1e-9)
+        out["reference_total_ms"] = sum(c["reference"]["median_ms"] for c in out["calls"].values())
+        out["native_total_ms"] = sum(c.get("native", {}).get("median_ms", 0.0)
+                                     for c in out["calls"].values())
+        return out
+    finally:
+        if pinned and affinity is not None:
+            os.sched_setaffinity(0, affinity)

@@ -119,14 +119,6 @@ int ls_probe_bulk_stream(const void* src, uint64_t per_cta, int32_t stage_bytes,
                  "ls_probe_bulk_stream");
 }
 
-int ls_k_ecf_decode(const void* blob, void* out, void* stream) {
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  return cuda_rc(launch_ecf_decode(static_cast<const uint8_t*>(blob), out, nsm,
-                                   static_cast<cudaStream_t>(stream)),
-                 "ls_k_ecf_decode");
-}
-
 int ls_k_ect_decode(const void* blob, void* out, void* stream) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);

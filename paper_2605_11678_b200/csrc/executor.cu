@@ -69,6 +69,8 @@ namespace {
 struct NcclApi {
   ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
   ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
@@ -87,9 +89,11 @@ NcclApi& nccl_api() {
       api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
       api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
       api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
       api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
       api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy &&
+      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.all_gather &&
+               api.comm_destroy &&
                api.error_string;
     }
   }
@@ -146,13 +150,20 @@ int vis_tokens(const ls_dims& d) {
 int prompt_len(const ls_dims& d) { return d.prompt_prefix + vis_tokens(d) + d.prompt_suffix; }
 int ctx_len(const ls_dims& d) { return prompt_len(d) + d.decode_steps; }
 int rope_rows(const ls_dims& d) { return ctx_len(d) + 1 + (d.has_expert ? d.ex_tokens : 0); }
+// lm-head rows this rank holds: vocab-parallel under tensor parallelism (rank r
+// owns rows [r*head_rows, (r+1)*head_rows) of the vocabulary, zero padded)
+int head_rows(const ls_dims& d) {
+  return d.tp_world > 1 ? (d.vocab + d.tp_world - 1) / d.tp_world : d.vocab;
+}
+int head_row0(const ls_dims& d) { return d.tp_world > 1 ? d.tp_rank * head_rows(d) : 0; }
+int head_valid(const ls_dims& d) { return std::min(head_rows(d), d.vocab - head_row0(d)); }
 
 uint64_t global_bytes(const ls_dims& d, int id) {
   const bool v = d.has_vit, x = d.has_expert;
   const uint64_t vd = d.vit_d, md = 4ull * d.vit_d;
   switch (id) {
     case 0: return d.embed_on_host ? 0 : 2ull * d.vocab * d.lm_d;  // embed (row-major)
-    case 1: return tiled_bytes(d.vocab, d.lm_d);                  // lm_head
+    case 1: return tiled_bytes(head_rows(d), d.lm_d);             // lm_head (this rank's rows)
     case 2: return 2ull * d.lm_d;                                 // final norm
     case 3: return 8ull * rope_rows(d) * (d.lm_hd / 2);           // rope (cos, sin)
     case 4: return v ? tiled_bytes(d.vit_d, d.vit_patch_dim) : 0; // patch embed
@@ -205,9 +216,6 @@ struct Module {
   std::vector<const char*> host;
   std::vector<char*> resident;  // nullptr: streamed
   std::vector<int> phase_reps;
-  bool ecf = false;                 // stream ECF-compressed blobs
-  std::vector<const char*> host_ecf;
-  std::vector<uint64_t> ecf_bytes;
   // ECT (exponent-coded tiles): the module lives in compact form everywhere --
   // host arena, DFB slots and resident blocks hold ECT blobs; EXE decodes
   // (or the decode GEMV reads pages directly)
@@ -263,13 +271,12 @@ struct ls_exec {
       m_lm_attn, m_lm_mlp, m_ex_norm, m_ex_attn, m_ex_mlp;
   GemvPlan gp_qkv{}, gp_o{}, gp_gu{}, gp_down{}, gp_head{}, gp_t1{}, gp_t2{};
   bool use_pdl = true, pdl_ok = false;
-  // tensor parallelism: row-parallel outputs go to tp_buf, are summed across
-  // ranks by NCCL on the compute stream, then added into the residual stream
+  // tensor parallelism: row-parallel outputs are summed in place in the
+  // residual stream by NCCL on the compute stream (resid_gemm / resid_gemv);
+  // the lm-head is vocab-parallel (argmax key MAX-reduced across ranks)
   int tp_world = 1, tp_rank = 0;
   bool tp_on = false;
   ncclComm_t comm = nullptr;
-  float* tp_buf = nullptr;
-  uint64_t tp_buf_elems = 0;
   int64_t launches = 0, h2d_copies = 0;
   double enqueue_us = 0.0;  // host time to enqueue the last run (before its final sync)
   // Untimed runs are captured once into a CUDA graph (both streams, events,
@@ -425,31 +432,34 @@ FlashArgs flash_base(int Tq, int hq, int hkv, int hd) {
   } while (0)
 
 // Row-parallel projections (o-proj, down-proj, ViT proj / fc2) into the fp32
-// residual stream dst[T x n]: the fused RESID epilogue on one GPU; under tensor
-// parallelism the partial product goes to tp_buf, is summed across ranks by
-// NCCL on the compute stream, and is then added.
-int tp_reduce_add(ls_exec* e, float* dst, long count) {
+// residual stream dst[T x n]: the fused RESID epilogue on one GPU.  Under tensor
+// parallelism every rank holds the same residual; rank 0 writes residual +
+// its partial product (the same RESID epilogue), every other rank overwrites
+// its copy with its bare partial, and one in-place NCCL all-reduce (fp32 sum)
+// over dst leaves residual + sum of partials on every rank -- no staging
+// buffer and no separate add kernel.  At world size 1 this is the fused path
+// exactly (an all-reduce over one rank is the identity).
+int tp_allreduce_inplace(ls_exec* e, float* dst, long count) {
   NcclApi& api = nccl_api();
-  ncclResult_t r = api.all_reduce(e->tp_buf, e->tp_buf, static_cast<size_t>(count), ncclFloat32,
-                                  ncclSum, e->comm, e->ss);
+  ncclResult_t r = api.all_reduce(dst, dst, static_cast<size_t>(count), ncclFloat32, ncclSum,
+                                  e->comm, e->ss);
   if (r != ncclSuccess) return set_error(LS_ERR_NCCL, "ncclAllReduce: %s", api.error_string(r));
-  e->pdl_ok = false;
-  KL(launch_add_f32(dst, e->tp_buf, count, e->ss));
+  e->pdl_ok = false;  // no programmatic launch edge across the NCCL kernel
   return LS_OK;
 }
 
 int resid_gemm(ls_exec* e, const char* w, int n, int k, int T, const CUtensorMap& map, float* dst,
                const void* bias_bf16 = nullptr, const char* ct_blob = nullptr, int ct_page0 = 0) {
-  if (!e->tp_on) return gemm(e, GEMM_RESID_F32, w, n, k, T, map, dst, n, bias_bf16, -1, ct_blob, ct_page0);
-  RC(gemm(e, GEMM_F32, w, n, k, T, map, e->tp_buf, n, bias_bf16, -1, ct_blob, ct_page0));
-  return tp_reduce_add(e, dst, static_cast<long>(T) * n);
+  const int epi = (!e->tp_on || e->tp_rank == 0) ? GEMM_RESID_F32 : GEMM_F32;
+  RC(gemm(e, epi, w, n, k, T, map, dst, n, bias_bf16, -1, ct_blob, ct_page0));
+  return e->tp_on ? tp_allreduce_inplace(e, dst, static_cast<long>(T) * n) : LS_OK;
 }
 
 int resid_gemv(ls_exec* e, const GemvPlan& p, const char* w, const float* x, float* dst,
                const char* ct_blob = nullptr, int ct_page0 = 0) {
-  if (!e->tp_on) return gemv(e, GEMV_RESID, p, w, x, dst, nullptr, nullptr, -1, nullptr, ct_blob, ct_page0);
-  RC(gemv(e, GEMV_F32, p, w, x, e->tp_buf, nullptr, nullptr, -1, nullptr, ct_blob, ct_page0));
-  return tp_reduce_add(e, dst, p.n);
+  const int epi = (!e->tp_on || e->tp_rank == 0) ? GEMV_RESID : GEMV_F32;
+  RC(gemv(e, epi, p, w, x, dst, nullptr, nullptr, -1, nullptr, ct_blob, ct_page0));
+  return e->tp_on ? tp_allreduce_inplace(e, dst, p.n) : LS_OK;
 }
 
 int vit_layer(ls_exec* e, const char* w, const ls_layer_layout& L, const CtView& ct = CtView()) {
@@ -662,7 +672,24 @@ int post_invocation(ls_exec* e, int kind, int phase, int inv, const ls_run_io* i
   } else if (kind == LS_KIND_LM) {
     const int step = phase == 0 ? 0 : inv + 1;
     const float* x = phase == 0 ? e->lm_h + static_cast<long>(e->S - 1) * d.lm_d : e->dec_h;
-    RC(gemv(e, GEMV_ARGMAX, e->gp_head, e->g[1], x, e->logits, e->g[2]));
+    // vocab-parallel under TP: this rank scores its rows, its packed argmax key
+    // carries the GLOBAL row index (GemvArgs.key_row0), and a MAX all-reduce of
+    // the 8-byte key picks the global winner (ties -> lowest index, as on one GPU)
+    GemvArgs head{};
+    head.key_row0 = head_row0(d);
+    RC(gemv(e, GEMV_ARGMAX, e->gp_head, e->g[1], x, e->logits + head_row0(d), e->g[2], nullptr,
+            head_valid(d), &head));
+    if (e->tp_on) {
+      NcclApi& api = nccl_api();
+      ncclResult_t r = api.all_reduce(e->amax, e->amax, 1, ncclUint64, ncclMax, e->comm, e->ss);
+      if (r != ncclSuccess) return set_error(LS_ERR_NCCL, "ncclAllReduce(argmax): %s", api.error_string(r));
+      if (io->logits_out) {  // tests: gather every rank's logits slice in place
+        r = api.all_gather(e->logits + head_row0(d), e->logits, static_cast<size_t>(head_rows(d)),
+                           ncclFloat32, e->comm, e->ss);
+        if (r != ncclSuccess) return set_error(LS_ERR_NCCL, "ncclAllGather(logits): %s", api.error_string(r));
+      }
+      e->pdl_ok = false;
+    }
     KL(launch_argmax_to_token(e->amax, e->token, e->hist, step, e->amax, e->ss));
     if (io->logits_out)
       SSOP(cudaMemcpyAsync(io->logits_out + static_cast<long>(step) * d.vocab, e->logits,
@@ -704,19 +731,6 @@ int finalize_layout(ls_exec* e) {
     if (m.ct && e->ct_fused)
       for (int i = 0; i < 4; ++i) scratch = std::max(scratch, align_up(m.lay.bytes[i], 256));
     std::fill(m.resident.begin(), m.resident.end(), nullptr);
-  }
-  for (auto& m : e->mods) {
-    if (!m.ecf || m.ct) continue;
-    uint64_t worst = 0;
-    for (uint64_t b : m.ecf_bytes) worst = std::max(worst, b);
-    // the ECF decoder writes whole 1024-word units: up to 2046 bytes past the layer
-    if (align_up(m.lay.total + 2048, 256) + worst + 256 > e->slot_bytes)
-      return set_error(LS_ERR_VALUE,
-                       "compressed staging does not fit in a DFB slot (layer %llu + blob %llu > "
-                       "slot %llu bytes)",
-                       static_cast<unsigned long long>(m.lay.total),
-                       static_cast<unsigned long long>(worst),
-                       static_cast<unsigned long long>(e->slot_bytes));
   }
   for (int s = 0; s < e->n_slots; ++s)
     if (int rc = alloc_into(e, &e->slots[s], e->slot_bytes, &e->bytes_slots)) return rc;
@@ -839,7 +853,8 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     OV(dec_q, 4ull * AH);
     OV(dec_attn, 4ull * AH);
     OV(dec_mlp, 4ull * d.lm_ffn);
-    OV(logits, 4ull * d.vocab);
+    OV(logits, 4ull * std::max<uint64_t>(d.vocab, static_cast<uint64_t>(head_rows(d)) *
+                                                  std::max(1, d.tp_world)));
     OV(amax, 16);
     OV(token, 16);
     OV(hist, 4ull * (d.decode_steps + 1));
@@ -855,7 +870,7 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     e->gp_o = plan_gemv(d.lm_d, AH, gs[1]);
     e->gp_gu = plan_gemv(2 * d.lm_ffn, d.lm_d, gs[2]);
     e->gp_down = plan_gemv(d.lm_d, d.lm_ffn, gs[3]);
-    e->gp_head = plan_gemv(d.vocab, d.lm_d, e->nsm);
+    e->gp_head = plan_gemv(head_rows(d), d.lm_d, e->nsm);
     std::vector<GemvPlan> plans = {e->gp_qkv, e->gp_o, e->gp_gu, e->gp_down, e->gp_head};
     if (d.has_expert) {
       e->gp_t1 = plan_gemv(d.ex_d, d.time_dim, e->nsm);
@@ -915,14 +930,6 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
     e->tp_world = std::max(1, d.tp_world);
     e->tp_rank = d.tp_rank;
     e->tp_on = e->tp_world > 1 || d.tp_force;
-    if (e->tp_on) {
-      uint64_t m1 = std::max<uint64_t>(static_cast<uint64_t>(S) * d.lm_d,
-                                       static_cast<uint64_t>(Tv) * d.vit_d);
-      uint64_t m2 = std::max<uint64_t>(static_cast<uint64_t>(Te) * d.ex_d,
-                                       static_cast<uint64_t>(d.lm_d));
-      e->tp_buf_elems = std::max(m1, m2);
-      OV(tp_buf, 4ull * e->tp_buf_elems);
-    }
     uint64_t scratch = 0, alias_off = 0;
     for (int si = 0; si < 3; ++si) {
       uint64_t sz = 0;
@@ -1055,29 +1062,6 @@ int ls_exec_set_host_layers(ls_exec* e, int32_t kind, const void* const* host_pt
   return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
 }
 
-int ls_exec_set_host_layers_ecf(ls_exec* e, int32_t kind, const void* const* host_ptrs,
-                                const uint64_t* bytes, int32_t n) {
-  for (auto& m : e->mods) {
-    if (m.kind != kind) continue;
-    if (n != m.layers) return set_error(LS_ERR_VALUE, "expected %d host layers, got %d", m.layers, n);
-    if (m.ct) return set_error(LS_ERR_VALUE, "module kind %d is stored as ECT; ECF staging does not apply", kind);
-    m.host_ecf.assign(n, nullptr);
-    m.ecf_bytes.assign(n, 0);
-    for (int i = 0; i < n; ++i) {
-      m.host_ecf[i] = static_cast<const char*>(host_ptrs[i]);
-      m.ecf_bytes[i] = bytes[i];
-    }
-    m.ecf = true;
-    if (int rc = finalize_layout(e)) {
-      m.ecf = false;
-      finalize_layout(e);
-      return rc;
-    }
-    return LS_OK;
-  }
-  return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
-}
-
 int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host_ptrs,
                                const uint64_t* bytes, int32_t n) {
   for (auto& m : e->mods) {
@@ -1111,7 +1095,6 @@ int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host
     m.ct_bytes.assign(bytes, bytes + n);
     m.ct_stride = align_up(worst, 256);
     m.ct = true;
-    m.ecf = false;
     return finalize_layout(e);
   }
   return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
@@ -1242,8 +1225,8 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
   const bool blind = opts->blind_offload != 0;
   if (blind)
     for (auto& m : e->mods)
-      if (m.ct || m.ecf) return set_error(LS_ERR_VALUE, "blind offload runs plain (non-compact, non-ECF) layers only");
-  const bool graph = e->use_graph && !timing && !e->tp_on && !blind;
+      if (m.ct) return set_error(LS_ERR_VALUE, "blind offload runs plain (non-compact) layers only");
+  const bool graph = e->use_graph && !timing && !blind;  // NCCL calls are capturable
   const uint64_t key[12] = {reinterpret_cast<uint64_t>(io->patches), reinterpret_cast<uint64_t>(io->text_ids),
                             reinterpret_cast<uint64_t>(io->noise), reinterpret_cast<uint64_t>(io->tokens_out),
                             reinterpret_cast<uint64_t>(io->actions_out), reinterpret_cast<uint64_t>(io->logits_out),
@@ -1289,7 +1272,6 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
         for (int l = 0; l < m.layers; ++l) {
           const char* w = m.resident[l];
           int slot = -1, dma0 = -1, dma1 = -1;
-          const uint8_t* ecf_src = nullptr;
           if (!w) {
             slot = sseq++ % nsl;
             if (slot_used[slot]) CK(cudaStreamWaitEvent(e->cs, e->comp_done[slot], 0));
@@ -1298,10 +1280,8 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
               CK(cudaStreamWaitEvent(e->cs, e->inv_done, 0));
               pending_barrier = false;
             }
-            // ECF: blob lands in the slot's tail, decoded into its head on the compute stream
-            const uint64_t nbytes = m.ct ? m.ct_bytes[l] : m.ecf ? m.ecf_bytes[l] : m.lay.total;
-            char* dst = m.ecf ? e->slots[slot] + ((e->slot_bytes - nbytes) & ~uint64_t(255))
-                              : e->slots[slot];
+            const uint64_t nbytes = m.ct ? m.ct_bytes[l] : m.lay.total;
+            char* dst = e->slots[slot];
             if (timing) dma0 = tick(e->cs);
             if (blind) {
               // the layer's compute stream is idle (device-wide sync after every layer);
@@ -1312,7 +1292,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
                 CK(cudaStreamSynchronize(e->cs));
               }
             } else {
-            CK(cudaMemcpyAsync(dst, m.ct ? m.host_ct[l] : m.ecf ? m.host_ecf[l] : m.host[l], nbytes,
+            CK(cudaMemcpyAsync(dst, m.ct ? m.host_ct[l] : m.host[l], nbytes,
                                cudaMemcpyHostToDevice, e->cs));
             }
             ++e->h2d_copies;
@@ -1321,16 +1301,8 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
             CK(cudaEventRecord(e->dma_done[slot], e->cs));
             SSOP(cudaStreamWaitEvent(e->ss, e->dma_done[slot], 0));
             w = e->slots[slot];
-            if (m.ecf) ecf_src = reinterpret_cast<const uint8_t*>(dst);
           }
           int x0 = timing ? tick(e->ss) : -1;
-          if (ecf_src) {
-            KL(launch_ecf_decode(ecf_src, const_cast<char*>(w), e->nsm, e->ss));
-            ++e->launches;  // decode + exception patch
-            // the layer's kernels request weights before their pdl_wait: they must
-            // not start before the decoded layer is complete
-            e->pdl_ok = false;
-          }
           CtView ct;
           if (m.ct && e->ct_fused) {
             ct = CtView(w, m.lay);  // GEMV / GEMM kernels read the blob's pages directly

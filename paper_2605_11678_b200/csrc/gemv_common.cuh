@@ -122,7 +122,7 @@ __device__ void gemv_epilogue(const GemvArgs& a, int mt, const float* red, int t
     unsigned long long key = 0ull;
     if (row < a.n_valid) {
       a.out[row] = y;
-      key = argmax_key(y, static_cast<uint32_t>(row));
+      key = argmax_key(y, static_cast<uint32_t>(row + a.key_row0));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -50,6 +50,7 @@ struct GemvArgs {
   // nullptr: plain 16 KiB tiles.
   const uint8_t* ct_blob;
   int ct_page0;
+  int key_row0;            // ARGMAX: global index of row 0 (vocab-parallel lm-head shard)
 };
 
 int gemv_max_contrib(int n_mt, int n_kb, int grid);
@@ -177,26 +178,6 @@ cudaError_t launch_action_out_euler(const float* h, const bf16* norm_w, float ep
                                     int a_dim, float dt, float* actions, float* velocity,
                                     cudaStream_t st);
 cudaError_t launch_fill_u64(unsigned long long* p, unsigned long long v, int n, cudaStream_t st);
-
-// ---------------- ECF: lossless exponent-coded BF16 for streamed layers ----------
-// Self-describing blob: this 128-byte header, then the SM plane (n_words
-// bytes), the 3-bit primary-code plane (3*n_words/8 bytes), per-unit nibble
-// offsets into the secondary stream (u32 per 1024-word unit), the 4-bit
-// secondary stream, exception word indices (u32) and exponents (u8); every
-// section 16-byte aligned.  n_words % kEcfUnit == 0 (zero padded).
-constexpr int kEcfUnit = 1024;
-struct EcfHeader {
-  uint32_t magic;  // 'ECF2'
-  uint32_t n_exc;
-  uint64_t n_words;
-  uint64_t off_sm, off_prim, off_uoff, off_sec, off_idx, off_exp;
-  uint8_t codebook1[8];   // primary: exponents of codes 0..6 (7 = escape)
-  uint8_t codebook2[16];  // secondary: exponents of codes 0..14 (15 = exception)
-  uint8_t _pad[40];
-};
-static_assert(sizeof(EcfHeader) == 128, "ECF header is 128 bytes");
-// decode + exception patch (two kernels) from a device blob into `out`
-cudaError_t launch_ecf_decode(const uint8_t* blob, void* out, int num_sms, cudaStream_t st);
 
 // ---------------- ECT: exponent-coded tiles (compact resident / streamed layers) --
 // Fixed-rate: every 16 KiB weight tile (page) is 12 KiB = 8192 sign+mantissa

@@ -161,16 +161,43 @@ def _run(p: ModelProfile, placement: Placement, config: SimConfig,
     return events, n.value, total.value
 
 
+_EVENT_DTYPE = None
+
+
+def events_to_tuple(events, n: int, mods: list[str], phs: list[list[str]]) -> tuple:
+    """Native Event records -> SimEvent tuple.  The records are read through
+    one numpy structured view and each frozen SimEvent is filled through its
+    __dict__ (what the generated __init__ does field by field), so building
+    the Python Timeline costs about as much as the native schedule itself."""
+    global _EVENT_DTYPE
+    import numpy as np
+    if n == 0:
+        return ()
+    if _EVENT_DTYPE is None:
+        _EVENT_DTYPE = np.dtype([("engine", "<i4"), ("module", "<i4"), ("phase", "<i4"),
+                                 ("_pad", "<i4"), ("invocation", "<i8"), ("layer", "<i8"),
+                                 ("start_ms", "<f8"), ("end_ms", "<f8")])
+    arr = np.frombuffer(events, dtype=_EVENT_DTYPE, count=n)
+    engines = (Engine.COPY, Engine.EXECUTE)
+    names = [[(mods[m], ph) for ph in phs[m]] for m in range(len(mods))]
+    new = object.__new__
+    out = []
+    for eng, m, ph, _, inv, layer, s, e in arr.tolist():
+        ev = new(SimEvent)
+        mod, phase = names[m][ph]
+        ev.__dict__.update(engine=engines[eng], module=mod, phase=phase, invocation=inv,
+                           layer=layer, start_ms=s, end_ms=e)
+        out.append(ev)
+    return tuple(out)
+
+
 def simulate(p: ModelProfile, placement: Placement, config: SimConfig = SimConfig(),
              layer_costs: LayerCosts | None = None) -> Timeline:
     """One inference over all modules/phases/repetitions (dfbsim.py:179-247)."""
     events, n, total = _run(p, placement, config, layer_costs, True)
     mods = [m.name for m in p.modules]
     phs = [[ph.name for ph in m.phases] for m in p.modules]
-    engines = (Engine.COPY, Engine.EXECUTE)
-    out = tuple(SimEvent(engines[e.engine], mods[e.module], phs[e.module][e.phase],
-                         e.invocation, e.layer, e.start_ms, e.end_ms) for e in events[:n])
-    return Timeline(events=out, total_ms=total)
+    return Timeline(events=events_to_tuple(events, n, mods, phs), total_ms=total)
 
 
 def simulated_total(p: ModelProfile, placement: Placement, config: SimConfig = SimConfig(),

@@ -7,7 +7,7 @@ Alpamayo-shaped stack streams over PCIe (55 GB/s) instead of running from HBM
 every 16 KiB weight tile as
     [8192 B sign+mantissa plane | 4096 B 4-bit exponent-code plane]
 (12 KiB, 75 %) lets ~33 % more layers stay resident, and every streamed layer
-moves 25 % fewer bytes.  Unlike ECF2 (ecf.py, variable-rate, ~69 %), pages are
+moves 25 % fewer bytes.  Pages are
 FIXED size, so a page is addressable by tile index: the decode GEMV streams
 compressed pages straight into its shared-memory ring and decodes in
 registers (no decoded copy), and the decoder is a pure 12-byte -> 16-byte

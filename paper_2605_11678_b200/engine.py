@@ -20,7 +20,6 @@ from dataclasses import dataclass
 import torch
 
 from . import _native
-from . import ecf
 from . import ect
 from . import model as M
 from .dfbsim import Engine as EngineKind
@@ -51,8 +50,6 @@ def _bind():
         "ls_exec_global_ptr": [vp, C.c_int32, C.POINTER(vp)],
         "ls_exec_set_global_host": [vp, C.c_int32, vp],
         "ls_exec_set_host_layers": [vp, C.c_int32, C.POINTER(vp), C.c_int32],
-        "ls_exec_set_host_layers_ecf": [vp, C.c_int32, C.POINTER(vp), C.POINTER(C.c_uint64),
-                                        C.c_int32],
         "ls_exec_set_host_layers_ct": [vp, C.c_int32, C.POINTER(vp), C.POINTER(C.c_uint64),
                                        C.c_int32],
         "ls_exec_set_placement": [vp, C.POINTER(C.c_uint8), C.c_int64],
@@ -112,9 +109,10 @@ class DemandLayeringEngine:
 
     def __init__(self, cfg: M.ModelConfig = M.ALPAMAYO, *, device: int = 0,
                  vram_cap_mb: float = 16000.0, n_slots: int = 2, seed: int = 0,
-                 init_device=None, ecf: bool = True, compact: bool = True,
+                 init_device=None, compact: bool = True,
                  tp_world: int = 1,
-                 tp_rank: int = 0, tp_id: bytes | None = None, tp_force: bool = False) -> None:
+                 tp_rank: int = 0, tp_id: bytes | None = None, tp_force: bool = False,
+                 agree=None) -> None:
         """tp_world > 1: this engine is rank `tp_rank` of a tensor-parallel group;
         it holds and streams only its shard of every layer (model.tp_config /
         shard_layer_tensors) and all-reduces row-parallel outputs with NCCL
@@ -126,12 +124,18 @@ class DemandLayeringEngine:
         launches are then the executor's own).  The generator device selects
         the random stream, so an oracle must regenerate on the same device.
 
+        agree: under tensor parallelism, a callable bool -> bool returning the
+        AND over all ranks (e.g. a MIN all-reduce); the profiling run uses it so
+        that every rank takes the same branch when a placement fits on one rank
+        but not another (ECT blob sizes differ slightly per shard), keeping the
+        ranks' NCCL call sequences identical.
+
         compact=True stores every module as ECT blobs (ect.py: exponent-coded
         tiles, lossless, 75 % of the bytes) in the host arena, the DFB slots
         and the resident blocks; the profile then reports the compact resident
         footprint, so the unchanged planner fits ~1/3 more layers under the
-        cap.  compact=False keeps plain layers (ECF-compressed streaming where
-        layer + blob fit a slot, ecf=True)."""
+        cap.  compact=False keeps plain 16 KiB-tile layers (the Accelerate-style
+        blind-offload baseline runs on those)."""
         if not torch.cuda.is_available():
             raise RuntimeError("DemandLayeringEngine needs a CUDA device (B200, sm_100a)")
         self.lib = _bind()
@@ -150,8 +154,8 @@ class DemandLayeringEngine:
         self.vram_cap_mb = vram_cap_mb
         self.n_slots = n_slots
         self.seed = seed
-        self.use_ecf = ecf
         self.use_compact = compact
+        self._agree = agree if agree is not None else (lambda ok: ok)
         torch.cuda.set_device(device)
         self._dims = cfg.dims()
         self.handle = C.c_void_p()
@@ -178,6 +182,8 @@ class DemandLayeringEngine:
     def _init_globals(self) -> None:
         tensors = M.global_tensors(self.cfg, self.seed, self.init_dev)
         for gid, t in tensors.items():
+            if gid == M.G_LM_HEAD:  # vocab-parallel under tensor parallelism
+                t = M.shard_lm_head(self.full_cfg, t, self.cfg.tp_world, self.tp_rank)
             raw = M.global_bytes_of(gid, t)
             if gid == M.G_EMBED and self.cfg.embed_on_host:
                 arena = HostArena(raw.numel())
@@ -194,14 +200,12 @@ class DemandLayeringEngine:
     def _init_layers(self) -> None:
         self.stream_bytes = {}
         self.resident_bytes = {}
-        self.ecf_kinds = []
         self.ct_kinds = []
         if self.use_compact:
             for kind in self.kinds:
                 self._init_compact(kind)
             torch.cuda.synchronize()
             return
-        slot = max(self.layouts[k].total for k in self.kinds)
         for kind in self.kinds:
             lay = self.layouts[kind]
             n = self.cfg.layers_of(kind)
@@ -209,25 +213,14 @@ class DemandLayeringEngine:
             arena = HostArena(stride * n)
             self.arenas[kind] = arena
             ptrs = (C.c_void_p * n)()
-            # ECF only where layer + blob fit one DFB slot (no change to VRAM accounting)
-            want_ecf = self.use_ecf and _a256(lay.total + 2048) + int(0.75 * lay.total) + 256 <= slot
-            blobs = []
             for layer in range(n):
                 buf = self._packed_layer(kind, layer)
                 arena.tensor[layer * stride:layer * stride + lay.total].copy_(buf)
                 ptrs[layer] = arena.ptr.value + layer * stride
-                if want_ecf:
-                    blobs.append(ecf.compress(buf))
                 del buf
             _native.check(self.lib.ls_exec_set_host_layers(self.handle, kind, ptrs, n), RuntimeError)
             self.stream_bytes[kind] = [lay.total] * n
             self.resident_bytes[kind] = _a256(lay.total)
-            if blobs and _a256(lay.total + 2048) + max(b.numel() for b in blobs) + 256 <= slot:
-                sizes = [b.numel() for b in blobs]
-                self._blob_arena(("ecf", kind), blobs, self.lib.ls_exec_set_host_layers_ecf, kind)
-                self.stream_bytes[kind] = sizes
-                self.ecf_kinds.append(kind)
-            del blobs
         torch.cuda.synchronize()
 
     def _packed_layer(self, kind: int, layer: int) -> torch.Tensor:
@@ -455,7 +448,12 @@ class DemandLayeringEngine:
             pl = Placement.of({name: range(n)})
             try:
                 self.set_placement(pl)
+                ok = True
             except MemoryError:
+                ok = False
+            if not self._agree(ok):
+                if ok:
+                    self.set_placement(Placement.empty())
                 continue
             self.execute(pl, config, record_timeline=False)  # warm-up
             spans: dict[str, list[float]] = {}

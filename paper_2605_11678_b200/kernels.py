@@ -23,7 +23,7 @@ class GemvArgs(C.Structure):
                 ("hkv", C.c_int32), ("hd", C.c_int32), ("pos", C.c_int32), ("qn_w", _vp),
                 ("kn_w", _vp), ("rope", _vp), ("q_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
                 ("cache_head_stride", C.c_int32), ("amax", _vp), ("ct_blob", _vp),
-                ("ct_page0", C.c_int32)]
+                ("ct_page0", C.c_int32), ("key_row0", C.c_int32)]
 
 
 class DecodeAttnArgs(C.Structure):

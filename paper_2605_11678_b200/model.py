@@ -394,3 +394,17 @@ def shard_layer_tensors(cfg: ModelConfig, kind: int, t: dict, world: int, rank: 
             "down": _cols(t["down"], flo, flo + Ff, F),
             "attn_norm": t["attn_norm"], "mlp_norm": t["mlp_norm"],
             "q_norm": t["q_norm"], "k_norm": t["k_norm"]}
+
+
+def lm_head_rows(cfg: ModelConfig, world: int) -> int:
+    """Vocabulary rows of the lm-head one rank holds (vocab-parallel; executor.cu head_rows)."""
+    return -(-cfg.vocab // world) if world > 1 else cfg.vocab
+
+
+def shard_lm_head(cfg: ModelConfig, t: torch.Tensor, world: int, rank: int) -> torch.Tensor:
+    """lm-head [vocab x d] -> this rank's rows [rank*Vs, (rank+1)*Vs), zero padded
+    (the padded rows are excluded from the argmax by n_valid)."""
+    if world == 1:
+        return t
+    vs = lm_head_rows(cfg, world)
+    return _rows(t, rank * vs, (rank + 1) * vs, vs)

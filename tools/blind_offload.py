@@ -37,7 +37,7 @@ def main():
     out = {"config": cfg.name, "vram_cap_mb": args.vram_cap_mb}
 
     # ---- baseline: plain layers, module-order static fill, blind offload ----
-    base = DemandLayeringEngine(cfg, vram_cap_mb=args.vram_cap_mb, compact=False, ecf=False)
+    base = DemandLayeringEngine(cfg, vram_cap_mb=args.vram_cap_mb, compact=False)
     mem = base.memory()
     room = mem["cap"] - mem["used"]
     resident, used = {}, 0
