@@ -349,6 +349,30 @@ def do_execute(args) -> Report:
     return Report(summary, _placement(p, placement))
 
 
+def do_diff(args) -> Report:
+    """Measured trace CSV (from `execute --trace` / the bench) vs the schedule
+    model on the same profile, placement and config, event by event."""
+    from . import tracediff
+    p = load_profile(resolve_input(args.profile))
+    placement = (planner.load_placement(resolve_input(args.plan)) if args.plan
+                 else planner.plan_for_budget(p, p.hardware.vram_mb).placement)
+    measured = tracediff.read_trace(resolve_input(args.measured, ".csv"))
+    diff = tracediff.diff_timelines(measured, simulate(p, placement, _config(args)))
+    if args.events_csv:
+        tracediff.write_diff_csv(diff, args.events_csv)
+    summary = Section("summary", ["field", "value"], [
+        ["measured_ms", r3(diff.measured_total_ms)], ["simulated_ms", r3(diff.simulated_total_ms)],
+        ["total_slack_ms", r3(diff.total_slack_ms)], ["events", len(diff.events)],
+        ["max_abs_end_slack_ms", r3(diff.max_abs_end_slack_ms)]], kv=True)
+    rows = [[d.engine, d.module, d.phase, d.events, r3(d.measured_busy_ms), r3(d.simulated_busy_ms),
+             r3(d.first_end_slack_ms), r3(d.last_end_slack_ms), r3(d.drift_ms), r3(d.max_abs_end_slack_ms)]
+            for d in diff.phases]
+    return Report(summary, Section("phases", ["engine", "module", "phase", "events", "measured_busy_ms",
+                                              "simulated_busy_ms", "first_end_slack_ms",
+                                              "last_end_slack_ms", "drift_ms", "max_abs_end_slack_ms"],
+                                   rows))
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="layerswap", description=(
         "Analyze, simulate, plan and execute layer-wise CPU-to-GPU parameter-swapping "
@@ -389,6 +413,13 @@ def build_parser() -> argparse.ArgumentParser:
     sp.add_argument("--module")
     sp.add_argument("--calibrate", type=float)
     sp.add_argument("--slope-ms", type=float, dest="slope_ms")
+    sp = add("diff", do_diff, "measured trace vs simulated timeline, per event and per phase")
+    sp.add_argument("measured", help="measured trace CSV (execute --trace)")
+    sp.add_argument("plan", nargs="?", help="plan file (default: plan_for_budget at the profile's VRAM)")
+    sp.add_argument("--mode", choices=[m.value for m in Mode], default=Mode.PIPELINED.value)
+    sp.add_argument("--slots", type=int, default=2)
+    sp.add_argument("--prefetch", action="store_true")
+    sp.add_argument("--events-csv", dest="events_csv", help="write the per-event diff CSV here")
     sp = add("profile", do_profile, "measure a profile on this B200 (writes JSON)", profile=False)
     sp.add_argument("--model", default="alpamayo-r1-10b-shape")
     sp.add_argument("--vram-mb", type=float, default=16000.0)
