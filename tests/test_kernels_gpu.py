@@ -431,3 +431,4 @@ def test_gemv_ect_fused_epilogues_bit_identical(epi):
     K.gemv(epi, None, n, k, x, b, ws, norm_w=nw, n_valid=nv, ct_blob=blob)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+

@@ -18,9 +18,18 @@ import torch  # noqa: E402
 from paper_2605_11678_b200 import kernels as K  # noqa: E402
 
 
+EAGER = int(__import__("os").environ.get("KB_EAGER", "0"))  # ncu: N eager calls, no graph
+
+
 def timed(fn, reps=20, warm=5):
     """Mean device time per call: `reps` calls captured in one CUDA graph (no
-    host launch overhead in the measurement), replayed after warm-up."""
+    host launch overhead in the measurement), replayed after warm-up.
+    KB_EAGER=N: N plain eager calls instead (for ncu -s/-c selection)."""
+    if EAGER:
+        for _ in range(EAGER):
+            fn()
+        torch.cuda.synchronize()
+        return float("nan")
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -205,6 +214,19 @@ def main():
         res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
         res.append(bench_gemv_ect(6144, 4096, K.GEMV_F32))
         res.append(bench_ect_decode())
+    if args.only == "ectgemm_gu":
+        res.append(bench_gemm(64, 13824, 2048, K.GEMM_SILU_BF16, splitk=True, ct=True))
+    if args.only == "plaingemm_gu":
+        res.append(bench_gemm(64, 13824, 2048, K.GEMM_SILU_BF16, splitk=True))
+    if args.only == "ectgemm_qkv":
+        res.append(bench_gemm(64, 6144, 2048, K.GEMM_BF16, splitk=True, ct=True))
+    if args.only == "attn16":
+        res.append(bench_decode_attn(n_split=16))
+    if args.only == "flash4":
+        res.append(bench_flash_expert(4))
+    if args.only == "prefill_gemm":
+        res.append(bench_gemm(1024, 24576, 4096, K.GEMM_SILU_BF16))
+        res.append(bench_gemm(1024, 4096, 12288, K.GEMM_RESID_F32))
     if args.only == "flash":
         for sp in (1, 2, 4, 8):
             res.append(bench_flash_expert(sp))

@@ -24,7 +24,8 @@ DEC_MASKS = {"dec attention": 128, "dec qkv gemv": 256, "dec o gemv": 512, "dec 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--profile", default="profiles/r1_profile_alpamayo_ect.json")
+    ap.add_argument("--profile", default=None, help="profile JSON (default: measure one now)")
+    ap.add_argument("--only", default="expert,decode,prefill,vit")
     ap.add_argument("--runs", type=int, default=3)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -32,9 +33,10 @@ def main():
     from paper_2605_11678_b200 import model as M
     from paper_2605_11678_b200.engine import DemandLayeringEngine
     cfg = M.PRESETS["alpamayo-r1-10b-shape"]
-    prof = ls.load_profile(args.profile)
+    eng = DemandLayeringEngine(cfg, vram_cap_mb=16000.0)
+    prof = ls.load_profile(args.profile) if args.profile else eng.profile_run(iterations=2, warmup=1)
     plan = ls.plan_for_budget(prof, prof.hardware.vram_mb)
-    eng = DemandLayeringEngine(cfg, vram_cap_mb=prof.hardware.vram_mb)
+    only = set(args.only.split(","))
     inputs = M.synthetic_inputs(cfg, 0)
     n_inv = cfg.layers_of(M.KIND_EXPERT) * cfg.euler_steps
 
@@ -46,26 +48,27 @@ def main():
 
     base = run(0)
     res = {"base_ms": base, "expert_layer_invocations": n_inv, "per_layer_us": {}}
-    for name, m in MASKS.items():
+    for name, m in (MASKS.items() if "expert" in only else ()):
         ms = run(m)
         res["per_layer_us"][name] = (base - ms) * 1e3 / n_inv
         print(f"{name:14s} {ms:8.2f} ms  -> {res['per_layer_us'][name]:7.2f} us per expert layer", flush=True)
     n_dec = cfg.layers_of(M.KIND_LM) * cfg.decode_steps
-    for name, m in DEC_MASKS.items():
+    for name, m in (DEC_MASKS.items() if "decode" in only else ()):
         ms = run(m)
         res["per_layer_us"][name] = (base - ms) * 1e3 / n_dec
         print(f"{name:16s} {ms:8.2f} ms  -> {res['per_layer_us'][name]:7.2f} us per decode layer-step", flush=True)
     n_pre = cfg.layers_of(M.KIND_LM)
-    for name, m in {"prefill ECT scratch decodes (all layers)": 1 << 12, "prefill attention": 1 << 13,
+    for name, m in ({"prefill ECT scratch decodes (all layers)": 1 << 12, "prefill attention": 1 << 13,
                     "prefill qkv gemm": 1 << 14, "prefill o gemm": 1 << 15, "prefill gate|up gemm": 1 << 16,
-                    "prefill down gemm": 1 << 17}.items():
+                    "prefill down gemm": 1 << 17}.items() if "prefill" in only else ()):
         ms = run(m)
         per = (base - ms) * 1e3 / n_pre
         res["per_layer_us"][name] = per
         print(f"{name:16s} {ms:8.2f} ms  -> {per:7.2f} us per prefill layer", flush=True)
     n_vit = cfg.layers_of(M.KIND_VIT)
-    for name, m in {"vit layernorm x2": 1 << 18, "vit qkv gemm": 1 << 19, "vit attention": 1 << 20,
-                    "vit proj gemm": 1 << 21, "vit fc1 gemm": 1 << 22, "vit fc2 gemm": 1 << 23}.items():
+    for name, m in ({"vit layernorm x2": 1 << 18, "vit qkv gemm": 1 << 19, "vit attention": 1 << 20,
+                    "vit proj gemm": 1 << 21, "vit fc1 gemm": 1 << 22, "vit fc2 gemm": 1 << 23}.items()
+                    if "vit" in only else ()):
         ms = run(m)
         per = (base - ms) * 1e3 / n_vit
         res["per_layer_us"][name] = per
