@@ -502,6 +502,11 @@ def main():
             ctx = cfg.prompt_len + e.invocation + 1
             dec_rates.append((nbytes + ctx * kv_bytes_tok) / (dur * 1e6))
     h2d_streamed = statistics.fmean(dma_rates) if dma_rates else None
+    # (f)2: the measured per-layer timeline vs the schedule model on the measured
+    # profile, event by event (per-layer timing events break the PDL chains between
+    # layers, so this run is slower than the untimed steps; the drift says where)
+    from paper_2605_11678_b200 import tracediff
+    tdiff = tracediff.diff_timelines(tl, ls.simulate(prof, placement, sim_cfg))
 
     # warm-up, then EXACTLY K timed steps (device events per step; barrier + sync both sides)
     for _ in range(args.warmup):
@@ -589,6 +594,7 @@ def main():
         from paper_2605_11678_b200.planner import save_plan
         save_plan(plan, out / f"plan_{cfg.name}.json")
         ls.write_trace(tl, out / f"trace_{cfg.name}.csv")
+        tracediff.write_diff_csv(tdiff, out / f"trace_diff_{cfg.name}.csv")
     eng.close()
 
     cpu = None
@@ -624,6 +630,12 @@ def main():
                 "peak_source": "measured on this box: pinned 1 GiB cudaMemcpyAsync, best of 5"},
         "tokens": tokens,
         "predictor": pred,
+        "timeline_diff": {k: v for k, v in tracediff.summary_dict(tdiff).items()
+                          if k in ("measured_total_ms", "simulated_total_ms", "total_slack_ms", "events")}
+        | {"phase_drift_ms": {f"{p['engine']}/{p['module']}/{p['phase']}": round(p["drift_ms"], 3)
+                              for p in tracediff.summary_dict(tdiff)["phases"]},
+           "note": "per-layer-timed run (events between layers break PDL chains) vs dfbsim on the "
+                   "measured profile; per-event CSV in --dump"},
         "lower_bound": {"dfbsim_total_s": sim_bound_s, "measured_over_bound": (ms / 1e3) / sim_bound_s,
                         "note": "dfbsim total of the chosen placement on the measured profile"},
         "roofline": {"bound": "hbm", "achieved": gv["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",

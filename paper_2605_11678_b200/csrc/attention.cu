@@ -8,6 +8,7 @@
 //   bf16 mma.sync m16n8k16 tiles, online softmax in fp32, causal /
 //   block-diagonal (per image) / two-segment KV (expert: VLM cache + own).
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -263,8 +264,11 @@ struct FlashCfg {
 };
 
 // G > 1 (GQA packing): one CTA = G query heads of one KV head, 4 warps per head,
-// so each K/V block is loaded once for all G heads.
-template <int HD, int G = 1>
+// so each K/V block is loaded once for all G heads.  NS: K/V block stages in
+// flight (2 = double buffering; the split-KV expert launch, one CTA per SM with a
+// few blocks each, keeps NS - 1 blocks ahead so L2/HBM latency is not exposed
+// per block).
+template <int HD, int G = 1, int NS = 2>
 __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   using Cfg = FlashCfg<HD>;
   constexpr int NT = 128 * G;
@@ -272,8 +276,8 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(16) uint8_t fsm[];
   bf16* qs = reinterpret_cast<bf16*>(fsm);
-  bf16* ks_buf = qs + G * BM * LD;      // [2][BN][LD]: double-buffered K and V blocks
-  bf16* vs_buf = ks_buf + 2 * BN * LD;
+  bf16* ks_buf = qs + G * BM * LD;      // [NS][BN][LD]: K and V block stages
+  bf16* vs_buf = ks_buf + NS * BN * LD;
   pdl_trigger();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -357,8 +361,14 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   const int q_lo = q0 + a.q_offset;  // smallest query position of the tile (causal)
   // the first K/V block is requested before griddepcontrol.wait when it lies in
   // a segment the previous kernel did not write (the expert over the VLM cache)
-  const bool early = a.k1_ready && k_begin < k_end && k_begin + BN <= a.len1;
-  if (early) load_kv(0, k_begin);
+  // the first NS - 1 blocks are requested before griddepcontrol.wait when they lie
+  // in a segment the previous kernel did not write (the expert over the VLM cache)
+  const int nblk = k_begin < k_end ? (k_end - k_begin + BN - 1) / BN : 0;
+  int issued = 0;
+  while (issued < NS - 1 && issued < nblk && a.k1_ready && k_begin + (issued + 1) * BN <= a.len1) {
+    load_kv(issued % NS, k_begin + issued * BN);
+    ++issued;
+  }
   pdl_wait();
   // ---- Q tile -> smem (zero padded), after griddepcontrol.wait ----
   for (int i = threadIdx.x; i < G * BM * (DK / 8); i += NT) {
@@ -385,15 +395,16 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   float o[ND][4];
 #pragma unroll
   for (int j = 0; j < ND; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  if (!early && k_begin < k_end) load_kv(0, k_begin);
+  for (; issued < NS - 1; ++issued) {  // empty groups keep the group count uniform
+    if (issued < nblk) load_kv(issued % NS, k_begin + issued * BN);
+    else cp_async_commit();
+  }
   int buf = 0;
-  for (int j0 = k_begin; j0 < k_end; j0 += BN, buf ^= 1) {
-    if (j0 + BN < k_end) {
-      load_kv(buf ^ 1, j0 + BN);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+  for (int j0 = k_begin, jb = 0; j0 < k_end; j0 += BN, ++jb, buf = (buf + 1 == NS ? 0 : buf + 1)) {
+    // block jb + NS - 1 into the stage block jb - 1 used (freed by the loop's final barrier)
+    if (jb + NS - 1 < nblk) load_kv((jb + NS - 1) % NS, j0 + (NS - 1) * BN);
+    else cp_async_commit();
+    cp_async_wait<NS - 1>();  // block jb has landed
     __syncthreads();
     const bf16* ks = ks_buf + buf * BN * LD;
     const bf16* vs = vs_buf + buf * BN * LD;
@@ -559,13 +570,13 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   }
 }
 
-template <int HD, int G = 1>
+template <int HD, int G = 1, int NS = 2>
 static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   using Cfg = FlashCfg<HD>;
-  const size_t smem = static_cast<size_t>(G * Cfg::kBM + 4 * Cfg::kBN) * Cfg::kLd * 2;
+  const size_t smem = static_cast<size_t>(G * Cfg::kBM + 2 * NS * Cfg::kBN) * Cfg::kLd * 2;
   static DeviceFlags attr;
   if (!attr.done()) {
-    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD, G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr.mark();
@@ -589,7 +600,7 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   la[1].val.clusterDim.z = static_cast<unsigned>(splits);
   cfg.attrs = la;
   cfg.numAttrs = splits > 1 ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, flash_kernel<HD, G>, a);
+  return cudaLaunchKernelEx(&cfg, flash_kernel<HD, G, NS>, a);
 }
 
 int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms) {
@@ -614,7 +625,17 @@ cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {
     case 32: return flash_hd<32>(a, st);
     case 64: return flash_hd<64>(a, st);
     case 72: return flash_hd<72>(a, st);
-    case 128: return a.g_pack == 2 ? flash_hd<128, 2>(a, st) : flash_hd<128>(a, st);
+    case 128: {
+      if (a.g_pack == 2) return flash_hd<128, 2>(a, st);
+      if (a.kv_splits <= 1) return flash_hd<128>(a, st);
+      // split-KV (the expert): a few key blocks per CTA, one CTA per SM -- keep
+      // more blocks in flight (LS_DIAG_FLASH_NS: 2..4, diagnostics)
+      static const int ns = [] {
+        const char* v = std::getenv("LS_DIAG_FLASH_NS");
+        return v ? std::atoi(v) : 4;
+      }();
+      return ns <= 2 ? flash_hd<128>(a, st) : ns == 3 ? flash_hd<128, 1, 3>(a, st) : flash_hd<128, 1, 4>(a, st);
+    }
   }
   return cudaErrorInvalidValue;
 }

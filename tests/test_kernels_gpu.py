@@ -432,3 +432,39 @@ def test_gemv_ect_fused_epilogues_bit_identical(epi):
     torch.cuda.synchronize()
     assert torch.equal(a, b)
 
+
+
+# T > 256 with plain weights: the activation-multicast cluster GEMM (CM = 4 when
+# n_mt % 4 == 0, 2 when even, else the single-CTA kernel) -- ragged T, short K,
+# every epilogue; run-to-run bit-stable.
+@pytest.mark.parametrize("epi,T,n,k", [(0, 1024, 6144, 4096), (3, 512, 1024, 1024), (2, 1024, 256, 2048),
+                                       (1, 300, 384, 512), (4, 700, 512, 640), (0, 3072, 1152, 1152),
+                                       (2, 1024, 4096, 12288)])
+def test_gemm_cluster_multicast(epi, T, n, k):
+    torch.manual_seed(31)
+    w = (torch.randn(n, k, device=DEV) * 0.03).to(torch.bfloat16)
+    x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
+    ncol = n // 2 if epi == K.GEMM_SILU_BF16 else n
+    odt = torch.float32 if epi in (K.GEMM_RESID_F32, K.GEMM_F32) else torch.bfloat16
+    base = torch.randn(T, ncol, device=DEV).to(odt)
+    bias = torch.randn(n, device=DEV).to(torch.bfloat16) if epi == K.GEMM_BF16_GELU else None
+    outs = []
+    for _ in range(2):
+        out = base.clone()
+        K.gemm(epi, K.pack_tiled(w), n, k, x, out, n_valid=ncol, bias=bias)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    y = x.float() @ w.float().t()
+    if epi == K.GEMM_SILU_BF16:
+        yg = y.view(T, n // 128, 2, 64)
+        ref = (torch.nn.functional.silu(yg[:, :, 0]) * yg[:, :, 1]).reshape(T, ncol)
+        _close(outs[0], ref, rel=1.5e-2, abs_=1e-2)
+    elif epi == K.GEMM_BF16_GELU:
+        _close(outs[0], torch.nn.functional.gelu(y + bias.float(), approximate="tanh"), rel=1.5e-2, abs_=1e-2)
+    elif epi == K.GEMM_RESID_F32:
+        _close(outs[0], base + y, rel=2e-3, abs_=2e-3)
+    elif epi == K.GEMM_F32:
+        _close(outs[0], y, rel=2e-3, abs_=2e-3)
+    else:
+        _close(outs[0], y, rel=1.5e-2, abs_=1e-2)

@@ -224,6 +224,14 @@ def main():
         res.append(bench_decode_attn(n_split=16))
     if args.only == "flash4":
         res.append(bench_flash_expert(4))
+    if args.only == "prefill_all":  # LM prefill (T = 1024) and ViT (T = 3072) shapes
+        res.append(bench_gemm(1024, 6144, 4096))
+        res.append(bench_gemm(1024, 4096, 4096, K.GEMM_RESID_F32))
+        res.append(bench_gemm(1024, 24576, 4096, K.GEMM_SILU_BF16))
+        res.append(bench_gemm(1024, 4096, 12288, K.GEMM_RESID_F32))
+        res.append(bench_gemm(3072, 3456, 1152))
+        res.append(bench_gemm(3072, 4352, 1152, K.GEMM_BF16_GELU))
+        res.append(bench_gemm(3072, 1152, 4352, K.GEMM_RESID_F32))
     if args.only == "prefill_gemm":
         res.append(bench_gemm(1024, 24576, 4096, K.GEMM_SILU_BF16))
         res.append(bench_gemm(1024, 4096, 12288, K.GEMM_RESID_F32))

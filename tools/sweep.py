@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--vram-cap-mb", type=float, default=16000.0)
     ap.add_argument("--out", default="profiles/r2_sweep.json")
     ap.add_argument("--no-prefetch", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=5)
     args = ap.parse_args()
     import paper_2605_11678_b200 as ls
     from bench import max_resident_run
@@ -44,7 +45,7 @@ def main():
     eng = DemandLayeringEngine(cfg, vram_cap_mb=args.vram_cap_mb)
     sim_cfg = ls.SimConfig(cross_invocation_prefetch=not args.no_prefetch)
     t0 = time.time()
-    prof = eng.profile_run(iterations=2, warmup=1, config=sim_cfg)
+    prof = eng.profile_run(iterations=args.profile_iters, warmup=1, config=sim_cfg)
     vlm = prof.module("vlm")
     L = vlm.layers
     plan = ls.plan_for_budget(prof, prof.hardware.vram_mb, sim_cfg)
