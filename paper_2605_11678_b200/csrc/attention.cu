@@ -627,7 +627,13 @@ cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {
     case 72: return flash_hd<72>(a, st);
     case 128: {
       if (a.g_pack == 2) return flash_hd<128, 2>(a, st);
-      if (a.kv_splits <= 1) return flash_hd<128>(a, st);
+      if (a.kv_splits <= 1) {  // causal prefill (LS_DIAG_FLASH_NSP: 2 = two CTAs per SM)
+        static const int nsp = [] {
+          const char* v = std::getenv("LS_DIAG_FLASH_NSP");
+          return v ? std::atoi(v) : 2;
+        }();
+        return nsp <= 2 ? flash_hd<128>(a, st) : nsp == 3 ? flash_hd<128, 1, 3>(a, st) : flash_hd<128, 1, 4>(a, st);
+      }
       // split-KV (the expert): a few key blocks per CTA, one CTA per SM -- keep
       // more blocks in flight (LS_DIAG_FLASH_NS: 2..4, diagnostics)
       static const int ns = [] {

@@ -64,7 +64,7 @@ int ls_k_gemm(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void
               int32_t n_valid, void* stream) {
   CUtensorMap map;
   int rc = make_tmap_bf16(&map, x, static_cast<uint64_t>(T), static_cast<uint64_t>(n_kb) * 64,
-                          static_cast<uint64_t>(ldx), static_cast<uint32_t>(gemm_block_n(T)));
+                          static_cast<uint64_t>(ldx), static_cast<uint32_t>(gemm_box_rows()));
   if (rc) return set_error(LS_ERR_CUDA, "ls_k_gemm: cuTensorMapEncodeTiled failed (%d)", rc);
   GemmArgs a{};
   a.w = static_cast<const uint8_t*>(w);
@@ -85,7 +85,7 @@ int ls_k_gemm_ws(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const v
                  int32_t sk_cnt_n, const void* ct_blob, int32_t ct_page0, void* stream) {
   CUtensorMap map;
   int rc = make_tmap_bf16(&map, x, static_cast<uint64_t>(T), static_cast<uint64_t>(n_kb) * 64,
-                          static_cast<uint64_t>(ldx), static_cast<uint32_t>(gemm_block_n(T)));
+                          static_cast<uint64_t>(ldx), static_cast<uint32_t>(gemm_box_rows()));
   if (rc) return set_error(LS_ERR_CUDA, "ls_k_gemm_ws: cuTensorMapEncodeTiled failed (%d)", rc);
   GemmArgs a{};
   a.w = static_cast<const uint8_t*>(w);

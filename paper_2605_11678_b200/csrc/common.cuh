@@ -210,7 +210,9 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+// x * sigmoid(x) with the approximate divide (MUFU.RCP + one multiply, vs the
+// ~10-instruction IEEE division): the SiLU*up GEMM epilogue was issue-bound on it
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 // tanh.approx.f32: one MUFU op (max rel. error ~2^-11, far below the bf16
 // rounding of the GELU output); tanhf's accurate path made the ViT fc1 GEMM
 // epilogue-bound (65 us for 30 GFLOP)

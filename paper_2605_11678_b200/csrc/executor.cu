@@ -334,7 +334,7 @@ int alloc_into(ls_exec* e, void* dst_ptr, uint64_t bytes, uint64_t* counter) {
 int tmap(CUtensorMap* m, const void* base, int rows, int cols, int ld) {
   if (rows <= 0) return LS_OK;
   int r = make_tmap_bf16(m, base, static_cast<uint64_t>(rows), static_cast<uint64_t>(cols),
-                         static_cast<uint64_t>(ld), static_cast<uint32_t>(gemm_block_n(rows)));
+                         static_cast<uint64_t>(ld), static_cast<uint32_t>(gemm_box_rows()));
   if (r) return set_error(LS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
   return LS_OK;
 }

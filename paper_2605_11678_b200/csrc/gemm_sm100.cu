@@ -124,8 +124,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
             if (round) mbar_wait(&empty[s], (round - 1) & 1);
             a_load(s, mt, kb);
           }
+          // activations in 64-row boxes (gemm_box_rows: one tensor map serves every BN)
           mbar_arrive_expect_tx(&bfull[s], Cfg::kBBytes);
-          tma_load_2d(sb + s * Cfg::kBBytes, &xmap, kb * kTileCols, n0, &bfull[s]);
+#pragma unroll
+          for (int q = 0; q < BN / 64; ++q)
+            tma_load_2d(sb + s * Cfg::kBBytes + q * 8192, &xmap, kb * kTileCols, n0 + q * 64, &bfull[s]);
           if (++s == Cfg::kStages) {
             s = 0;
             ++round;
@@ -229,67 +232,106 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
         if (a.bias) bias = a.bias[f];
         else if (a.bias_bf16) bias = bf2f(a.bias_bf16[f]);
       }
-      // fused epilogue of 16 consecutive tokens n0 + c0 .. (all 128 epilogue threads call it)
-      auto emit = [&](int c0, const float (&v)[16]) {
-        if constexpr (EPI == GEMM_SILU_BF16) {
-          named_bar(2, 128);  // previous chunk's readers are done with stage_f
-#pragma unroll
-          for (int j = 0; j < 16; ++j) stage_f[m * 17 + j] = v[j];
-          named_bar(2, 128);
-          if (m < 64) {
-            const int g = mt * 64 + m;
-            bf16* out = static_cast<bf16*>(a.out);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int tok = n0 + c0 + j;
-              if (tok < a.T && g < a.n_valid)
-                out[static_cast<long>(tok) * a.ldo + g] =
-                    f2bf(silu(stage_f[m * 17 + j]) * stage_f[(m + 64) * 17 + j]);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int tok = n0 + c0 + j;
-            if (tok >= a.T) break;
-            const long o = static_cast<long>(tok) * a.ldo + f;
-            const float y = v[j] + bias;
-            if constexpr (EPI == GEMM_BF16) static_cast<bf16*>(a.out)[o] = f2bf(y);
-            else if constexpr (EPI == GEMM_BF16_GELU) static_cast<bf16*>(a.out)[o] = f2bf(gelu_tanh(y));
-            else if constexpr (EPI == GEMM_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] = y; }
-            else if constexpr (EPI == GEMM_RESID_F32) { if (f < a.n_valid) static_cast<float*>(a.out)[o] += y; }
-          }
-        }
-      };
       const uint32_t acc = tmem + b * Cfg::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
       if (ks == 1 && EPI == GEMM_RESID_F32) {
-        // residual add: all 32 old values of a chunk are loaded before any store
-        // (a load-add-store per token would serialise on possible aliasing)
+        // residual add, one thread per feature: all 32 old values of a chunk are
+        // loaded before any store (32 independent loads in flight per thread; the
+        // transposed float4 variant below measured slower here: its loads, one
+        // chunk ahead, leave a round trip exposed per 16 tokens)
         float* out = static_cast<float*>(a.out);
         const bool fv = f < a.n_valid;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float old[32], v0[16], v1[16];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int tok = n0 + c0 + j;
-            old[j] = (fv && tok < a.T) ? out[static_cast<long>(tok) * a.ldo + f] : 0.f;
+          for (int jj = 0; jj < 32; ++jj) {
+            const int tok = n0 + c0 + jj;
+            old[jj] = (fv && tok < a.T) ? out[static_cast<long>(tok) * a.ldo + f] : 0.f;
           }
           tmem_ld16(acc + c0, v0);
           tmem_ld16(acc + c0 + 16, v1);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int tok = n0 + c0 + j;
+          for (int jj = 0; jj < 32; ++jj) {
+            const int tok = n0 + c0 + jj;
             if (fv && tok < a.T)
-              out[static_cast<long>(tok) * a.ldo + f] = old[j] + ((j < 16 ? v0[j] : v1[j - 16]) + bias);
+              out[static_cast<long>(tok) * a.ldo + f] = old[jj] + ((jj < 16 ? v0[jj] : v1[jj - 16]) + bias);
           }
         }
       } else if (ks == 1) {
+        // Fused epilogue per 16-token chunk, transposed through shared memory: the
+        // TMEM read gives a thread one feature x 16 tokens; after the exchange a
+        // thread owns 8 (bf16) or 4 (fp32) consecutive features of one token, so a
+        // store is one 16-byte access instead of 8-16 scalar ones, and every one of
+        // the 128 threads computes (SiLU*up used 64) -- the per-element epilogue was
+        // the bottleneck of the K = 1152 / 4096 GEMMs (gate|up 239 -> 156 us)
+        const bool vec = (a.ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
+        const bool vec4 = (a.ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
           tmem_ld16(acc + c0, v);
-          emit(c0, v);
+          named_bar(2, 128);  // previous chunk's readers are done with stage_f
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) stage_f[m * 17 + jj] = EPI == GEMM_SILU_BF16 ? v[jj] : v[jj] + bias;
+          named_bar(2, 128);
+          if constexpr (EPI == GEMM_SILU_BF16) {
+            const int jt = m & 15, fg = m >> 4;  // token, 8-feature group of the tile's 64
+            const int tok = n0 + c0 + jt, g0 = mt * 64 + fg * 8;
+            if (tok < a.T) {
+              float o[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                o[e] = silu(stage_f[(fg * 8 + e) * 17 + jt]) * stage_f[(64 + fg * 8 + e) * 17 + jt];
+              bf16* dst = static_cast<bf16*>(a.out) + static_cast<long>(tok) * a.ldo + g0;
+              if (vec && g0 + 8 <= a.n_valid) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                                            pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  if (g0 + e < a.n_valid) dst[e] = f2bf(o[e]);
+              }
+            }
+          } else if constexpr (EPI == GEMM_BF16 || EPI == GEMM_BF16_GELU) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const int item = m + 128 * r, jt = item & 15, fg = item >> 4;  // token, 8-feature group
+              const int tok = n0 + c0 + jt, f0 = mt * kTileRows + fg * 8;
+              if (tok >= a.T) continue;
+              float o[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float y = stage_f[(fg * 8 + e) * 17 + jt];
+                o[e] = EPI == GEMM_BF16_GELU ? gelu_tanh(y) : y;
+              }
+              bf16* dst = static_cast<bf16*>(a.out) + static_cast<long>(tok) * a.ldo + f0;
+              if (vec) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                                            pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) dst[e] = f2bf(o[e]);
+              }
+            }
+          } else {  // GEMM_F32: float4 per (token, 4 features)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int item = m + 128 * r, jt = item & 15, fq = item >> 4;  // token, 4-feature group
+              const int tok = n0 + c0 + jt, f0 = mt * kTileRows + fq * 4;
+              if (tok >= a.T) continue;
+              float4 y = make_float4(stage_f[(fq * 4) * 17 + jt], stage_f[(fq * 4 + 1) * 17 + jt],
+                                     stage_f[(fq * 4 + 2) * 17 + jt], stage_f[(fq * 4 + 3) * 17 + jt]);
+              float* dst = static_cast<float*>(a.out) + static_cast<long>(tok) * a.ldo + f0;
+              if (vec4 && f0 + 4 <= a.n_valid) {
+                *reinterpret_cast<float4*>(dst) = y;
+              } else {
+                const float yy[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (f0 + e < a.n_valid) dst[e] = yy[e];
+              }
+            }
+          }
         }
       }
       if (ks == 1) {
@@ -387,6 +429,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
 }
 
 int gemm_block_n(int T) { return T <= 64 ? 64 : (T <= 256 ? 128 : 256); }
+int gemm_box_rows() { return 64; }  // activation tensor-map box: 64 token rows
 
 int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n, bool ct) {
   const int bn = gemm_block_n(T);

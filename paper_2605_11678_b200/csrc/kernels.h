@@ -72,7 +72,7 @@ struct GemmArgs {
   const uint8_t* w;   // tiled weights (n_mt x n_kb tiles)
   int n_mt, n_kb;
   int T;              // tokens (rows of X)
-  const CUtensorMap* x_map;  // X [T x n_kb*64] bf16 row-major, SWIZZLE_128B box {64, BN}
+  const CUtensorMap* x_map;  // X [T x n_kb*64] bf16 row-major, SWIZZLE_128B box {64, 64} (gemm_box_rows)
   void* out;
   long ldo;           // elements between consecutive tokens in out
   const float* bias;  // per output feature (optional)
@@ -95,6 +95,7 @@ struct GemmArgs {
 };
 
 int gemm_block_n(int T);
+int gemm_box_rows();  // rows of the activation tensor-map box (the kernels load BN/64 boxes per stage)
 // split factor launch_gemm picks for a shape (1 = no split)
 int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n, bool ct = false);
 cudaError_t launch_gemm(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st);
