@@ -22,5 +22,11 @@ if [ -f "$PROF" ] && [ -z "$SKIP_NCU" ]; then
   ncu -i $OUT/gemv_silu_ect.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > $OUT/gemv_silu_ect_dram.csv 2>&1
   cat $OUT/gemv_silu_ect_dram.csv | tail -3
   python tools/ncu_kv.py $OUT/gemv_silu_ect.ncu-rep > $OUT/gemv_silu_ect_summary.txt 2>&1
+  # the prefill gate|up tcgen05 GEMM as launched in the step: tensor-pipe utilisation
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k 'regex:gemm_kernel<.int.256, .int.3' -s 2 -c 1 -o $OUT/gemm_gu_prefill python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_gemm.log 2>&1
+  ncu -i $OUT/gemm_gu_prefill.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum > $OUT/gemm_gu_prefill_raw.csv 2>&1
+  tail -1 $OUT/gemm_gu_prefill_raw.csv
+  python tools/ncu_kv.py $OUT/gemm_gu_prefill.ncu-rep > $OUT/gemm_gu_prefill_summary.txt 2>&1
 fi
 ls -la $OUT
