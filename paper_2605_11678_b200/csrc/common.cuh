@@ -139,6 +139,12 @@ __device__ __forceinline__ uint32_t ect_plain_word(uint32_t q) {
   const uint32_t k = 16 * ks + 8 * (j >> 2) + 2 * (lane & 3) + (j & 1);
   return r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7);
 }
+// Row-chunk page order (EctHeader.order 1, ect.py ORDER_ROWS): page word
+// (g * 128 + r) * 16 + j is row r, k = 16 g + j of the tile.
+__device__ __forceinline__ uint32_t ect_plain_word_rows(uint32_t q) {
+  const uint32_t r = (q >> 4) & 127u, k = ((q >> 11) << 4) | (q & 15u);
+  return r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7);
+}
 // bit 4k set iff word k's code is 15 (escape)
 __device__ __forceinline__ uint32_t ect_escapes(uint32_t nib) {
   // low 3 bits == 7 carries into bit 3; with bit 3 set the nibble is 15
@@ -368,6 +374,24 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+// Same with the A operand in tensor memory (M = 128 rows in lanes 0..127, K
+// packed two bf16 per 32-bit column): D[tmem] (+)= A[tmem_a] . B[smem desc]
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 8 consecutive 32-bit columns from registers (then wait for the stores)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(a.x),
+      "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

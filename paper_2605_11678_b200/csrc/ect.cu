@@ -34,9 +34,17 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
   // one page per CTA iteration: fragments decoded into the plain tile image in
   // shared memory (pair stores are bank-conflict-free thanks to the 128 B
   // swizzle), then streamed out as coalesced 16-byte stores
-  uint32_t pos[4];  // plain-tile u32 slots of fragment threadIdx.x's word pairs
+  // plain-tile u32 slots of this thread's word pairs (words 8 f .. 8 f + 7 of
+  // fragment f = it * 256 + threadIdx.x), per page order
+  const bool rows = h->order == 1;
+  uint32_t pos[4][4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) pos[p] = ect_plain_word(threadIdx.x * 8 + 2 * p) >> 1;
+  for (int it = 0; it < 4; ++it)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t q = (it * 256 + threadIdx.x) * 8 + 2 * p;
+      pos[it][p] = (rows ? ect_plain_word_rows(q) : ect_plain_word(q)) >> 1;
+    }
   for (uint32_t page = blockIdx.x; page < n_pages; page += gridDim.x) {
     const uint8_t* pg = pages + static_cast<uint64_t>(page) * kEctPageBytes;
 #pragma unroll
@@ -47,11 +55,10 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
       uint4 w = ect_decode8(sm, nib, e0p);
       const uint32_t esc = ect_escapes(nib);
       if (esc) w = ect_zero_escapes(w, esc);  // exponent 0 unless an exc entry patches it below
-      uint32_t* tb = tile + it * 1024;  // fragment + 256 = 2 row blocks (32 rows) lower
-      tb[pos[0]] = w.x;
-      tb[pos[1]] = w.y;
-      tb[pos[2]] = w.z;
-      tb[pos[3]] = w.w;
+      tile[pos[it][0]] = w.x;
+      tile[pos[it][1]] = w.y;
+      tile[pos[it][2]] = w.z;
+      tile[pos[it][3]] = w.w;
     }
     __syncthreads();
     // the page's exceptions (true exponents of escaped words) patched in shared memory
@@ -60,7 +67,7 @@ __global__ void __launch_bounds__(256) ect_decode_kernel(const uint8_t* __restri
       uint16_t* t16 = reinterpret_cast<uint16_t*>(tile);
       for (uint32_t i = e_lo + threadIdx.x; i < e_hi; i += blockDim.x) {
         const uint32_t x = exc[i];
-        const uint32_t k = ect_plain_word(x >> 8);
+        const uint32_t k = rows ? ect_plain_word_rows(x >> 8) : ect_plain_word(x >> 8);
         t16[k] = static_cast<uint16_t>((t16[k] & 0x807Fu) | ((x & 0xFFu) << 7));
       }
       if (e_hi > e_lo) __syncthreads();

@@ -35,7 +35,10 @@ struct GemmCfg {
   static constexpr int kPBytes = CT ? kEctPageBytes : 0;  // page staging
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kAccCols = BN < 32 ? 32 : BN;     // one accumulator
-  static constexpr int kTmemCols = 2 * kAccCols;         // double-buffered (<= 512)
+  // double-buffered accumulators; single-token-tile ECT launches (BN <= 128) also
+  // hold the decoded A stages in TMEM (32 columns each) for row-order pages
+  static constexpr bool kTmA = CT && BN <= 128;
+  static constexpr int kTmemCols = kTmA ? 512 : 2 * kAccCols;
   static constexpr int kDecWarps = CT ? 16 : 0;
   static constexpr int kThreads = 192 + 32 * kDecWarps;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * (kStageBytes + kPBytes) +
@@ -91,6 +94,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // row-order ECT pages (EctHeader.order 1): the decoders write A straight into
+  // TMEM (tcgen05.st, one row per lane) and the MMA reads it from there
+  bool tm = false;
+  if constexpr (Cfg::kTmA) tm = reinterpret_cast<const EctHeader*>(a.ct_blob)->order == 1;
+  const uint32_t tmem_a = tmem + 2 * Cfg::kAccCols;  // A stage s at column +32 s
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
@@ -156,9 +164,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(sa + s * Cfg::kABytes);
           const uint64_t db = umma_desc_sw128(sb + s * Cfg::kBBytes);
+          if (tm) {
 #pragma unroll
-          for (int k = 0; k < kTileCols / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-            umma_bf16(acc, da + 2ull * k, db + 2ull * k, idesc, (kb > kb0 || k) ? 1u : 0u);
+            for (int k = 0; k < kTileCols / 16; ++k)  // A: 8 TMEM columns per K=16 step
+              umma_bf16_ts(acc, tmem_a + s * 32 + 8 * k, db + 2ull * k, idesc, (kb > kb0 || k) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int k = 0; k < kTileCols / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+              umma_bf16(acc, da + 2ull * k, db + 2ull * k, idesc, (kb > kb0 || k) ? 1u : 0u);
+          }
           umma_commit(&empty[s]);
           if (++s == Cfg::kStages) {
             s = 0;
@@ -177,10 +191,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
     const int dt = threadIdx.x - 192;  // 0 .. 32 * kDecWarps - 1
     // u32 slots of this thread's 4 word pairs in the plain tile for fragment dt; fragment
     // dt + it * 32 * kDecWarps sits 2 * it * kDecWarps / 8 row blocks (x 32 rows) lower
-    uint32_t pos[4];
+    constexpr int kIts = Cfg::kDecWarps ? 1024 / (32 * Cfg::kDecWarps) : 1;
+    // row-order pages reaching the shared-memory path (multi-token-tile launches
+    // through the kernel API) map per fragment, not by a fixed stride
+    const bool rows = h->order == 1;
+    uint32_t pos[kIts][4];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) pos[p] = ect_plain_word(dt * 8 + 2 * p) >> 1;
-    constexpr uint32_t kItStride = (32u * Cfg::kDecWarps / 128u) * 16u * 32u;  // u32 per iteration
+    for (int it = 0; it < kIts; ++it)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const uint32_t q = (it * 32 * Cfg::kDecWarps + dt) * 8 + 2 * p;
+        pos[it][p] = (rows ? ect_plain_word_rows(q) : ect_plain_word(q)) >> 1;
+      }
     int s = 0;
     uint32_t round = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -193,19 +215,40 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
         const uint8_t* pg = spg + s * Cfg::kPBytes;
         uint32_t* ta = reinterpret_cast<uint32_t*>(sa + s * Cfg::kABytes);
         const uint32_t page = static_cast<uint32_t>(mt * n_kb + kb);
+        if (tm) {
+          // row r = 32 (warp % 4) + lane of the TMEM lane quarter this warp may
+          // write, k-group cg = 16 k: 16 sign+mantissa bytes + 8 code bytes, one
+          // tcgen05.st of 8 columns (bf16 pairs); no shared-memory A tile, no proxy fence
+          const int r = 32 * (warp & 3) + lane, cg = (warp - 6) >> 2;
+          const uint32_t q0 = static_cast<uint32_t>(cg * 128 + r) * 16;  // first page word
+          const uint4 sm = *reinterpret_cast<const uint4*>(pg + q0);
+          const uint2 nib = *reinterpret_cast<const uint2*>(pg + kEctPageWords + q0 / 2);
+          uint4 w0 = ect_decode8(make_uint2(sm.x, sm.y), nib.x, e0p);
+          uint4 w1 = ect_decode8(make_uint2(sm.z, sm.w), nib.y, e0p);
+          if (ect_escapes(nib.x) | ect_escapes(nib.y))
+            ect_patch16(w0, w1, ect_escapes(nib.x), ect_escapes(nib.y), page, q0, exc_off, exc);
+          tmem_st8(tmem_a + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + s * 32 + cg * 8, w0, w1);
+          tc_fence_before();  // the TMEM stores precede the arrive the MMA thread waits on
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dec[s]);
+          if (++s == Cfg::kStages) {
+            s = 0;
+            ++round;
+          }
+          continue;
+        }
 #pragma unroll
-        for (int it = 0; it < (Cfg::kDecWarps ? 1024 / (32 * Cfg::kDecWarps) : 0); ++it) {
+        for (int it = 0; it < (Cfg::kDecWarps ? kIts : 0); ++it) {
           const uint32_t f = it * 32 * Cfg::kDecWarps + dt;  // fragment
           const uint2 sm = *reinterpret_cast<const uint2*>(pg + f * 8);
           const uint32_t nib = *reinterpret_cast<const uint32_t*>(pg + kEctPageWords + f * 4);
           uint4 w = ect_decode8(sm, nib, e0p);
           const uint32_t esc = ect_escapes(nib);
           if (esc) w = ect_patch8(w, esc, page, f * 8, exc_off, exc);
-          uint32_t* tb = ta + it * kItStride;
-          tb[pos[0]] = w.x;
-          tb[pos[1]] = w.y;
-          tb[pos[2]] = w.z;
-          tb[pos[3]] = w.w;
+          ta[pos[it][0]] = w.x;
+          ta[pos[it][1]] = w.y;
+          ta[pos[it][2]] = w.z;
+          ta[pos[it][3]] = w.w;
         }
         fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
         __syncwarp();

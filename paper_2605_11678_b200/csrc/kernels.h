@@ -199,7 +199,10 @@ struct EctHeader {
   // per page u32: bit r set <=> page words [256 r, 256 r + 256) hold an escape
   // (code 15); 0 = section absent (decoders then test every code)
   uint64_t off_escmask;
-  uint8_t _pad[40];
+  // page word order: 0 = mma.sync A-fragment order (decode GEMV), 1 = row-chunk
+  // order (skinny tcgen05 GEMM decoding into TMEM; ect.py ORDER_ROWS)
+  uint32_t order;
+  uint8_t _pad[36];
 };
 static_assert(sizeof(EctHeader) == 128, "ECT header is 128 bytes");
 // blob -> plain layer bytes (whole 16-byte chunks: out needs a16(total) bytes);

@@ -47,15 +47,31 @@ HEADER = 128
 PAGE_PLAIN = 16384
 PAGE_WORDS = PAGE_PLAIN // 2
 PAGE_BYTES = 12288
-_HDR_FMT = "<IIQQQQQQII16BQ40x"  # ..., n_exc, e0, codebook[16], off_escmask
+_HDR_FMT = "<IIQQQQQQII16BQI36x"  # ..., n_exc, e0, codebook[16], off_escmask, order
+
+# Page word orders (EctHeader.order):
+#   0 (ORDER_MMA)  mma.sync A-fragment order -- the decode GEMV decodes a lane's
+#                  fragments straight into registers (LM layers);
+#   1 (ORDER_ROWS) row-chunk order -- word (g * 128 + r) * 16 + j is row r, k =
+#                  16 g + j of the tile, so a thread of the skinny tcgen05 GEMM
+#                  loads one row's 16 consecutive words (16 + 8 contiguous bytes,
+#                  conflict-free across the warp's 32 rows) and writes them to its
+#                  TMEM lane with one tcgen05.st (the 64-token expert layers).
+ORDER_MMA = 0
+ORDER_ROWS = 1
 
 
-def page_order() -> torch.Tensor:
-    """perm[q] = plain (swizzled tile) word index of page word q.  Fragment
-    f = ((w * 2 + kstep / 2) * 32 + lane) * 2 + kstep % 2 holds the 8 words a
-    decode-GEMV lane feeds to mma.sync m16n8k16 as A registers a0..a3
-    (csrc/common.cuh ect_plain_word)."""
+def page_order(order: int = ORDER_MMA) -> torch.Tensor:
+    """perm[q] = plain (swizzled tile) word index of page word q.
+    ORDER_MMA: fragment f = ((w * 2 + kstep / 2) * 32 + lane) * 2 + kstep % 2
+    holds the 8 words a decode-GEMV lane feeds to mma.sync m16n8k16 as A
+    registers a0..a3 (csrc/common.cuh ect_plain_word).  ORDER_ROWS: word
+    (g * 128 + r) * 16 + j = row r, k = 16 g + j (ect_plain_word_rows)."""
     q = torch.arange(PAGE_WORDS, dtype=torch.int64)
+    if order == ORDER_ROWS:
+        g, r, j = q >> 11, (q >> 4) & 127, q & 15
+        k = 16 * g + j
+        return r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7)
     f, j = q >> 3, q & 7
     w, lane = f >> 7, (f >> 1) & 31
     ks = ((f >> 6) & 1) * 2 + (f & 1)
@@ -67,10 +83,10 @@ def page_order() -> torch.Tensor:
 _PERM: dict = {}
 
 
-def _perm(device) -> torch.Tensor:
-    key = str(device)
+def _perm(device, order: int = ORDER_MMA) -> torch.Tensor:
+    key = (str(device), order)
     if key not in _PERM:
-        _PERM[key] = page_order().to(device)
+        _PERM[key] = page_order(order).to(device)
     return _PERM[key]
 
 
@@ -78,16 +94,16 @@ def _a16(v: int) -> int:
     return (v + 15) // 16 * 16
 
 
-def compress(buf: torch.Tensor, mat_bytes: int) -> torch.Tensor:
+def compress(buf: torch.Tensor, mat_bytes: int, order: int = ORDER_MMA) -> torch.Tensor:
     """uint8 packed layer (any device) whose first `mat_bytes` bytes are 16 KiB
-    weight tiles -> ECT blob (uint8, same device)."""
+    weight tiles -> ECT blob (uint8, same device), pages in `order`."""
     assert buf.dtype == torch.uint8 and buf.dim() == 1
     assert mat_bytes % PAGE_PLAIN == 0 and mat_bytes <= buf.numel(), (mat_bytes, buf.numel())
     dev = buf.device
     total = buf.numel()
     n_pages = mat_bytes // PAGE_PLAIN
     w = buf[:mat_bytes].view(torch.int16).to(torch.int32) & 0xFFFF
-    w = w.view(n_pages, PAGE_WORDS)[:, _perm(dev)].reshape(-1)  # page (fragment) order
+    w = w.view(n_pages, PAGE_WORDS)[:, _perm(dev, order)].reshape(-1)  # page order
     e = (w >> 7) & 0xFF
     cnt = torch.bincount(e, minlength=256 + 15).to(torch.int64)
     win = torch.cumsum(cnt, 0)
@@ -117,7 +133,7 @@ def compress(buf: torch.Tensor, mat_bytes: int) -> torch.Tensor:
     size = _a16(off_exc + 4 * n_exc)
     cb = [e0 + c for c in range(15)] + [0]
     head = struct.pack(_HDR_FMT, MAGIC, n_pages, total, mat_bytes, off_pages, off_tail, off_excoff,
-                       off_exc, n_exc, e0, *cb, off_escmask)
+                       off_exc, n_exc, e0, *cb, off_escmask, order)
     assert len(head) == HEADER
     blob = torch.zeros(size, dtype=torch.uint8, device=dev)
     blob[:HEADER] = torch.frombuffer(bytearray(head), dtype=torch.uint8).to(dev)
@@ -149,6 +165,7 @@ def header(blob: torch.Tensor) -> dict:
     h = dict(zip(keys, f[:10]))
     h["codebook"] = list(f[10:26])
     h["off_escmask"] = f[26]
+    h["order"] = f[27]
     assert h["magic"] == MAGIC, "not an ECT blob"
     return h
 
@@ -172,7 +189,7 @@ def decompress_cpu(blob: torch.Tensor) -> torch.Tensor:
         exp[idx] = exc & 0xFF
     w = ((sm & 0x80) << 8) | (exp << 7) | (sm & 0x7F)
     plain = torch.empty_like(w).view(n_pages, PAGE_WORDS)
-    plain[:, page_order()] = w.view(n_pages, PAGE_WORDS)
+    plain[:, page_order(h["order"])] = w.view(n_pages, PAGE_WORDS)
     w = plain.reshape(-1)
     signed = (w - ((w & 0x8000) << 1)).to(torch.int16).view(torch.uint8)
     tail = b[h["off_tail"]:h["off_tail"] + (h["total"] - mat)]

@@ -251,7 +251,10 @@ class DemandLayeringEngine:
         blobs = []
         for layer in range(self.cfg.layers_of(kind)):
             buf = self._packed_layer(kind, layer)
-            blobs.append(ect.compress(buf, mat))
+            # the 64-token expert's matrices are only read by the single-token-tile
+            # tcgen05 GEMM, which decodes row-order pages straight into TMEM
+            order = ect.ORDER_ROWS if kind == M.KIND_EXPERT else ect.ORDER_MMA
+            blobs.append(ect.compress(buf, mat, order))
             del buf
         self._blob_arena(("ect", kind), blobs, self.lib.ls_exec_set_host_layers_ct, kind)
         sizes = [b.numel() for b in blobs]

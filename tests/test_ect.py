@@ -55,6 +55,22 @@ def test_cpu_roundtrip_no_tail_and_single_page():
     assert torch.equal(ect.decompress_cpu(ect.compress(buf, mat)), buf)
 
 
+@pytest.mark.parametrize("order", [ect.ORDER_MMA, ect.ORDER_ROWS])
+def test_page_orders_are_permutations_and_roundtrip(order):
+    """Both page word orders are permutations of the tile; row order puts a
+    row's 16 consecutive k of one k-group at page words (g * 128 + r) * 16 + j."""
+    perm = ect.page_order(order)
+    assert torch.equal(torch.sort(perm).values, torch.arange(ect.PAGE_WORDS))
+    if order == ect.ORDER_ROWS:
+        r, g, j = 37, 2, 5
+        k = 16 * g + j
+        assert int(perm[(g * 128 + r) * 16 + j]) == r * 64 + (((k >> 3) ^ (r & 7)) << 3) + (k & 7)
+    buf, mat = _layer(5, 300, seed=4)
+    blob = ect.compress(buf, mat, order)
+    assert ect.header(blob)["order"] == order
+    assert torch.equal(ect.decompress_cpu(blob), buf)
+
+
 def test_rejects_unaligned_matrix_region():
     buf, _ = _layer(2, 8)
     with pytest.raises(AssertionError):
@@ -63,9 +79,10 @@ def test_rejects_unaligned_matrix_region():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")
-def test_gpu_decoder_bit_exact():
+@pytest.mark.parametrize("order", [ect.ORDER_MMA, ect.ORDER_ROWS])
+def test_gpu_decoder_bit_exact(order):
     buf, mat = _layer(300, 2 * 4096 + 136, seed=3, device="cuda")
-    blob = ect.compress(buf, mat)
+    blob = ect.compress(buf, mat, order)
     out = ect.decompress_gpu(blob)
     torch.cuda.synchronize()
     assert torch.equal(out, buf)

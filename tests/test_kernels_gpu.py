@@ -357,12 +357,17 @@ def test_gemm_split_k(epi, T, n, k):
 
 
 # epi: 0 BF16, 1 BF16_GELU, 2 RESID_F32, 3 SILU_BF16, 4 F32
-@pytest.mark.parametrize("epi,T,n,k,splitk,page0", [(0, 1024, 6144, 4096, False, 0), (2, 1024, 4096, 4096, False, 5),
-                                                    (3, 200, 1024, 512, False, 0), (2, 64, 2048, 4096, True, 2),
-                                                    (0, 64, 3072, 2048, True, 0), (1, 3072, 1152, 1152, False, 1)])
-def test_gemm_ect_pages_bit_identical(epi, T, n, k, splitk, page0):
-    """tcgen05 GEMM with ECT weight pages decoded into shared memory by decoder
-    warps == the same GEMM over plain tiles, bit for bit (escapes included)."""
+@pytest.mark.parametrize("epi,T,n,k,splitk,page0,order", [
+    (0, 1024, 6144, 4096, False, 0, 0), (2, 1024, 4096, 4096, False, 5, 0), (3, 200, 1024, 512, False, 0, 0),
+    (2, 64, 2048, 4096, True, 2, 0), (0, 64, 3072, 2048, True, 0, 0), (1, 3072, 1152, 1152, False, 1, 0),
+    # row-order pages: decoded into TMEM for single-token-tile launches (the expert),
+    # into the scratch for multi-token-tile ones
+    (2, 64, 2048, 4096, True, 2, 1), (0, 64, 3072, 2048, True, 0, 1), (3, 64, 13824, 2048, True, 3, 1),
+    (3, 16, 512, 320, True, 0, 1), (0, 100, 384, 640, True, 1, 1), (2, 1024, 512, 1024, False, 0, 1)])
+def test_gemm_ect_pages_bit_identical(epi, T, n, k, splitk, page0, order):
+    """tcgen05 GEMM with ECT weight pages decoded in-kernel (shared-memory A tiles
+    for fragment-order pages, TMEM A for row-order pages) == the same GEMM over
+    plain tiles, bit for bit (escapes included)."""
     from paper_2605_11678_b200 import ect
     torch.manual_seed(12)
     w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
@@ -370,8 +375,8 @@ def test_gemm_ect_pages_bit_identical(epi, T, n, k, splitk, page0):
     tiled = K.pack_tiled(w)
     lead = torch.zeros(page0 * ect.PAGE_PLAIN, dtype=torch.uint8, device=DEV)
     layer = torch.cat([lead, tiled.view(torch.uint8).reshape(-1), torch.ones(32, dtype=torch.uint8, device=DEV)])
-    blob = ect.compress(layer, layer.numel() - 32)
-    assert ect.header(blob)["n_exc"] > 0
+    blob = ect.compress(layer, layer.numel() - 32, order)
+    assert ect.header(blob)["n_exc"] > 0 and ect.header(blob)["order"] == order
     x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
     ncol = n // 2 if epi == 3 else n
     odt = torch.float32 if epi in (2, 4) else torch.bfloat16

@@ -118,7 +118,7 @@ def bench_ect_decode(nbytes=385_892_352, copies=2):
     return {"kernel": f"ect_decode {nbytes} B", "us": ms * 1e3, "GBps_moved": moved / (ms * 1e6)}
 
 
-def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False, ct=False):
+def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False, ct=False, order=None):
     dev = "cuda"
     # rotate weight copies so skinny (weight-bound) shapes stream from HBM, not L2
     copies = max(1, min(12, (256 << 20) // (n * k * 2)))
@@ -126,7 +126,9 @@ def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False, ct=False):
     blobs = None
     if ct:
         from paper_2605_11678_b200 import ect
-        blobs = [ect.compress(w.view(torch.uint8).reshape(-1), w.view(torch.uint8).numel()) for w in ws_]
+        # row-order pages (TMEM A) for single-token-tile launches, as the engine stores the expert
+        order = (ect.ORDER_ROWS if T <= 64 else ect.ORDER_MMA) if order is None else order
+        blobs = [ect.compress(w.view(torch.uint8).reshape(-1), w.view(torch.uint8).numel(), order) for w in ws_]
     x = torch.randn(T, k, device=dev).to(torch.bfloat16)
     ncol = n // 2 if epi == K.GEMM_SILU_BF16 else n
     out = torch.zeros(T, ncol, dtype=torch.bfloat16 if epi != K.GEMM_RESID_F32 else torch.float32,
@@ -140,7 +142,8 @@ def bench_gemm(T, n, k, epi=K.GEMM_BF16, splitk=False, ct=False):
         it[0] += 1
     ms = timed(run)
     f = 2.0 * T * n * k
-    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}" + (" splitk" if splitk else "") + (" ect" if ct else ""),
+    return {"kernel": f"gemm epi={epi} T={T} {n}x{k}" + (" splitk" if splitk else "") +
+            (f" ect order={order}" if ct else ""),
             "us": ms * 1e3,
             "TFLOPs": f / (ms * 1e9), "weight_GBps": n * k * 2 / (ms * 1e6)}
 
@@ -208,7 +211,8 @@ def main():
         for T, n, k, epi in ((64, 2048, 4096, K.GEMM_RESID_F32), (64, 2048, 6912, K.GEMM_RESID_F32),
                              (64, 6144, 2048, K.GEMM_BF16), (64, 13824, 2048, K.GEMM_SILU_BF16)):
             res.append(bench_gemm(T, n, k, epi, splitk=True))
-            res.append(bench_gemm(T, n, k, epi, splitk=True, ct=True))
+            res.append(bench_gemm(T, n, k, epi, splitk=True, ct=True, order=0))
+            res.append(bench_gemm(T, n, k, epi, splitk=True, ct=True, order=1))
     if args.only in ("all", "ect"):
         res.append(bench_gemv_ect(24576, 4096, K.GEMV_SILU))
         res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
