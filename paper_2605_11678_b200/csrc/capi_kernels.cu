@@ -103,7 +103,13 @@ int ls_k_gemm_ws(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const v
   a.sk_cnt_n = sk_cnt_n;
   a.ct_blob = static_cast<const uint8_t*>(ct_blob);
   a.ct_page0 = ct_page0;
-  if (ct_blob) a.w = static_cast<const uint8_t*>(ct_blob) + sizeof(EctHeader) + static_cast<long>(ct_page0) * kEctPageBytes;
+  if (ct_blob) {
+    a.w = static_cast<const uint8_t*>(ct_blob) + sizeof(EctHeader) + static_cast<long>(ct_page0) * kEctPageBytes;
+    EctHeader h;  // kernel-API entry point (tests / tools): the page order from the device header
+    if (cudaMemcpy(&h, ct_blob, sizeof(h), cudaMemcpyDefault) != cudaSuccess)
+      return set_error(LS_ERR_CUDA, "ls_k_gemm_ws: cannot read the ECT header");
+    a.ct_order = static_cast<int>(h.order);
+  }
   return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm_ws");
 }
 

@@ -220,6 +220,7 @@ struct Module {
   // host arena, DFB slots and resident blocks hold ECT blobs; EXE decodes
   // (or the decode GEMV reads pages directly)
   bool ct = false;
+  int ct_order = 0;  // EctHeader.order of the module's blobs (1: expert, A decoded into TMEM)
   std::vector<const char*> host_ct;
   std::vector<uint64_t> ct_bytes;
   uint64_t ct_stride = 0;  // resident footprint per layer (largest blob, 256-aligned)
@@ -345,8 +346,9 @@ int tmap(CUtensorMap* m, const void* base, int rows, int cols, int ld) {
 struct CtView {
   const char* blob = nullptr;  // nullptr: plain layer
   uint64_t mat = 0, tail = 0;
+  int order = 0;  // EctHeader.order of the module's blobs
   CtView() = default;
-  CtView(const char* b, const ls_layer_layout& L) : blob(b) {
+  CtView(const char* b, const ls_layer_layout& L, int o = 0) : blob(b), order(o) {
     mat = L.offset[3] + L.bytes[3];
     tail = align_up(sizeof(EctHeader) + mat / 16384 * kEctPageBytes, 16);
   }
@@ -360,8 +362,9 @@ struct CtView {
 
 int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensorMap& map, void* out,
          long ldo, const void* bias_bf16 = nullptr, int n_valid = -1, const char* ct_blob = nullptr,
-         int ct_page0 = 0) {
+         int ct_page0 = 0, int ct_order = 0) {
   GemmArgs a{};
+  a.ct_order = ct_order;
   if (ct_blob && (T + gemm_block_n(T) - 1) / gemm_block_n(T) > 1) {
     // several token tiles would each re-decode every page inside the GEMM: expand
     // this matrix's pages once into the decode scratch and run the plain GEMM on it
@@ -449,9 +452,10 @@ int tp_allreduce_inplace(ls_exec* e, float* dst, long count) {
 }
 
 int resid_gemm(ls_exec* e, const char* w, int n, int k, int T, const CUtensorMap& map, float* dst,
-               const void* bias_bf16 = nullptr, const char* ct_blob = nullptr, int ct_page0 = 0) {
+               const void* bias_bf16 = nullptr, const char* ct_blob = nullptr, int ct_page0 = 0,
+               int ct_order = 0) {
   const int epi = (!e->tp_on || e->tp_rank == 0) ? GEMM_RESID_F32 : GEMM_F32;
-  RC(gemm(e, epi, w, n, k, T, map, dst, n, bias_bf16, -1, ct_blob, ct_page0));
+  RC(gemm(e, epi, w, n, k, T, map, dst, n, bias_bf16, -1, ct_blob, ct_page0, ct_order));
   return e->tp_on ? tp_allreduce_inplace(e, dst, static_cast<long>(T) * n) : LS_OK;
 }
 
@@ -590,7 +594,8 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   const long shift = static_cast<long>(e->ctx) * d.ex_hd;  // store index t, RoPE position ctx + t
   const uint32_t skip = e->diag_skip;
   if (!(skip & 1)) KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(4), e->ex_norm, T, D, d.lm_eps, e->ss));
-  if (!(skip & 8)) RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0)));
+  const int co = ct.order;
+  if (!(skip & 8)) RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0), co));
   if (!(skip & 2)) KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
                          (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], e->ctx, e->ex_q,
                          ek - shift, ev - shift, T * d.ex_hd, e->ss));
@@ -617,12 +622,12 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   f.ws = e->flash_ws;
   f.counters = e->flash_cnt;
   if (!(skip & 4)) KL(launch_flash_attention(f, e->ss));
-  if (!(skip & 16)) RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h, nullptr, cb, pg(1)));
+  if (!(skip & 16)) RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h, nullptr, cb, pg(1), co));
   if (!(skip & 1)) KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
   if (!(skip & 32))
     RC(gemm(e, GEMM_SILU_BF16, part(2), 2 * d.ex_ffn, D, T, e->m_ex_norm, e->ex_mlp, d.ex_ffn,
-            nullptr, d.ex_ffn, cb, pg(2)));
-  if (!(skip & 64)) RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, nullptr, cb, pg(3)));
+            nullptr, d.ex_ffn, cb, pg(2), co));
+  if (!(skip & 64)) RC(resid_gemm(e, part(3), D, d.ex_ffn, T, e->m_ex_mlp, e->ex_h, nullptr, cb, pg(3), co));
   return LS_OK;
 }
 
@@ -1095,6 +1100,10 @@ int ls_exec_set_host_layers_ct(ls_exec* e, int32_t kind, const void* const* host
     m.ct_bytes.assign(bytes, bytes + n);
     m.ct_stride = align_up(worst, 256);
     m.ct = true;
+    m.ct_order = static_cast<int>(reinterpret_cast<const EctHeader*>(host_ptrs[0])->order);
+    for (int i = 1; i < n; ++i)
+      if (static_cast<int>(reinterpret_cast<const EctHeader*>(host_ptrs[i])->order) != m.ct_order)
+        return set_error(LS_ERR_VALUE, "ECT blobs of module kind %d mix page orders", kind);
     return finalize_layout(e);
   }
   return set_error(LS_ERR_VALUE, "module kind %d not present", kind);
@@ -1305,7 +1314,7 @@ int ls_exec_run(ls_exec* e, const ls_run_io* io, const ls_run_opts* opts, ls_eve
           int x0 = timing ? tick(e->ss) : -1;
           CtView ct;
           if (m.ct && e->ct_fused) {
-            ct = CtView(w, m.lay);  // GEMV / GEMM kernels read the blob's pages directly
+            ct = CtView(w, m.lay, m.ct_order);  // GEMV / GEMM kernels read the blob's pages directly
           } else if (m.ct) {
             // compact layer (slot or resident block) -> plain layer in the scratch;
             // the next kernel must not start early: its weight producer reads the scratch

@@ -26,19 +26,21 @@ namespace lsb {
 // CT = true: weights arrive as ECT pages (12 KiB) in a staging ring and 8
 // decoder warps expand each into the swizzled 16 KiB A tile in shared memory
 // (no decoded copy of the layer in HBM, 25 % fewer weight bytes).
-template <int BN, bool CT = false>
+// TM = true (CT, BN <= 128, row-order pages): A is decoded into TMEM, so a
+// stage is just a page + an activation tile and the ring is twice as deep.
+template <int BN, bool CT = false, bool TM = false>
 struct GemmCfg {
-  static constexpr int kStages = CT ? (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5))
-                                    : (BN >= 256 ? 4 : (BN >= 128 ? 6 : 8));
-  static constexpr int kABytes = kTileBytes;
+  static constexpr int kStages = TM ? (BN >= 128 ? 6 : 10)
+                                    : CT ? (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5))
+                                         : (BN >= 256 ? 4 : (BN >= 128 ? 6 : 8));
+  static constexpr int kABytes = TM ? 0 : kTileBytes;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kPBytes = CT ? kEctPageBytes : 0;  // page staging
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kAccCols = BN < 32 ? 32 : BN;     // one accumulator
-  // double-buffered accumulators; single-token-tile ECT launches (BN <= 128) also
-  // hold the decoded A stages in TMEM (32 columns each) for row-order pages
-  static constexpr bool kTmA = CT && BN <= 128;
-  static constexpr int kTmemCols = kTmA ? 512 : 2 * kAccCols;
+  // double-buffered accumulators (+ the decoded A stages, 32 columns each, for TM)
+  static_assert(!TM || (CT && 2 * (BN < 32 ? 32 : BN) + 32 * kStages <= 512), "TMEM budget");
+  static constexpr int kTmemCols = TM ? 512 : 2 * kAccCols;
   static constexpr int kDecWarps = CT ? 16 : 0;
   static constexpr int kThreads = 192 + 32 * kDecWarps;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * (kStageBytes + kPBytes) +
@@ -49,10 +51,10 @@ struct GemmCfg {
 // are ordered token-tile fastest, so the CTAs working on one weight m-tile at
 // the same time share it through L2 (each weight byte read from HBM ~once).
 // Two TMEM accumulators: the epilogue of tile i overlaps the MMAs of tile i+1.
-template <int BN, int EPI, bool CT>
-__global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
+template <int BN, int EPI, bool CT, bool TM = false>
+__global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmArgs a) {
-  using Cfg = GemmCfg<BN, CT>;
+  using Cfg = GemmCfg<BN, CT, TM>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
@@ -94,10 +96,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // row-order ECT pages (EctHeader.order 1): the decoders write A straight into
-  // TMEM (tcgen05.st, one row per lane) and the MMA reads it from there
-  bool tm = false;
-  if constexpr (Cfg::kTmA) tm = reinterpret_cast<const EctHeader*>(a.ct_blob)->order == 1;
+  // TM (row-order ECT pages, EctHeader.order 1): the decoders write A straight
+  // into TMEM (tcgen05.st, one row per lane) and the MMA reads it from there
+  constexpr bool tm = TM;
   const uint32_t tmem_a = tmem + 2 * Cfg::kAccCols;  // A stage s at column +32 s
 
   if (warp == 0) {
@@ -487,12 +488,12 @@ int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_
   return ks < 1 ? 1 : ks;
 }
 
-template <int BN, int EPI, bool CT>
+template <int BN, int EPI, bool CT, bool TM = false>
 static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
-  using Cfg = GemmCfg<BN, CT>;
+  using Cfg = GemmCfg<BN, CT, TM>;
   static DeviceFlags attr;
   if (!attr.done()) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI, CT>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI, CT, TM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
@@ -509,26 +510,28 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   if (ks_cap > 0 && b.ks > ks_cap) b.ks = ks_cap;
   const int units = a.n_mt * ((a.T + BN - 1) / BN) * b.ks;
   dim3 grid(units < nsm ? units : nsm);
-  return launch_k(gemm_kernel<BN, EPI, CT>, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, map, b);
+  return launch_k(gemm_kernel<BN, EPI, CT, TM>, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, map, b);
 }
 
-template <int BN, bool CT>
+template <int BN, bool CT, bool TM = false>
 static cudaError_t launch_epi(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
   switch (epi) {
-    case GEMM_BF16: return launch_bn<BN, GEMM_BF16, CT>(a, map, st);
-    case GEMM_BF16_GELU: return launch_bn<BN, GEMM_BF16_GELU, CT>(a, map, st);
-    case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32, CT>(a, map, st);
-    case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16, CT>(a, map, st);
-    case GEMM_F32: return launch_bn<BN, GEMM_F32, CT>(a, map, st);
+    case GEMM_BF16: return launch_bn<BN, GEMM_BF16, CT, TM>(a, map, st);
+    case GEMM_BF16_GELU: return launch_bn<BN, GEMM_BF16_GELU, CT, TM>(a, map, st);
+    case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32, CT, TM>(a, map, st);
+    case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16, CT, TM>(a, map, st);
+    case GEMM_F32: return launch_bn<BN, GEMM_F32, CT, TM>(a, map, st);
   }
   return cudaErrorInvalidValue;
 }
 
 template <bool CT>
 static cudaError_t launch_ct(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  // row-order pages on a single-token-tile launch: A decoded into TMEM
+  const bool tm = CT && a.ct_order == 1 && a.T <= gemm_block_n(a.T);
   switch (gemm_block_n(a.T)) {
-    case 64: return launch_epi<64, CT>(epi, a, map, st);
-    case 128: return launch_epi<128, CT>(epi, a, map, st);
+    case 64: return tm ? launch_epi<64, true, true>(epi, a, map, st) : launch_epi<64, CT>(epi, a, map, st);
+    case 128: return tm ? launch_epi<128, true, true>(epi, a, map, st) : launch_epi<128, CT>(epi, a, map, st);
     default: return launch_epi<256, CT>(epi, a, map, st);
   }
 }

@@ -92,6 +92,7 @@ struct GemmArgs {
   // 1: w was written by the previous kernel (ECT decode scratch) -- no weight
   // tile is requested before griddepcontrol.wait
   int w_dep;
+  int ct_order;  // EctHeader.order of ct_blob (1: row order -> A decoded into TMEM)
 };
 
 int gemm_block_n(int T);
