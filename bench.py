@@ -185,8 +185,11 @@ def concurrent_h2d_probe(torch, dist, device, world, nbytes=1 << 30, reps=4) -> 
 
 def gemv_microbench(torch, device, n, k, reps=30, ect_pages=False):
     """Dominant decode kernel alone: gate|up GEMV (+fused RMSNorm, SiLU*up),
-    over plain tiles or (ect_pages) the ECT pages the engine actually stores.
-    Timed with CUDA events on the stream it is launched on."""
+    over plain tiles or (ect_pages) the ECT pages the engine actually stores,
+    launched as the executor launches it in the step (programmatic dependent
+    launch: a launch's barrier setup and first weight pages overlap the previous
+    launch's tail).  Timed with CUDA events on the stream it is launched on;
+    `ms_no_pdl` is the same loop with plain serialised launches."""
     from paper_2605_11678_b200 import ect
     from paper_2605_11678_b200 import kernels as K
     w = K.pack_tiled((torch.randn(n, k, device=device) * 0.02).to(torch.bfloat16))
@@ -201,24 +204,29 @@ def gemv_microbench(torch, device, n, k, reps=30, ect_pages=False):
     ws = K.GemvWorkspace(device)
     s = torch.cuda.Stream(device)
 
-    def launch(i):
+    def launch(i, pdl):
         K.gemv(K.GEMV_SILU, copies[i % 3], n, k, x, out, ws, norm_w=nw, n_valid=n // 2, stream=s,
-               ct_blob=blobs[i % 3] if blobs else None)
-    with torch.cuda.stream(s):
-        for i in range(5):
-            launch(i)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for i in range(reps):
-            launch(i)
-        e1.record(s)
-    s.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+               ct_blob=blobs[i % 3] if blobs else None, pdl=pdl)
+
+    def loop(pdl):
+        with torch.cuda.stream(s):
+            for i in range(5):
+                launch(i, False)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            launch(0, False)  # the first launch after the event record: no PDL edge across it
+            for i in range(1, reps):
+                launch(i, pdl)
+            e1.record(s)
+        s.synchronize()
+        return e0.elapsed_time(e1) / reps
+    ms_plain = loop(False)
+    ms = loop(True)
     # ECT: 12 KiB page + 16 B escape mask per 16 KiB tile (the bytes the kernel moves)
     w_bytes = n * k * 2 * 3 // 4 + (n * k * 2 // 16384) * 16 if ect_pages else n * k * 2
     algo_bytes = w_bytes + k * 4 + k * 2 + (n // 2) * 4
     return {"bytes": algo_bytes, "ms": ms, "gbs": algo_bytes / (ms * 1e6),
-            "plain_equiv_gbs": (n * k * 2) / (ms * 1e6)}
+            "plain_equiv_gbs": (n * k * 2) / (ms * 1e6), "ms_no_pdl": ms_plain}
 
 
 def gemm_microbench(torch, device, T, n, k, reps=20):
@@ -645,7 +653,8 @@ def main():
                                             f"{n_gu}x{cfg.lm_d}"),
                      "kernel": f"{'gemv_ect_kernel<SILU> (ECT pages)' if ect_dec else 'gemv_kernel<SILU>'} gate|up "
                                f"{n_gu}x{cfg.lm_d} bf16 ({gv['bytes']} algorithmic B/launch, "
-                               f"{gv['ms'] * 1e3:.1f} us)",
+                               f"{gv['ms'] * 1e3:.1f} us PDL-chained as in the step; "
+                               f"{gv['ms_no_pdl'] * 1e3:.1f} us with serialised launches)",
                      "plain_equivalent_gbs": gv["plain_equiv_gbs"],
                      "plain_tile_kernel": {"gbs": gv_plain["gbs"], "us": gv_plain["ms"] * 1e3,
                                            "frac": gv_plain["gbs"] / peaks["hbm_gbs"],

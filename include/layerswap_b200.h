@@ -298,6 +298,11 @@ int ls_num_sms(int device, int32_t* out);
 int ls_gemv_plan(int32_t n_mt, int32_t n_kb, int32_t num_sms, int32_t* grid, int32_t* max_contrib);
 /* args points at the GemvArgs / DecodeAttnArgs / FlashArgs blocks of csrc/kernels.h */
 int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream);
+/* Programmatic dependent launch for the NEXT ls_k_* launch of this thread (how the
+   executor launches every in-step kernel: its prologue -- barrier init, weight
+   prefetch -- overlaps the previous kernel's tail; it reads activations only
+   after griddepcontrol.wait). */
+int ls_set_launch_pdl(int32_t on);
 int ls_k_gemm(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, const void* x,
               int32_t T, int64_t ldx, void* out, int64_t ldo, const float* bias,
               const void* bias_bf16, int32_t n_valid, void* stream);

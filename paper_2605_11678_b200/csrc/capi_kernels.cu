@@ -53,6 +53,11 @@ int ls_gemv_plan(int32_t n_mt, int32_t n_kb, int32_t num_sms, int32_t* grid, int
   return LS_OK;
 }
 
+int ls_set_launch_pdl(int32_t on) {
+  set_launch_pdl(on != 0);
+  return LS_OK;
+}
+
 int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream) {
   return cuda_rc(launch_gemv(epi, *static_cast<const GemvArgs*>(args), grid,
                              static_cast<cudaStream_t>(stream)),

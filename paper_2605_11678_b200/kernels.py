@@ -61,6 +61,7 @@ def _lib():
             "ls_gemv_plan": [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                              C.POINTER(C.c_int32)],
             "ls_k_gemv": [C.c_int32, _vp, C.c_int32, _vp],
+            "ls_set_launch_pdl": [C.c_int32],
             "ls_k_gemm": [C.c_int32, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int64, _vp,
                           C.c_int64, _vp, _vp, C.c_int32, _vp],
             "ls_k_gemm_ws": [C.c_int32, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int64, _vp,
@@ -155,9 +156,10 @@ class GemvWorkspace:
 
 def gemv(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: torch.Tensor,
          ws: GemvWorkspace, *, norm_w=None, eps=1e-6, bias=None, n_valid=None, qkv=None,
-         amax=None, grid=None, stream=None, ct_blob=None, ct_page0=0):
+         amax=None, grid=None, stream=None, ct_blob=None, ct_page0=0, pdl=False):
     """w_tiled: plain tiles, or (ct_blob given) an ECT blob whose pages
-    ct_page0.. hold this matrix -- the GEMV then decodes pages in registers."""
+    ct_page0.. hold this matrix -- the GEMV then decodes pages in registers.
+    pdl: launch with programmatic dependent launch, as the executor does."""
     n_mt, n_kb = tile_dims(n, k)
     lib = _lib()
     g, mc = C.c_int32(), C.c_int32()
@@ -173,6 +175,8 @@ def gemv(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: 
     if qkv is not None:
         for key, val in qkv.items():
             setattr(a, key, _p(val) if isinstance(val, torch.Tensor) else val)
+    if pdl:
+        lib.ls_set_launch_pdl(1)
     _native.check(lib.ls_k_gemv(epi, C.byref(a), g.value, _stream(stream)), RuntimeError)
 
 
