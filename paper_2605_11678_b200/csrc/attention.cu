@@ -268,10 +268,17 @@ struct FlashCfg {
 // flight (2 = double buffering; the split-KV expert launch, one CTA per SM with a
 // few blocks each, keeps NS - 1 blocks ahead so L2/HBM latency is not exposed
 // per block).
-template <int HD, int G = 1, int NS = 2>
-__global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
+//
+// KG = 2 (key groups): a second set of 4 G warps takes every other key block of
+// the same queries (own running max / sum / O, merged in group order at the end),
+// halving the per-warp chain -- the split-KV expert launch has one CTA per SM and
+// only a few blocks per CTA, so its latency, not its math, is the cost.
+template <int HD, int G = 1, int NS = 2, int KG = 1>
+__global__ void __launch_bounds__(128 * G * KG) flash_kernel(const FlashArgs a) {
+  static_assert(NS % KG == 0, "whole rounds of KG blocks per stage group");
   using Cfg = FlashCfg<HD>;
-  constexpr int NT = 128 * G;
+  constexpr int NT = 128 * G * KG;
+  constexpr int NR = NS / KG;  // rounds of KG blocks in flight
   constexpr int DK = Cfg::kDK, LD = Cfg::kLd, ND = Cfg::kND, BM = Cfg::kBM, BN = Cfg::kBN;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(16) uint8_t fsm[];
@@ -281,7 +288,8 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   pdl_trigger();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hw = warp >> 2, wr = warp & 3;  // head of this warp within the CTA, row block
+  const int kg = warp / (4 * G);                     // key group
+  const int hw = (warp >> 2) % G, wr = warp & 3;      // head of this warp within the CTA, row block
   const int h = static_cast<int>(blockIdx.y) * G + hw, kvh = static_cast<int>(blockIdx.y) * G / (a.hq / a.hkv);
   const int q0 = blockIdx.x * BM;
   const int g = lane >> 2, t4 = lane & 3;
@@ -328,7 +336,7 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
     cp_async16(kd, kp, ok);
     cp_async16(vd, vp, ok);
   };
-  auto load_kv = [&](int buf, int j0) {
+  auto load_kv_nocommit = [&](int buf, int j0) {
     bf16* kb = ks_buf + buf * BN * LD;
     bf16* vb = vs_buf + buf * BN * LD;
     if constexpr (NT % CPR == 0) {
@@ -353,7 +361,6 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
         cp_async16(vd, vp, ok);
       }
     }
-    cp_async_commit();
   };
   // ldmatrix source row / column of this lane for K^T fragments: matrices
   // 0..3 = dims +0, +8, +16, +24 of a k-step pair, rows = the 8 keys of n-tile
@@ -364,9 +371,20 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   // the first NS - 1 blocks are requested before griddepcontrol.wait when they lie
   // in a segment the previous kernel did not write (the expert over the VLM cache)
   const int nblk = k_begin < k_end ? (k_end - k_begin + BN - 1) / BN : 0;
-  int issued = 0;
-  while (issued < NS - 1 && issued < nblk && a.k1_ready && k_begin + (issued + 1) * BN <= a.len1) {
-    load_kv(issued % NS, k_begin + issued * BN);
+  // round r = blocks r KG .. r KG + KG - 1 (block jb in stage jb % NS), one
+  // cp.async group per round; NR - 1 rounds are requested ahead
+  auto issue_round = [&](int r) {
+#pragma unroll
+    for (int i = 0; i < KG; ++i) {
+      const int jb = r * KG + i;
+      if (jb < nblk) load_kv_nocommit(jb % NS, k_begin + jb * BN);
+    }
+    cp_async_commit();
+  };
+  int issued = 0;  // rounds
+  while (issued < NR - 1 && issued * KG < nblk && a.k1_ready &&
+         k_begin + min(nblk, (issued + 1) * KG) * BN <= a.len1) {
+    issue_round(issued);
     ++issued;
   }
   pdl_wait();
@@ -395,19 +413,20 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   float o[ND][4];
 #pragma unroll
   for (int j = 0; j < ND; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  for (; issued < NS - 1; ++issued) {  // empty groups keep the group count uniform
-    if (issued < nblk) load_kv(issued % NS, k_begin + issued * BN);
-    else cp_async_commit();
-  }
-  int buf = 0;
-  for (int j0 = k_begin, jb = 0; j0 < k_end; j0 += BN, ++jb, buf = (buf + 1 == NS ? 0 : buf + 1)) {
-    // block jb + NS - 1 into the stage block jb - 1 used (freed by the loop's final barrier)
-    if (jb + NS - 1 < nblk) load_kv((jb + NS - 1) % NS, j0 + (NS - 1) * BN);
-    else cp_async_commit();
-    cp_async_wait<NS - 1>();  // block jb has landed
+  for (; issued < NR - 1; ++issued) issue_round(issued);  // (empty groups keep the count uniform)
+  for (int r = 0; r * KG < nblk; ++r) {
+    // round r + NR - 1 into the stages round r - 1 used (freed by the loop's final barrier)
+    issue_round(r + NR - 1);
+    cp_async_wait<NR - 1>();  // round r has landed
     __syncthreads();
-    const bf16* ks = ks_buf + buf * BN * LD;
-    const bf16* vs = vs_buf + buf * BN * LD;
+    const int jb = r * KG + kg;
+    if (jb >= nblk) {  // this group has no block in the last round
+      __syncthreads();
+      continue;
+    }
+    const int j0 = k_begin + jb * BN;
+    const bf16* ks = ks_buf + (jb % NS) * BN * LD;
+    const bf16* vs = vs_buf + (jb % NS) * BN * LD;
     // S = Q K^T  (16 x 64 per warp); K^T fragments by ldmatrix (two k-steps per x4)
     float s[BN / 8][4];
 #pragma unroll
@@ -488,7 +507,46 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
         mma_bf16_16816(o[dt], pa, b0, b1);
       }
     }
-    __syncthreads();  // everyone is done with `buf` before the next prefetch overwrites it
+    __syncthreads();  // everyone is done with the round's stages before the next prefetch overwrites them
+  }
+  if constexpr (KG > 1) {
+    // ---- key groups -> group 0 (group order, deterministic); the K/V stages are free ----
+    cp_async_wait<0>();
+    float* xg = reinterpret_cast<float*>(ks_buf);  // [KG - 1][4 G warps][32 lanes][ND * 4 + 4]
+    constexpr int W = ND * 4 + 4;
+    const int slot = (warp % (4 * G)) * 32 + lane;
+    if (kg > 0) {
+      float* d = xg + ((kg - 1) * 4 * G * 32 + slot) * W;
+#pragma unroll
+      for (int j = 0; j < ND; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) d[j * 4 + e] = o[j][e];
+      d[ND * 4 + 0] = mrow[0];
+      d[ND * 4 + 1] = mrow[1];
+      d[ND * 4 + 2] = lrow[0];
+      d[ND * 4 + 3] = lrow[1];
+    }
+    __syncthreads();
+    // (group-k warps stay resident: the merges below use block-wide barriers)
+#pragma unroll
+    for (int q = 1; q < KG; ++q) {
+      if (kg > 0) break;
+      const float* d = xg + ((q - 1) * 4 * G * 32 + slot) * W;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const float m2 = d[ND * 4 + r], l2 = d[ND * 4 + 2 + r];
+        const float mn = fmaxf(mrow[r], m2);
+        const float base = mn == -INFINITY ? 0.f : mn;
+        const float c1 = exp2f(mrow[r] - base), c2 = exp2f(m2 - base);
+        lrow[r] = lrow[r] * c1 + l2 * c2;
+        mrow[r] = mn;
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {
+          o[j][2 * r] = o[j][2 * r] * c1 + d[j * 4 + 2 * r] * c2;
+          o[j][2 * r + 1] = o[j][2 * r + 1] * c1 + d[j * 4 + 2 * r + 1] * c2;
+        }
+      }
+    }
   }
   if (splits > 1) {
     // ---- split-KV merge inside the thread-block cluster (the splits of one
@@ -503,7 +561,7 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
     float* rec = reinterpret_cast<float*>(fsm);  // [RT][W]: o unnormalised, m, l
     __syncthreads();                             // K/V buffers are free
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 2 && kg == 0; ++r) {
       const int row = hw * BM + wr * 16 + g + 8 * r;
 #pragma unroll
       for (int dt = 0; dt < ND; ++dt) {
@@ -560,7 +618,7 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   // normalise + store
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    if (qi[r] >= a.Tq) continue;
+    if (qi[r] >= a.Tq || kg > 0) continue;
     const float inv = lrow[r] > 0.f ? 1.0f / lrow[r] : 0.f;
     bf16* op = a.out + static_cast<long>(qi[r]) * a.o_tok_stride + static_cast<long>(h) * a.o_head_stride;
 #pragma unroll
@@ -570,13 +628,13 @@ __global__ void __launch_bounds__(128 * G) flash_kernel(const FlashArgs a) {
   }
 }
 
-template <int HD, int G = 1, int NS = 2>
+template <int HD, int G = 1, int NS = 2, int KG = 1>
 static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   using Cfg = FlashCfg<HD>;
   const size_t smem = static_cast<size_t>(G * Cfg::kBM + 2 * NS * Cfg::kBN) * Cfg::kLd * 2;
   static DeviceFlags attr;
   if (!attr.done()) {
-    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD, G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(flash_kernel<HD, G, NS, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr.mark();
@@ -588,7 +646,7 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
     return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(128 * G);
+  cfg.blockDim = dim3(128 * G * KG);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute la[2];
@@ -600,7 +658,7 @@ static cudaError_t flash_hd(const FlashArgs& a, cudaStream_t st) {
   la[1].val.clusterDim.z = static_cast<unsigned>(splits);
   cfg.attrs = la;
   cfg.numAttrs = splits > 1 ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, flash_kernel<HD, G, NS>, a);
+  return cudaLaunchKernelEx(&cfg, flash_kernel<HD, G, NS, KG>, a);
 }
 
 int flash_kv_splits(int Tq, int hq, int n_keys, int num_sms) {
@@ -640,6 +698,11 @@ cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st) {
         const char* v = std::getenv("LS_DIAG_FLASH_NS");
         return v ? std::atoi(v) : 4;
       }();
+      static const int kgs = [] {  // LS_DIAG_FLASH_KG: key groups (diagnostics)
+        const char* v = std::getenv("LS_DIAG_FLASH_KG");
+        return v ? std::atoi(v) : 2;
+      }();
+      if (kgs == 2 && ns >= 4) return flash_hd<128, 1, 4, 2>(a, st);
       return ns <= 2 ? flash_hd<128>(a, st) : ns == 3 ? flash_hd<128, 1, 3>(a, st) : flash_hd<128, 1, 4>(a, st);
     }
   }
