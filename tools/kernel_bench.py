@@ -95,6 +95,51 @@ def bench_gemv_ect(n, k, epi=K.GEMV_F32, copies=4):
             "plain_equiv_GBps": plain / (ms * 1e6)}
 
 
+def bench_gemv_ect_tails(n=24576, k=4096, copies=3):
+    """ECT on heavier-tailed weights than N(0, 0.02): Student-t (df 3 and 5) and a
+    mixture with 0.1 % outliers x 50, same 0.02 scale.  Reports the escape rate
+    (exception entries / words), the blob's size vs plain, and the gate|up
+    decode GEMV time (escape patches are the slow path)."""
+    from paper_2605_11678_b200 import ect
+    dev = "cuda"
+    out_rows = []
+    g = torch.Generator(device=dev).manual_seed(5)
+    dists = {
+        "normal": lambda: torch.randn(n, k, device=dev, generator=g),
+        "student_t_df5": lambda: torch.distributions.StudentT(5.0).sample((n, k)).to(dev),
+        "student_t_df3": lambda: torch.distributions.StudentT(3.0).sample((n, k)).to(dev),
+        "outliers_0.1pct_x50": lambda: torch.randn(n, k, device=dev, generator=g) *
+        torch.where(torch.rand(n, k, device=dev, generator=g) < 1e-3, 50.0, 1.0),
+    }
+    for name, gen in dists.items():
+        blobs = []
+        n_exc = 0
+        for _ in range(copies):
+            w = (gen() * 0.02).to(torch.bfloat16)
+            t = K.pack_tiled(w).view(torch.uint8).reshape(-1)
+            b = ect.compress(t, t.numel())
+            n_exc = ect.header(b)["n_exc"]
+            blobs.append(b)
+            del w, t
+        x = torch.randn(k, device=dev)
+        nw = torch.ones(k, dtype=torch.bfloat16, device=dev)
+        out = torch.zeros(n, device=dev)
+        ws = K.GemvWorkspace(dev)
+        it = [0]
+
+        def run():
+            b = blobs[it[0] % copies]
+            it[0] += 1
+            K.gemv(K.GEMV_SILU, None, n, k, x, out, ws, norm_w=nw, n_valid=n // 2, ct_blob=b)
+        ms = timed(run)
+        out_rows.append({"weights": name, "escape_rate": n_exc / (n * k), "blob_over_plain":
+                         blobs[0].numel() / (n * k * 2), "gemv_us": ms * 1e3,
+                         "pages_GBps": blobs[0].numel() / (ms * 1e6)})
+        del blobs
+        torch.cuda.empty_cache()
+    return out_rows
+
+
 def bench_ect_decode(nbytes=385_892_352, copies=2):
     from paper_2605_11678_b200 import ect
     dev = "cuda"
@@ -218,6 +263,8 @@ def main():
         res.append(bench_gemv_ect(4096, 12288, K.GEMV_RESID))
         res.append(bench_gemv_ect(6144, 4096, K.GEMV_F32))
         res.append(bench_ect_decode())
+    if args.only == "ect_tails":
+        res.extend(bench_gemv_ect_tails())
     if args.only == "ectgemm_gu":
         res.append(bench_gemm(64, 13824, 2048, K.GEMM_SILU_BF16, splitk=True, ct=True))
     if args.only == "plaingemm_gu":
