@@ -11,7 +11,8 @@
 //     SWIZZLE_128B -- both land in the UMMA K-major SW128 layout;
 //   * warp 0: TMA producer, warp 1: TMEM allocator + single-thread MMA issuer
 //     (tcgen05.mma.cta_group::1.kind::f16, accumulator in TMEM), warps 2-5:
-//     epilogue (tcgen05.ld -> fused bias / GELU / SiLU*up / residual -> HBM);
+//     epilogue (tcgen05.ld -> shared-memory transpose -> fused bias / GELU /
+//     SiLU*up / residual -> 16-byte stores), warps 6-21 (ECT): page decoders;
 //   * mbarrier full/empty ring, tcgen05.commit releases smem stages.
 #include <dlfcn.h>
 
@@ -23,7 +24,7 @@
 
 namespace lsb {
 
-// CT = true: weights arrive as ECT pages (12 KiB) in a staging ring and 8
+// CT = true: weights arrive as ECT pages (12 KiB) in a staging ring and 16
 // decoder warps expand each into the swizzled 16 KiB A tile in shared memory
 // (no decoded copy of the layer in HBM, 25 % fewer weight bytes).
 // TM = true (CT, BN <= 128, row-order pages): A is decoded into TMEM, so a
