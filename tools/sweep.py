@@ -8,6 +8,10 @@ model (dfbsim.simulate on the measured profile).
 
 Each point: one untimed run (graph capture), then `--trials` timed runs; the
 median is the measurement (the paper: 30 trials + 1 warm-up).
+The trials are taken in `--trials` passes over all (placement, k) points in a
+fresh random order each pass, so a disturbance of the box (the host-to-device
+bandwidth of a shared PCIe root wanders by a few %) spreads over many points as
+one outlier trial each instead of shifting a contiguous block of k.
 Eq. 10 error is reported over all k and over the k whose interleaved runs of
 resident layers stay within the consecutive limit of every DMA-intensive
 phase (the regime where Eq. 10 is linear by construction, bench.eq10_report).
@@ -53,13 +57,26 @@ def main():
     inputs = M.synthetic_inputs(cfg, seed=0)
     placements = {"interleaved": lambda k: ls.interleaved_indices(k, L) if k < L else range(L),
                   "contiguous": lambda k: range(k)}
+    import random
+    points = [(name, k) for name in placements for k in range(0, L + 1)]
+    trials = {p: [] for p in points}
+    rng = random.Random(0)
+    for p in points:  # warm-up (graph capture) run of every point
+        name, k = p
+        pl = ls.Placement.of({"vlm": placements[name](k)}) if k else ls.Placement.empty()
+        eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False)
+    for _ in range(args.trials):
+        order = points[:]
+        rng.shuffle(order)
+        for p in order:
+            name, k = p
+            pl = ls.Placement.of({"vlm": placements[name](k)}) if k else ls.Placement.empty()
+            trials[p].append(eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False).total_ms)
     rows = []
     for name, fn in placements.items():
         for k in range(0, L + 1):
             pl = ls.Placement.of({"vlm": fn(k)}) if k else ls.Placement.empty()
-            eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False)  # warm-up
-            ms = [eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False).total_ms
-                  for _ in range(args.trials)]
+            ms = trials[(name, k)]
             sim = ls.simulated_total(prof, pl, sim_cfg)
             idx = list(fn(k)) if k else []
             rows.append({"placement": name, "k": k, "measured_s": statistics.median(ms) / 1e3,
