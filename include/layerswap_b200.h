@@ -296,7 +296,10 @@ int ls_copy(void* dst, const void* src, uint64_t bytes);
 /* ==== 3. kernel launchers (raw device pointers, shapes, cudaStream_t) ====== */
 int ls_num_sms(int device, int32_t* out);
 int ls_gemv_plan(int32_t n_mt, int32_t n_kb, int32_t num_sms, int32_t* grid, int32_t* max_contrib);
-/* args points at the GemvArgs / DecodeAttnArgs / FlashArgs blocks of csrc/kernels.h */
+/* args points at the GemvArgs / DecodeAttnArgs / FlashArgs blocks of csrc/kernels.h;
+   ls_k_args_size(0 GemvArgs, 1 DecodeAttnArgs, 2 FlashArgs) is the size the
+   library was built with (binding layout check), -1 for an unknown kind. */
+int64_t ls_k_args_size(int32_t kind);
 int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream);
 /* Programmatic dependent launch for the NEXT ls_k_* launch of this thread (how the
    executor launches every in-step kernel: its prologue -- barrier init, weight

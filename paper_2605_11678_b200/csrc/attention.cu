@@ -73,6 +73,11 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAt
       bulk_g2s(vs, a.v_cache + off, bytes, &bar);
     }
   }
+  if (warp == 1) {  // next GEMVs' first pages into L2 while this latency-bound kernel runs
+    const int w = (blockIdx.y * gridDim.x + blockIdx.x) * 32 + lane, n = gridDim.x * gridDim.y * 32;
+    l2_prefetch_segments(a.pf[0], w, n);
+    l2_prefetch_segments(a.pf[1], w, n);
+  }
   pdl_wait();
   if (threadIdx.x == 0 && np > n_old) {
     const uint32_t bytes = static_cast<uint32_t>((np - n_old) * HD * 2);
@@ -288,6 +293,12 @@ __global__ void __launch_bounds__(128 * G * KG) flash_kernel(const FlashArgs a) 
   pdl_trigger();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && (a.pf[0].base || a.pf[1].base)) {  // next GEMMs' pages into L2
+    const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const int n = gridDim.x * gridDim.y * gridDim.z * 32;
+    l2_prefetch_segments(a.pf[0], b * 32 + lane, n);
+    l2_prefetch_segments(a.pf[1], b * 32 + lane, n);
+  }
   const int kg = warp / (4 * G);                     // key group
   const int hw = (warp >> 2) % G, wr = warp & 3;      // head of this warp within the CTA, row block
   const int h = static_cast<int>(blockIdx.y) * G + hw, kvh = static_cast<int>(blockIdx.y) * G / (a.hq / a.hkv);

@@ -138,6 +138,15 @@ int ls_k_ect_decode(const void* blob, void* out, void* stream) {
                  "ls_k_ect_decode");
 }
 
+int64_t ls_k_args_size(int32_t kind) {
+  switch (kind) {
+    case 0: return sizeof(GemvArgs);
+    case 1: return sizeof(DecodeAttnArgs);
+    case 2: return sizeof(FlashArgs);
+    default: return -1;
+  }
+}
+
 int ls_k_decode_attention(const void* args, void* stream) {
   return cuda_rc(launch_decode_attention(*static_cast<const DecodeAttnArgs*>(args),
                                          static_cast<cudaStream_t>(stream)),

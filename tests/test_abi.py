@@ -28,3 +28,14 @@ def test_version_and_error_channel():
     rc = lib.ls_interleaved_indices(5, 1, (ctypes.c_int64 * 5)())
     assert rc == _native.LS_ERR_VALUE
     assert "layers >= 2" in lib.ls_last_error().decode()
+
+
+def test_kernel_args_layout_matches_binding():
+    """The ctypes mirrors of csrc/kernels.h's argument blocks have the library's sizes
+    (kernels._lib() refuses a stale library the same way)."""
+    from paper_2605_11678_b200 import kernels
+
+    lib = kernels._lib()
+    for kind, st in enumerate((kernels.GemvArgs, kernels.DecodeAttnArgs, kernels.FlashArgs)):
+        assert lib.ls_k_args_size(kind) == ctypes.sizeof(st), st.__name__
+    assert lib.ls_k_args_size(7) == -1
