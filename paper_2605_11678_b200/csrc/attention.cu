@@ -33,16 +33,23 @@ constexpr int kDecChunk = 128;
 constexpr int kDecThreads = 256;  // 2 scores / 1 output pair per thread per head group
 constexpr int kDecMaxSplits = 16;
 
+__host__ __device__ inline int dec_cap(int n_ctx, int n_split) {
+  return ((n_ctx + n_split - 1) / n_split + 7) & ~7;
+}
+
 template <int HD, int G>
 __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAttnArgs a) {
   namespace cg = cooperative_groups;
   constexpr int HP = HD / 2;  // bf16 pairs per row
   extern __shared__ __align__(16) uint8_t dsm[];
+  // cap: positions per split rounded up to 8 (shared memory sized to the launch,
+  // so the CTA fits beside a GEMV CTA on the same SM)
+  const int cap = dec_cap(a.n_ctx, a.n_split);
   bf16* ks = reinterpret_cast<bf16*>(dsm);
-  bf16* vs = ks + kDecChunk * HD;
-  float* qs = reinterpret_cast<float*>(vs + kDecChunk * HD);  // [G][HD], pre-scaled
-  float* ps = qs + G * HD;                                     // [G][kDecChunk] scores -> probs
-  float* recv_o = ps + G * kDecChunk;          // [S][slice] partial O pushed by every split
+  bf16* vs = ks + cap * HD;
+  float* qs = reinterpret_cast<float*>(vs + cap * HD);  // [G][HD], pre-scaled
+  float* ps = qs + G * HD;                              // [G][cap] scores -> probs
+  float* recv_o = ps + G * cap;                         // [S][slice] partial O pushed by every split
   float* recv_ml = recv_o + G * HD + kDecMaxSplits;  // [S][2G] partial (max, sum) per head
   __shared__ __align__(8) uint64_t bar;
   __shared__ float sm_ml[2 * G];                               // partial max (log2), sum
@@ -90,8 +97,8 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAt
   __syncthreads();
   if (np > 0) mbar_wait(&bar, 0);
   // ---- scores (log2 domain) ----
-  for (int idx = threadIdx.x; idx < G * kDecChunk; idx += kDecThreads) {
-    const int g = idx / kDecChunk, p = idx % kDecChunk;
+  for (int idx = threadIdx.x; idx < G * cap; idx += kDecThreads) {
+    const int g = idx / cap, p = idx % cap;
     float sc = -INFINITY;
     if (p < np) {
       const uint32_t* kr = reinterpret_cast<const uint32_t*>(ks + p * HD);
@@ -113,13 +120,13 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAt
   // ---- softmax per head: warp g (strided) ----
   for (int g = warp; g < G; g += kDecThreads / 32) {
     float mx = -INFINITY;
-    for (int p = lane; p < kDecChunk; p += 32) mx = fmaxf(mx, ps[g * kDecChunk + p]);
+    for (int p = lane; p < cap; p += 32) mx = fmaxf(mx, ps[g * cap + p]);
     mx = warp_max(mx);
     float sum = 0.f;
-    for (int p = lane; p < kDecChunk; p += 32) {
-      const float v = ps[g * kDecChunk + p];
+    for (int p = lane; p < cap; p += 32) {
+      const float v = ps[g * cap + p];
       const float e = v == -INFINITY ? 0.f : exp2f(v - mx);
-      ps[g * kDecChunk + p] = e;
+      ps[g * cap + p] = e;
       sum += e;
     }
     sum = warp_sum(sum);
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAt
   for (int idx = threadIdx.x; idx < G * HP; idx += kDecThreads) {
     const int g = idx / HP, dp = idx % HP;
     const uint32_t* vc = reinterpret_cast<const uint32_t*>(vs) + dp;
-    const float* pg = ps + g * kDecChunk;
+    const float* pg = ps + g * cap;
     float o0 = 0.f, o1 = 0.f;
 #pragma unroll 8
     for (int p = 0; p < np; ++p) {
@@ -204,16 +211,20 @@ int decode_attn_splits(int n_ctx) {
 
 template <int HD, int G>
 static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
-  const size_t smem = 2ull * kDecChunk * HD * 2 +
-                      4ull * (G * (HD + kDecChunk) + G * HD + kDecMaxSplits + kDecMaxSplits * 2 * G);
+  const auto bytes = [](int cap) {
+    return 2ull * cap * HD * 2 + 4ull * (G * (HD + cap) + G * HD + kDecMaxSplits + kDecMaxSplits * 2 * G);
+  };
+  const size_t smem = bytes(dec_cap(a.n_ctx, a.n_split));
   static DeviceFlags attr;
   if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+                                         static_cast<int>(bytes(kDecChunk)));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr.mark();
   }

@@ -202,6 +202,7 @@ struct Arena {
 
 struct GemvPlan {
   int n, k, grid, max_contrib;
+  int slots = 0;  // GemvArgs.max_slots
 };
 
 // one DMA / EXE (or invocation span) timestamp pair of a run
@@ -418,6 +419,7 @@ int gemv(ls_exec* e, int epi, const GemvPlan& p, const char* w, const float* x, 
   a.bias = bias;
   a.n_valid = n_valid < 0 ? p.n : n_valid;
   a.amax = e->amax;
+  a.max_slots = p.slots;
   KL(launch_gemv(epi, a, p.grid, e->ss));
   return LS_OK;
 }
@@ -963,6 +965,7 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       if (const char* ov = std::getenv("LS_DIAG_PF_GU")) e->pf_gu = std::atoi(ov);
       if (const char* ov = std::getenv("LS_DIAG_PF_EX_O")) e->pf_ex_o = std::atoi(ov);
       if (const char* ov = std::getenv("LS_DIAG_PF_EX_GU")) e->pf_ex_gu = std::atoi(ov);
+      if (const char* ov = std::getenv("LS_DIAG_QO_SLOTS")) e->gp_qkv.slots = e->gp_o.slots = std::atoi(ov);
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
     e->tp_world = std::max(1, d.tp_world);

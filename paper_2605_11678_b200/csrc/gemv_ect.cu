@@ -43,15 +43,16 @@ constexpr int kSlotBytes = kChunk * (kEctPageBytes + kMaskBytes);
 constexpr int kMaxSlots = LS_GEMV_SLOTS;
 constexpr int kSmemBudget = 227 * 1024;
 
-__host__ __device__ inline int ect_slots(int n_kb) {
+__host__ __device__ inline int ect_slots(int n_kb, int max_slots) {
   const int avail = (kSmemBudget - n_kb * kTileCols * 4 - 4 * kTileRows * 4 - 64 - 2 * kMaxSlots * 8 - 16) /
                     kSlotBytes;
-  return avail > kMaxSlots ? kMaxSlots : avail;
+  const int cap = max_slots > 0 && max_slots < kMaxSlots ? max_slots : kMaxSlots;
+  return avail > cap ? cap : avail;
 }
 
-size_t ect_smem(int n_kb) {
-  return static_cast<size_t>(ect_slots(n_kb)) * kSlotBytes + static_cast<size_t>(n_kb) * kTileCols * 4 +
-         4 * kTileRows * 4 + 64 + 2 * kMaxSlots * 8 + 16;
+size_t ect_smem(int n_kb, int max_slots) {
+  return static_cast<size_t>(ect_slots(n_kb, max_slots)) * kSlotBytes +
+         static_cast<size_t>(n_kb) * kTileCols * 4 + 4 * kTileRows * 4 + 64 + 2 * kMaxSlots * 8 + 16;
 }
 }  // namespace
 
@@ -59,7 +60,7 @@ template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1) gemv_ect_kernel(const GemvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int K = a.n_kb * kTileCols;
-  const int NQ = ect_slots(a.n_kb);
+  const int NQ = ect_slots(a.n_kb, a.max_slots);
   uint8_t* slots = smem;
   uint32_t* xq = reinterpret_cast<uint32_t*>(smem + NQ * kSlotBytes);  // B words (gemv.cu layout)
   float* red = reinterpret_cast<float*>(xq + K);                        // 2 x [2][128]
@@ -239,13 +240,18 @@ static cudaError_t launch_ect_t(const GemvArgs& a, int grid, cudaStream_t st) {
     cudaError_t e =
         cudaFuncSetAttribute(gemv_ect_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return e;
+    // one shared-memory carveout for every in-step kernel: a decode-attention CTA
+    // can then share an SM with a GEMV CTA without a reconfiguration drain
+    e = cudaFuncSetAttribute(gemv_ect_kernel<EPI>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
     attr_set.mark();
   }
-  return launch_k(gemv_ect_kernel<EPI>, dim3(grid), dim3(kThreads), ect_smem(a.n_kb), st, a);
+  return launch_k(gemv_ect_kernel<EPI>, dim3(grid), dim3(kThreads), ect_smem(a.n_kb, a.max_slots), st, a);
 }
 
 cudaError_t launch_gemv_ect(int epi, const GemvArgs& a, int grid, cudaStream_t st) {
-  if (ect_slots(a.n_kb) < 2 || ect_smem(a.n_kb) > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidValue;
+  if (ect_slots(a.n_kb, a.max_slots) < 2 || ect_smem(a.n_kb, a.max_slots) > static_cast<size_t>(kSmemBudget))
+    return cudaErrorInvalidValue;
   switch (epi) {
     case GEMV_F32: return launch_ect_t<GEMV_F32>(a, grid, st);
     case GEMV_RESID: return launch_ect_t<GEMV_RESID>(a, grid, st);

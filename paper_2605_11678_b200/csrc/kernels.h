@@ -51,6 +51,9 @@ struct GemvArgs {
   const uint8_t* ct_blob;
   int ct_page0;
   int key_row0;            // ARGMAX: global index of row 0 (vocab-parallel lm-head shard)
+  // ECT: cap on the page-ring slots (0: as many as fit, <= LS_GEMV_SLOTS); fewer
+  // slots leave shared memory for a decode-attention CTA on the same SM
+  int max_slots;
 };
 
 int gemv_max_contrib(int n_mt, int n_kb, int grid);

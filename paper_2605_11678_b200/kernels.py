@@ -23,7 +23,7 @@ class GemvArgs(C.Structure):
                 ("hkv", C.c_int32), ("hd", C.c_int32), ("pos", C.c_int32), ("qn_w", _vp),
                 ("kn_w", _vp), ("rope", _vp), ("q_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
                 ("cache_head_stride", C.c_int32), ("amax", _vp), ("ct_blob", _vp),
-                ("ct_page0", C.c_int32), ("key_row0", C.c_int32)]
+                ("ct_page0", C.c_int32), ("key_row0", C.c_int32), ("max_slots", C.c_int32)]
 
 
 class L2Prefetch(C.Structure):
@@ -167,7 +167,7 @@ class GemvWorkspace:
 
 def gemv(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: torch.Tensor,
          ws: GemvWorkspace, *, norm_w=None, eps=1e-6, bias=None, n_valid=None, qkv=None,
-         amax=None, grid=None, stream=None, ct_blob=None, ct_page0=0, pdl=False):
+         amax=None, grid=None, stream=None, ct_blob=None, ct_page0=0, pdl=False, max_slots=0):
     """w_tiled: plain tiles, or (ct_blob given) an ECT blob whose pages
     ct_page0.. hold this matrix -- the GEMV then decodes pages in registers.
     pdl: launch with programmatic dependent launch, as the executor does."""
@@ -179,6 +179,7 @@ def gemv(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: 
     a = GemvArgs(w=_p(w_tiled), n_mt=n_mt, n_kb=n_kb, x=_p(x), norm_w=_p(norm_w), eps=eps,
                  ws=_p(ws.ws), counters=_p(ws.counters), max_contrib=mc.value, out=_p(out),
                  bias=_p(bias), n_valid=n if n_valid is None else n_valid, amax=_p(amax))
+    a.max_slots = max_slots
     if ct_blob is not None:
         a.ct_blob = ct_blob.data_ptr()
         a.ct_page0 = ct_page0

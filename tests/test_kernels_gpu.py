@@ -334,6 +334,11 @@ def test_gemv_ect_pages_bit_identical(n, k, page0):
     K.gemv(K.GEMV_F32, None, n, k, x, b, ws, norm_w=nw, ct_blob=blob, ct_page0=page0)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+    for slots in (2, 3):  # a shorter page ring (room for a decode-attention CTA beside it)
+        c = torch.empty(n, device=DEV)
+        K.gemv(K.GEMV_F32, None, n, k, x, c, ws, norm_w=nw, ct_blob=blob, ct_page0=page0, max_slots=slots)
+        torch.cuda.synchronize()
+        assert torch.equal(a, c), slots
 
 
 # epi: 0 BF16, 2 RESID_F32, 3 SILU_BF16, 4 F32 (kernels.GEMM_*)
