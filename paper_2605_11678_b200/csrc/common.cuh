@@ -210,6 +210,27 @@ __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// q/k RMSNorm + RoPE of one head (dim 128) for one token, one warp: lane l holds
+// dims (2l, 2l+1) in xa and (64+2l, 65+2l) in xb -- the rotation pairs (d, d+64)
+// stay in the lane.  w0/w1: the norm weight words of those dims; cs: (cos, sin)
+// of dims 2l, 2l+1.  Shared by qk_norm_rope128_kernel and the fused GEMM
+// epilogue so both round identically.
+__device__ __forceinline__ uint2 qk_norm_rope128_lane(uint32_t xa, uint32_t xb, bool norm, uint32_t w0,
+                                                      uint32_t w1, float4 cs, float eps) {
+  const float v0 = bf16_lo(xa), v1 = bf16_hi(xa), v2 = bf16_lo(xb), v3 = bf16_hi(xb);
+  float rstd = 1.0f;
+  if (norm) {
+    float ss = fmaf(v0, v0, 0.f);
+    ss = fmaf(v1, v1, ss);
+    ss = fmaf(v2, v2, ss);
+    ss = fmaf(v3, v3, ss);
+    rstd = rsqrtf(warp_sum(ss) / 128.f + eps);
+  }
+  const float n0 = v0 * rstd * bf16_lo(w0), n1 = v1 * rstd * bf16_hi(w0);
+  const float n2 = v2 * rstd * bf16_lo(w1), n3 = v3 * rstd * bf16_hi(w1);
+  return make_uint2(pack_bf16x2(n0 * cs.x - n2 * cs.y, n1 * cs.z - n3 * cs.w),
+                    pack_bf16x2(n2 * cs.x + n0 * cs.y, n3 * cs.z + n1 * cs.w));
+}
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

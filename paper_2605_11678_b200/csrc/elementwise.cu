@@ -288,23 +288,13 @@ __global__ void qk_norm_rope128_kernel(const bf16* qkv, int hq, int hkv, const b
     }
     const bool is_q = head < hq;
     const bf16* nwp = is_q ? qn_w : kn_w;
-    const uint32_t w0 = is_q ? wq[0] : wk[0], w1 = is_q ? wq[1] : wk[1];
-    const float v0 = bf16_lo(xa[i]), v1 = bf16_hi(xa[i]), v2 = bf16_lo(xb[i]), v3 = bf16_hi(xb[i]);
-    float rstd = 1.0f;
-    if (nwp) {
-      float ss = fmaf(v0, v0, 0.f);
-      ss = fmaf(v1, v1, ss);
-      ss = fmaf(v2, v2, ss);
-      ss = fmaf(v3, v3, ss);
-      rstd = rsqrtf(warp_sum(ss) / hd + eps);
-    }
-    const float n0 = v0 * rstd * bf16_lo(w0), n1 = v1 * rstd * bf16_hi(w0);
-    const float n2 = v2 * rstd * bf16_lo(w1), n3 = v3 * rstd * bf16_hi(w1);
+    const uint2 o = qk_norm_rope128_lane(xa[i], xb[i], nwp != nullptr, is_q ? wq[0] : wk[0],
+                                         is_q ? wq[1] : wk[1], cs, eps);
     dst = is_q ? reinterpret_cast<uint32_t*>(q_out + (static_cast<long>(t) * hq + head) * hd)
                : reinterpret_cast<uint32_t*>(k_cache + static_cast<long>(head - hq) * cache_head_stride +
                                              static_cast<long>(pos) * hd);
-    dst[lane] = pack_bf16x2(n0 * cs.x - n2 * cs.y, n1 * cs.z - n3 * cs.w);
-    dst[32 + lane] = pack_bf16x2(n2 * cs.x + n0 * cs.y, n3 * cs.z + n1 * cs.w);
+    dst[lane] = o.x;
+    dst[32 + lane] = o.y;
   }
 }
 

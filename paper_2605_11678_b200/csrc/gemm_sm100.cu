@@ -358,6 +358,43 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
                 for (int e = 0; e < 8; ++e) dst[e] = f2bf(o[e]);
               }
             }
+          } else if constexpr (EPI == GEMM_QKV_ROPE) {
+            // the tile is head mt (128 features); warp q finishes tokens 4q..4q+3 of
+            // the chunk: bf16 rounding as GEMM_BF16 stores it, then the q/k norm +
+            // RoPE of qk_norm_rope128_kernel, straight into q_out / the KV cache
+            const QkvRopeArgs& r = a.qr;
+            const int head = mt;
+#pragma unroll 1
+            for (int u = 0; u < 4; ++u) {
+              const int jt = q * 4 + u, tok = n0 + c0 + jt;
+              if (tok >= a.T) break;
+              const float* sf = stage_f + jt;
+              const uint32_t xa = pack_bf16x2(sf[(2 * lane) * 17], sf[(2 * lane + 1) * 17]);
+              const uint32_t xb = pack_bf16x2(sf[(64 + 2 * lane) * 17], sf[(65 + 2 * lane) * 17]);
+              const long pos = r.pos0 + tok;
+              uint32_t* dst;
+              if (head >= r.hq + r.hkv) {
+                dst = reinterpret_cast<uint32_t*>(r.v_cache + static_cast<long>(head - r.hq - r.hkv) * r.cache_head_stride +
+                                                  pos * 128);
+                dst[lane] = xa;
+                dst[32 + lane] = xb;
+                continue;
+              }
+              const bool is_q = head < r.hq;
+              const bf16* nwp = is_q ? r.qn_w : r.kn_w;
+              uint32_t w0 = 0x3f803f80u, w1 = 0x3f803f80u;  // bf16 1.0
+              if (nwp) {
+                w0 = reinterpret_cast<const uint32_t*>(nwp)[lane];
+                w1 = reinterpret_cast<const uint32_t*>(nwp)[32 + lane];
+              }
+              const float4 cs = reinterpret_cast<const float4*>(r.rope + pos * 64)[lane];
+              const uint2 o = qk_norm_rope128_lane(xa, xb, nwp != nullptr, w0, w1, cs, r.eps);
+              dst = is_q ? reinterpret_cast<uint32_t*>(r.q_out + (static_cast<long>(tok) * r.hq + head) * 128)
+                         : reinterpret_cast<uint32_t*>(r.k_cache + static_cast<long>(head - r.hq) * r.cache_head_stride +
+                                                       pos * 128);
+              dst[lane] = o.x;
+              dst[32 + lane] = o.y;
+            }
           } else {  // GEMM_F32: float4 per (token, 4 features)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -505,7 +542,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   GemmArgs b = a;
-  b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n, CT) : 1;
+  b.ks = a.sk_ws && EPI != GEMM_QKV_ROPE ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n, CT) : 1;
   static const int ks_cap = [] {  // LS_DIAG_GEMM_KS: split-K cap (diagnostics)
     const char* v = std::getenv("LS_DIAG_GEMM_KS");
     return v ? std::atoi(v) : 0;
@@ -524,6 +561,7 @@ static cudaError_t launch_epi(int epi, const GemmArgs& a, const CUtensorMap& map
     case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32, CT, TM>(a, map, st);
     case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16, CT, TM>(a, map, st);
     case GEMM_F32: return launch_bn<BN, GEMM_F32, CT, TM>(a, map, st);
+    case GEMM_QKV_ROPE: return launch_bn<BN, GEMM_QKV_ROPE, CT, TM>(a, map, st);
   }
   return cudaErrorInvalidValue;
 }
