@@ -80,11 +80,6 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(const DecodeAt
       bulk_g2s(vs, a.v_cache + off, bytes, &bar);
     }
   }
-  if (warp == 1) {  // next GEMVs' first pages into L2 while this latency-bound kernel runs
-    const int w = (blockIdx.y * gridDim.x + blockIdx.x) * 32 + lane, n = gridDim.x * gridDim.y * 32;
-    l2_prefetch_segments(a.pf[0], w, n);
-    l2_prefetch_segments(a.pf[1], w, n);
-  }
   pdl_wait();
   if (threadIdx.x == 0 && np > n_old) {
     const uint32_t bytes = static_cast<uint32_t>((np - n_old) * HD * 2);
@@ -214,7 +209,11 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   const auto bytes = [](int cap) {
     return 2ull * cap * HD * 2 + 4ull * (G * (HD + cap) + G * HD + kDecMaxSplits + kDecMaxSplits * 2 * G);
   };
-  const size_t smem = bytes(dec_cap(a.n_ctx, a.n_split));
+  static const bool full = [] {  // LS_DIAG_DEC_FULL_SMEM=1: every launch sized for 128 positions
+    const char* v = std::getenv("LS_DIAG_DEC_FULL_SMEM");
+    return v && std::atoi(v) == 1;
+  }();
+  const size_t smem = bytes(full ? kDecChunk : dec_cap(a.n_ctx, a.n_split));
   static DeviceFlags attr;
   if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
@@ -233,15 +232,24 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kDecThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute la[2];
+  static const int policy = [] {  // LS_DIAG_DEC_SPREAD=0: default cluster placement
+    const char* v = std::getenv("LS_DIAG_DEC_SPREAD");
+    return v ? std::atoi(v) : 1;
+  }();
+  cudaLaunchAttribute la[3];
   la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   la[0].val.programmaticStreamSerializationAllowed = take_launch_pdl() ? 1 : 0;
   la[1].id = cudaLaunchAttributeClusterDimension;
   la[1].val.clusterDim.x = 1;
   la[1].val.clusterDim.y = static_cast<unsigned>(a.n_split);
   la[1].val.clusterDim.z = 1;
+  // one CTA of a cluster per SM: small CTAs (sized to their positions) would
+  // otherwise be packed several to an SM
+  la[2].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+  la[2].val.clusterSchedulingPolicyPreference =
+      policy ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyDefault;
   cfg.attrs = la;
-  cfg.numAttrs = a.n_split > 1 ? 2 : 1;
+  cfg.numAttrs = a.n_split > 1 ? 3 : 1;
   return cudaLaunchKernelEx(&cfg, decode_attn_kernel<HD, G>, a);
 }
 
@@ -304,12 +312,6 @@ __global__ void __launch_bounds__(128 * G * KG) flash_kernel(const FlashArgs a) 
   pdl_trigger();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && (a.pf[0].base || a.pf[1].base)) {  // next GEMMs' pages into L2
-    const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    const int n = gridDim.x * gridDim.y * gridDim.z * 32;
-    l2_prefetch_segments(a.pf[0], b * 32 + lane, n);
-    l2_prefetch_segments(a.pf[1], b * 32 + lane, n);
-  }
   const int kg = warp / (4 * G);                     // key group
   const int hw = (warp >> 2) % G, wr = warp & 3;      // head of this warp within the CTA, row block
   const int h = static_cast<int>(blockIdx.y) * G + hw, kvh = static_cast<int>(blockIdx.y) * G / (a.hq / a.hkv);

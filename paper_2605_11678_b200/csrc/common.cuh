@@ -333,26 +333,6 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* smem_dst, const void*
       "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void l2_prefetch_bulk(const void* gmem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
-}
-// worker w of n issues its share of the prefetch (4-unit chunks, flattened over
-// (segment, chunk)); fire and forget -- nothing waits for it
-template <class P>  // P = L2Prefetch (kernels.h)
-__device__ inline void l2_prefetch_segments(const P& p, int w, int n) {
-  if (!p.base || !p.segs) return;
-  const uint32_t seg_max = (p.units + p.segs - 1) / p.segs;
-  const uint32_t cmax = (seg_max * p.permille / 1000 + 3) / 4;
-  for (uint32_t i = w; i < static_cast<uint32_t>(p.segs) * cmax; i += n) {
-    const uint32_t s = i / cmax, c = i % cmax;
-    const uint64_t t0 = static_cast<uint64_t>(s) * p.units / p.segs;
-    const uint64_t t1 = static_cast<uint64_t>(s + 1) * p.units / p.segs;
-    const uint32_t len = static_cast<uint32_t>((t1 - t0) * p.permille / 1000);
-    if (4 * c >= len) continue;
-    const uint32_t nu = min(4u, len - 4 * c);
-    l2_prefetch_bulk(p.base + (t0 + 4 * c) * p.unit_bytes, nu * p.unit_bytes);
-  }
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -607,18 +607,6 @@ int lm_decode_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l, 
   a.out = e->dec_attn;
   a.n_split = decode_attn_splits(pos + 1);  // one cluster of <= 16 CTAs, merged over DSMEM
   if (e->diag_dec_splits > a.n_split && e->diag_dec_splits <= 16) a.n_split = e->diag_dec_splits;
-  auto pf = [&](const GemvPlan& p, const char* base, int permille) {
-    L2Prefetch f{};
-    if (permille <= 0) return f;
-    f.base = reinterpret_cast<const uint8_t*>(base);
-    f.units = static_cast<uint32_t>(n_mt(p.n) * n_kb(p.k));
-    f.unit_bytes = cb ? kEctPageBytes : 16384;  // ECT page | plain 128 x 64 tile
-    f.segs = static_cast<uint16_t>(p.grid);
-    f.permille = static_cast<uint16_t>(std::min(permille, 1000));
-    return f;
-  };
-  a.pf[0] = pf(e->gp_o, part(1), e->pf_o);
-  a.pf[1] = pf(e->gp_gu, part(2), e->pf_gu);
   if (!(skip & 128)) KL(launch_decode_attention(a, e->ss));
   if (!(skip & 512)) RC(resid_gemv(e, e->gp_o, part(1), e->dec_attn, e->dec_h, cb, pg(1)));
   if (!(skip & 1024))
@@ -673,19 +661,6 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   f.g_pack = e->ex_g_pack;
   f.ws = e->flash_ws;
   f.counters = e->flash_cnt;
-  // segments: the GEMM's n-tiles (one CTA each when unsplit)
-  auto pf = [&](const char* base, int n, int k, int permille) {
-    L2Prefetch p{};
-    if (permille <= 0) return p;
-    p.base = reinterpret_cast<const uint8_t*>(base);
-    p.units = static_cast<uint32_t>(n_mt(n) * n_kb(k));
-    p.unit_bytes = cb ? kEctPageBytes : 16384;
-    p.segs = static_cast<uint16_t>(n_mt(n));
-    p.permille = static_cast<uint16_t>(std::min(permille, 1000));
-    return p;
-  };
-  f.pf[0] = pf(part(1), D, AH, e->pf_ex_o);
-  f.pf[1] = pf(part(2), 2 * d.ex_ffn, D, e->pf_ex_gu);
   if (!(skip & 4)) KL(launch_flash_attention(f, e->ss));
   if (!(skip & 16)) RC(resid_gemm(e, part(1), D, AH, T, e->m_ex_attn, e->ex_h, nullptr, cb, pg(1), co));
   if (!(skip & 1)) KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(5), e->ex_norm, T, D, d.lm_eps, e->ss));
@@ -995,10 +970,6 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq / e->ex_g_pack, e->ctx + Te, e->nsm);
       if (const char* ov = std::getenv("LS_DIAG_EX_KV_SPLITS")) e->ex_kv_splits = std::atoi(ov);  // diagnostics
       if (const char* ov = std::getenv("LS_DIAG_DEC_SPLITS")) e->diag_dec_splits = std::atoi(ov);
-      if (const char* ov = std::getenv("LS_DIAG_PF_O")) e->pf_o = std::atoi(ov);
-      if (const char* ov = std::getenv("LS_DIAG_PF_GU")) e->pf_gu = std::atoi(ov);
-      if (const char* ov = std::getenv("LS_DIAG_PF_EX_O")) e->pf_ex_o = std::atoi(ov);
-      if (const char* ov = std::getenv("LS_DIAG_PF_EX_GU")) e->pf_ex_gu = std::atoi(ov);
       if (const char* ov = std::getenv("LS_DIAG_QKV_FUSE")) e->qkv_fuse = std::atoi(ov) != 0;
       if (const char* ov = std::getenv("LS_DIAG_QO_SLOTS")) e->gp_qkv.slots = e->gp_o.slots = std::atoi(ov);
     }

@@ -311,6 +311,27 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
         // the bottleneck of the K = 1152 / 4096 GEMMs (gate|up 239 -> 156 us)
         const bool vec = (a.ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
         const bool vec4 = (a.ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
+        // GEMM_QKV_ROPE: the head's norm weights once per tile, the (cos, sin) of a
+        // chunk's tokens one chunk ahead -- no global round trip on the chunk's path
+        [[maybe_unused]] uint32_t qw0 = 0x3f803f80u, qw1 = 0x3f803f80u;  // bf16 1.0
+        [[maybe_unused]] float4 qcs[4];
+        [[maybe_unused]] const bool qrot = EPI == GEMM_QKV_ROPE && mt < a.qr.hq + a.qr.hkv;
+        [[maybe_unused]] auto load_cs = [&](int c) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int tok = n0 + c + q * 4 + u;
+            if (qrot && c < BN && tok < a.T)
+              qcs[u] = reinterpret_cast<const float4*>(a.qr.rope + static_cast<long>(a.qr.pos0 + tok) * 64)[lane];
+          }
+        };
+        if constexpr (EPI == GEMM_QKV_ROPE) {
+          const bf16* nwp = mt < a.qr.hq ? a.qr.qn_w : a.qr.kn_w;
+          if (qrot && nwp) {
+            qw0 = reinterpret_cast<const uint32_t*>(nwp)[lane];
+            qw1 = reinterpret_cast<const uint32_t*>(nwp)[32 + lane];
+          }
+          load_cs(0);
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
@@ -364,7 +385,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
             // RoPE of qk_norm_rope128_kernel, straight into q_out / the KV cache
             const QkvRopeArgs& r = a.qr;
             const int head = mt;
-#pragma unroll 1
+            float4 cs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cs[u] = qcs[u];
+            load_cs(c0 + 16);  // next chunk's tables, in flight while this one is stored
+            const bf16* nwp = head < r.hq ? r.qn_w : r.kn_w;
+#pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int jt = q * 4 + u, tok = n0 + c0 + jt;
               if (tok >= a.T) break;
@@ -373,25 +399,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
               const uint32_t xb = pack_bf16x2(sf[(64 + 2 * lane) * 17], sf[(65 + 2 * lane) * 17]);
               const long pos = r.pos0 + tok;
               uint32_t* dst;
-              if (head >= r.hq + r.hkv) {
+              if (!qrot) {  // V head: straight into the cache
                 dst = reinterpret_cast<uint32_t*>(r.v_cache + static_cast<long>(head - r.hq - r.hkv) * r.cache_head_stride +
                                                   pos * 128);
                 dst[lane] = xa;
                 dst[32 + lane] = xb;
                 continue;
               }
-              const bool is_q = head < r.hq;
-              const bf16* nwp = is_q ? r.qn_w : r.kn_w;
-              uint32_t w0 = 0x3f803f80u, w1 = 0x3f803f80u;  // bf16 1.0
-              if (nwp) {
-                w0 = reinterpret_cast<const uint32_t*>(nwp)[lane];
-                w1 = reinterpret_cast<const uint32_t*>(nwp)[32 + lane];
-              }
-              const float4 cs = reinterpret_cast<const float4*>(r.rope + pos * 64)[lane];
-              const uint2 o = qk_norm_rope128_lane(xa, xb, nwp != nullptr, w0, w1, cs, r.eps);
-              dst = is_q ? reinterpret_cast<uint32_t*>(r.q_out + (static_cast<long>(tok) * r.hq + head) * 128)
-                         : reinterpret_cast<uint32_t*>(r.k_cache + static_cast<long>(head - r.hq) * r.cache_head_stride +
-                                                       pos * 128);
+              const uint2 o = qk_norm_rope128_lane(xa, xb, nwp != nullptr, qw0, qw1, cs[u], r.eps);
+              dst = head < r.hq ? reinterpret_cast<uint32_t*>(r.q_out + (static_cast<long>(tok) * r.hq + head) * 128)
+                                : reinterpret_cast<uint32_t*>(r.k_cache + static_cast<long>(head - r.hq) * r.cache_head_stride +
+                                                              pos * 128);
               dst[lane] = o.x;
               dst[32 + lane] = o.y;
             }

@@ -126,16 +126,6 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
                    uint64_t ld_elems, uint32_t box_rows);
 
 // ---------------- attention --------------------------------------------------
-// Weight pages a latency-bound kernel warms in L2 for the GEMV that follows it
-// (cp.async.bulk.prefetch.L2): the first permille/1000 of every stream-K
-// segment [c*units/segs, (c+1)*units/segs) of that GEMV's grid.  base == nullptr: off.
-struct L2Prefetch {
-  const uint8_t* base;
-  uint32_t units, unit_bytes;
-  uint16_t segs, permille;
-  uint32_t _pad;
-};
-
 struct DecodeAttnArgs {
   const float* q;          // [hq*hd]
   const bf16* k_cache;     // [hkv][max_ctx][hd]
@@ -147,7 +137,6 @@ struct DecodeAttnArgs {
   float* ws;               // unused (splits merge over DSMEM); kept for ABI stability
   int* counters;           // unused
   int n_split;
-  L2Prefetch pf[2];        // warmed while the attention runs (O, gate|up pages)
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
 // splits (one cluster of <= 16 CTAs per KV head, <= 128 positions per CTA)
@@ -177,7 +166,6 @@ struct FlashArgs {
   // 2: GQA packing -- one CTA per (q tile, 2 query heads of one KV head), 8 warps;
   // hd 128, (hq / hkv) % 2 == 0; kv_splits counts CTAs per (q tile, head pair)
   int g_pack;
-  L2Prefetch pf[2];  // warmed while the attention runs (the expert's O, gate|up pages)
 };
 cudaError_t launch_flash_attention(const FlashArgs& a, cudaStream_t st);
 // kv_splits the launcher will use for (Tq, hq, keys) given num_sms, and the

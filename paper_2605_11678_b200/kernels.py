@@ -26,16 +26,11 @@ class GemvArgs(C.Structure):
                 ("ct_page0", C.c_int32), ("key_row0", C.c_int32), ("max_slots", C.c_int32)]
 
 
-class L2Prefetch(C.Structure):
-    _fields_ = [("base", _vp), ("units", C.c_uint32), ("unit_bytes", C.c_uint32),
-                ("segs", C.c_uint16), ("permille", C.c_uint16), ("_pad", C.c_uint32)]
-
-
 class DecodeAttnArgs(C.Structure):
     _fields_ = [("q", _vp), ("k_cache", _vp), ("v_cache", _vp), ("cache_head_stride", C.c_int32),
                 ("hq", C.c_int32), ("hkv", C.c_int32), ("hd", C.c_int32), ("n_ctx", C.c_int32),
                 ("scale", C.c_float), ("out", _vp), ("ws", _vp), ("counters", _vp),
-                ("n_split", C.c_int32), ("pf", L2Prefetch * 2)]
+                ("n_split", C.c_int32)]
 
 
 class FlashArgs(C.Structure):
@@ -48,7 +43,7 @@ class FlashArgs(C.Structure):
                 ("Tq", C.c_int32), ("hq", C.c_int32), ("hkv", C.c_int32), ("hd", C.c_int32),
                 ("causal", C.c_int32), ("q_offset", C.c_int32), ("seg_len", C.c_int32),
                 ("scale", C.c_float), ("kv_splits", C.c_int32), ("ws", _vp), ("counters", _vp),
-                ("k1_ready", C.c_int32), ("g_pack", C.c_int32), ("pf", L2Prefetch * 2)]
+                ("k1_ready", C.c_int32), ("g_pack", C.c_int32)]
 
 
 GEMV_F32, GEMV_RESID, GEMV_SILU, GEMV_QKV, GEMV_ARGMAX = range(5)
@@ -241,20 +236,11 @@ def gemm_splits(n: int, k: int, T: int, device=0) -> int:
     return _lib().ls_gemm_splits(n_mt, n_kb, T, nsm, nsm * 128 * 64, nsm)
 
 
-def l2_prefetch(pages: torch.Tensor, unit_bytes: int, segs: int, permille: int = 1000) -> L2Prefetch:
-    """Descriptor of weight pages a latency-bound kernel warms in L2 for the GEMV
-    after it: the first permille/1000 of each of `segs` stream-K segments."""
-    return L2Prefetch(base=_p(pages), units=pages.numel() * pages.element_size() // unit_bytes,
-                      unit_bytes=unit_bytes, segs=segs, permille=permille)
-
-
 def decode_attention(q, k_cache, v_cache, n_ctx, out, hq, hkv, hd, scale, ws, counters,
-                     n_split, stream=None, prefetch=()):
+                     n_split, stream=None):
     a = DecodeAttnArgs(q=_p(q), k_cache=_p(k_cache), v_cache=_p(v_cache),
                        cache_head_stride=k_cache.stride(0), hq=hq, hkv=hkv, hd=hd, n_ctx=n_ctx,
                        scale=scale, out=_p(out), ws=_p(ws), counters=_p(counters), n_split=n_split)
-    for i, f in enumerate(prefetch):
-        a.pf[i] = f
     _native.check(_lib().ls_k_decode_attention(C.byref(a), _stream(stream)), RuntimeError)
 
 

@@ -204,12 +204,6 @@ def test_decode_attention(hq, hkv, hd, n_ctx, n_split):
     att = torch.softmax((q.view(hq, 1, hd) @ kk.transpose(1, 2)) * scale, -1)
     ref = (att @ vv).view(-1)
     _close(out, ref, rel=1e-3, abs_=2e-3)
-    # warming the next GEMVs' pages in L2 from inside the kernel changes nothing
-    pages = torch.empty(3000 * 12288, dtype=torch.uint8, device=DEV)
-    out2 = torch.empty_like(out)
-    K.decode_attention(q, kc, vc, n_ctx, out2, hq, hkv, hd, scale, ws, cnt, n_split,
-                       prefetch=(K.l2_prefetch(pages, 12288, 148), K.l2_prefetch(pages, 12288, 37, 300)))
-    assert torch.equal(out, out2)
 
 
 def _attn_ref(q, k, v, mask, scale):
