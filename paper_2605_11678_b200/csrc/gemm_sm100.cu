@@ -33,7 +33,7 @@ template <int BN, bool CT = false, bool TM = false>
 struct GemmCfg {
   static constexpr int kStages = TM ? (BN >= 128 ? 6 : 10)
                                     : CT ? (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5))
-                                         : (BN >= 256 ? 4 : (BN >= 128 ? 6 : 8));
+                                         : (BN >= 256 ? 4 : (BN >= 192 ? 5 : (BN >= 128 ? 6 : 8)));
   static constexpr int kABytes = TM ? 0 : kTileBytes;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kPBytes = CT ? kEctPageBytes : 0;  // page staging
@@ -41,7 +41,8 @@ struct GemmCfg {
   static constexpr int kAccCols = BN < 32 ? 32 : BN;     // one accumulator
   // double-buffered accumulators (+ the decoded A stages, 32 columns each, for TM)
   static_assert(!TM || (CT && 2 * (BN < 32 ? 32 : BN) + 32 * kStages <= 512), "TMEM budget");
-  static constexpr int kTmemCols = TM ? 512 : 2 * kAccCols;
+  // tcgen05.alloc takes a power of two >= 32 columns (BN = 192: 384 -> 512)
+  static constexpr int kTmemCols = TM || 2 * kAccCols > 256 ? 512 : 2 * kAccCols;
   static constexpr int kDecWarps = CT ? 16 : 0;
   static constexpr int kThreads = 192 + 32 * kDecWarps;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * (kStageBytes + kPBytes) +
@@ -529,10 +530,28 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
 }
 
 int gemm_block_n(int T) { return T <= 64 ? 64 : (T <= 256 ? 128 : 256); }
+
+// Multi-token-tile GEMMs (T > 256) also have BN = 192: the persistent grid runs
+// ceil(tiles / #SMs) waves of BN-token tiles, and 192 wins wherever it needs no
+// more waves than 256 (ViT proj / fc2: 9 m-tiles x 12 token tiles = 108 tiles in
+// one wave at 256, 144 in one wave at 192 -- 25 % less per CTA; ViT QKV 3 waves
+// either way).  LS_DIAG_GEMM_BN192=0: off.
+int gemm_block_n(int T, int n_mt, int num_sms) {
+  static const bool on = [] {
+    const char* v = std::getenv("LS_DIAG_GEMM_BN192");
+    return !(v && std::atoi(v) == 0);
+  }();
+  if (T <= 256 || !on) return gemm_block_n(T);
+  auto cost = [&](int bn) {
+    const long tiles = static_cast<long>(n_mt) * ((T + bn - 1) / bn);
+    return (tiles + num_sms - 1) / num_sms * bn;
+  };
+  return cost(192) < cost(256) ? 192 : 256;
+}
 int gemm_box_rows() { return 64; }  // activation tensor-map box: 64 token rows
 
 int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n, bool ct) {
-  const int bn = gemm_block_n(T);
+  const int bn = ct ? gemm_block_n(T) : gemm_block_n(T, n_mt, num_sms);
   const int tiles = n_mt * ((T + bn - 1) / bn);
   // >= 4 splits or not worth the fix-up.  (ECT pages split from 2 while they were
   // decoded into shared memory; decoded into TMEM the expert QKV -- 48 tiles --
@@ -588,9 +607,14 @@ template <bool CT>
 static cudaError_t launch_ct(int epi, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
   // row-order pages on a single-token-tile launch: A decoded into TMEM
   const bool tm = CT && a.ct_order == 1 && a.T <= gemm_block_n(a.T);
-  switch (gemm_block_n(a.T)) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  switch (CT ? gemm_block_n(a.T) : gemm_block_n(a.T, a.n_mt, nsm)) {
     case 64: return tm ? launch_epi<64, true, true>(epi, a, map, st) : launch_epi<64, CT>(epi, a, map, st);
     case 128: return tm ? launch_epi<128, true, true>(epi, a, map, st) : launch_epi<128, CT>(epi, a, map, st);
+    case 192:
+      if constexpr (!CT) return launch_epi<192, false>(epi, a, map, st);
+      return cudaErrorInvalidValue;
     default: return launch_epi<256, CT>(epi, a, map, st);
   }
 }

@@ -117,6 +117,7 @@ struct GemmArgs {
 };
 
 int gemm_block_n(int T);
+int gemm_block_n(int T, int n_mt, int num_sms);  // plain weights, T > 256: 192 or 256 by waves
 int gemm_box_rows();  // rows of the activation tensor-map box (the kernels load BN/64 boxes per stage)
 // split factor launch_gemm picks for a shape (1 = no split)
 int gemm_splits(int n_mt, int n_kb, int T, int num_sms, long ws_floats, int cnt_n, bool ct = false);
