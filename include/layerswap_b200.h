@@ -297,7 +297,7 @@ int ls_copy(void* dst, const void* src, uint64_t bytes);
 int ls_num_sms(int device, int32_t* out);
 int ls_gemv_plan(int32_t n_mt, int32_t n_kb, int32_t num_sms, int32_t* grid, int32_t* max_contrib);
 /* args points at the GemvArgs / DecodeAttnArgs / FlashArgs blocks of csrc/kernels.h;
-   ls_k_args_size(0 GemvArgs, 1 DecodeAttnArgs, 2 FlashArgs, 3 QkvRopeArgs) is the size the
+   ls_k_args_size(0 GemvArgs, 1 DecodeAttnArgs, 2 FlashArgs) is the size the
    library was built with (binding layout check), -1 for an unknown kind. */
 int64_t ls_k_args_size(int32_t kind);
 int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream);
@@ -321,12 +321,6 @@ int ls_k_gemm_ws(int32_t epi, const void* w_tiled, int32_t n_mt, int32_t n_kb, c
                  void* stream);
 int ls_gemm_splits(int32_t n_mt, int32_t n_kb, int32_t T, int32_t num_sms, int64_t ws_floats,
                    int32_t cnt_n);
-/* epi 5 (GEMM_QKV_ROPE): the QKV projection with the per-head q/k RMSNorm, RoPE
-   and KV-cache append fused into the epilogue (head dim 128, one 128-feature tile
-   per head; out unused) -- the results of epi 0 followed by ls_k_qk_norm_rope,
-   bit for bit.  Its destinations (a QkvRopeArgs block of csrc/kernels.h) are set
-   for the next ls_k_gemm / ls_k_gemm_ws of this thread by: */
-int ls_set_gemm_qkv_rope(const void* args);
 int ls_k_decode_attention(const void* args, void* stream);
 /* Diagnostic: `grid` CTAs each stream `per_cta` bytes from src through a ring of
    `stages` x `stage_bytes` TMA bulk copies (per-SM streaming bandwidth probe). */

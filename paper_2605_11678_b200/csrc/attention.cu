@@ -33,6 +33,10 @@ constexpr int kDecChunk = 128;
 constexpr int kDecThreads = 256;  // 2 scores / 1 output pair per thread per head group
 constexpr int kDecMaxSplits = 16;
 
+constexpr int kDecCapMin = 112;
+
+// rows of the K / V / score buffers a CTA lays out: its share of the positions
+// rounded up to 8 (the launch reserves at least kDecCapMin rows)
 __host__ __device__ inline int dec_cap(int n_ctx, int n_split) {
   return ((n_ctx + n_split - 1) / n_split + 7) & ~7;
 }
@@ -209,11 +213,16 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   const auto bytes = [](int cap) {
     return 2ull * cap * HD * 2 + 4ull * (G * (HD + cap) + G * HD + kDecMaxSplits + kDecMaxSplits * 2 * G);
   };
-  static const bool full = [] {  // LS_DIAG_DEC_FULL_SMEM=1: every launch sized for 128 positions
-    const char* v = std::getenv("LS_DIAG_DEC_FULL_SMEM");
-    return v && std::atoi(v) == 1;
+  // Shared memory for max(positions, kDecCapMin) rows: 63.8 KiB fits beside a QKV /
+  // O GEMV CTA whose page ring is capped at 3 slots (162 KiB), so the attention
+  // CTAs start, and fetch their cached K/V, while the QKV GEMV still runs; never
+  // below that -- smaller CTAs pack more of a cluster onto one SM (sized to the
+  // ~67 positions: 42 KiB, +2.7 ms per inference)
+  static const int cap_min = [] {  // LS_DIAG_DEC_CAP_MIN (diagnostics)
+    const char* v = std::getenv("LS_DIAG_DEC_CAP_MIN");
+    return v ? std::atoi(v) : kDecCapMin;
   }();
-  const size_t smem = bytes(full ? kDecChunk : dec_cap(a.n_ctx, a.n_split));
+  const size_t smem = bytes(std::min(kDecChunk, std::max(cap_min, dec_cap(a.n_ctx, a.n_split))));
   static DeviceFlags attr;
   if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
@@ -232,24 +241,15 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kDecThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  static const int policy = [] {  // LS_DIAG_DEC_SPREAD=0: default cluster placement
-    const char* v = std::getenv("LS_DIAG_DEC_SPREAD");
-    return v ? std::atoi(v) : 1;
-  }();
-  cudaLaunchAttribute la[3];
+  cudaLaunchAttribute la[2];
   la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   la[0].val.programmaticStreamSerializationAllowed = take_launch_pdl() ? 1 : 0;
   la[1].id = cudaLaunchAttributeClusterDimension;
   la[1].val.clusterDim.x = 1;
   la[1].val.clusterDim.y = static_cast<unsigned>(a.n_split);
   la[1].val.clusterDim.z = 1;
-  // one CTA of a cluster per SM: small CTAs (sized to their positions) would
-  // otherwise be packed several to an SM
-  la[2].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
-  la[2].val.clusterSchedulingPolicyPreference =
-      policy ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyDefault;
   cfg.attrs = la;
-  cfg.numAttrs = a.n_split > 1 ? 3 : 1;
+  cfg.numAttrs = a.n_split > 1 ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, decode_attn_kernel<HD, G>, a);
 }
 

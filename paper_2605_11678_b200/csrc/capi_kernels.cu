@@ -64,28 +64,6 @@ int ls_k_gemv(int32_t epi, const void* args, int32_t grid, void* stream) {
                  "ls_k_gemv");
 }
 
-static thread_local QkvRopeArgs g_qkv_rope{};
-static thread_local bool g_qkv_rope_set = false;
-
-int ls_set_gemm_qkv_rope(const void* args) {
-  if (!args) return set_error(LS_ERR_VALUE, "ls_set_gemm_qkv_rope: args is NULL");
-  g_qkv_rope = *static_cast<const QkvRopeArgs*>(args);
-  g_qkv_rope_set = true;
-  return LS_OK;
-}
-
-// GEMM_QKV_ROPE takes its destinations from the last ls_set_gemm_qkv_rope (consumed)
-static int take_qkv_rope(int epi, GemmArgs& a, const char* who) {
-  if (epi != GEMM_QKV_ROPE) return LS_OK;
-  if (!g_qkv_rope_set) return set_error(LS_ERR_VALUE, "%s: GEMM_QKV_ROPE without ls_set_gemm_qkv_rope", who);
-  if (a.n_mt != g_qkv_rope.hq + 2 * g_qkv_rope.hkv)
-    return set_error(LS_ERR_VALUE, "%s: GEMM_QKV_ROPE needs one 128-feature tile per head (%d tiles, %d heads)",
-                     who, a.n_mt, g_qkv_rope.hq + 2 * g_qkv_rope.hkv);
-  a.qr = g_qkv_rope;
-  g_qkv_rope_set = false;
-  return LS_OK;
-}
-
 int ls_k_gemm(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void* x, int32_t T,
               int64_t ldx, void* out, int64_t ldo, const float* bias, const void* bias_bf16,
               int32_t n_valid, void* stream) {
@@ -103,7 +81,6 @@ int ls_k_gemm(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const void
   a.bias = bias;
   a.bias_bf16 = static_cast<const bf16*>(bias_bf16);
   a.n_valid = n_valid;
-  if (int r = take_qkv_rope(epi, a, "ls_k_gemm")) return r;
   return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm");
 }
 
@@ -138,7 +115,6 @@ int ls_k_gemm_ws(int32_t epi, const void* w, int32_t n_mt, int32_t n_kb, const v
       return set_error(LS_ERR_CUDA, "ls_k_gemm_ws: cannot read the ECT header");
     a.ct_order = static_cast<int>(h.order);
   }
-  if (int r = take_qkv_rope(epi, a, "ls_k_gemm_ws")) return r;
   return cuda_rc(launch_gemm(epi, a, map, static_cast<cudaStream_t>(stream)), "ls_k_gemm_ws");
 }
 
@@ -167,7 +143,6 @@ int64_t ls_k_args_size(int32_t kind) {
     case 0: return sizeof(GemvArgs);
     case 1: return sizeof(DecodeAttnArgs);
     case 2: return sizeof(FlashArgs);
-    case 3: return sizeof(QkvRopeArgs);
     default: return -1;
   }
 }

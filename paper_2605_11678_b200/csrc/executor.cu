@@ -293,13 +293,6 @@ struct ls_exec {
   // LM decode layer to leave out -- results are wrong, the timing difference is the cost
   uint32_t diag_skip = 0;
   int diag_dec_splits = 0;  // LS_DIAG_DEC_SPLITS: decode-attention split count override
-  // permille of the O / gate|up GEMV pages the decode attention warms in L2
-  // (LS_DIAG_PF_O / LS_DIAG_PF_GU)
-  int pf_o = 0, pf_gu = 0;
-  int pf_ex_o = 0, pf_ex_gu = 0;
-  // q/k norm + RoPE + KV append fused into the QKV GEMM epilogue (hd 128);
-  // LS_DIAG_QKV_FUSE=0: the separate qk_norm_rope kernel (A/B diagnostics)
-  bool qkv_fuse = true;  // the same for the expert's flash attention (LS_DIAG_PF_EX_O / _GU)
   std::vector<RunRec> grecs;  // invocation-span records of the captured run
   cudaEvent_t join_ev = nullptr, fork_ev = nullptr;
   uint64_t h2d_bytes = 0;
@@ -368,29 +361,11 @@ struct CtView {
   int page0(const ls_layer_layout& L, int i) const { return static_cast<int>(L.offset[i] / 16384); }
 };
 
-QkvRopeArgs qkv_rope(int hq, int hkv, int pos0, int cache_head_stride, float eps, const char* qn_w,
-                     const char* kn_w, const float2* rope, bf16* q_out, bf16* k_cache, bf16* v_cache) {
-  QkvRopeArgs r{};
-  r.hq = hq;
-  r.hkv = hkv;
-  r.pos0 = pos0;
-  r.cache_head_stride = cache_head_stride;
-  r.eps = eps;
-  r.qn_w = reinterpret_cast<const bf16*>(qn_w);
-  r.kn_w = reinterpret_cast<const bf16*>(kn_w);
-  r.rope = rope;
-  r.q_out = q_out;
-  r.k_cache = k_cache;
-  r.v_cache = v_cache;
-  return r;
-}
-
 int gemm(ls_exec* e, int epi, const char* w, int n, int k, int T, const CUtensorMap& map, void* out,
          long ldo, const void* bias_bf16 = nullptr, int n_valid = -1, const char* ct_blob = nullptr,
-         int ct_page0 = 0, int ct_order = 0, const QkvRopeArgs* qr = nullptr) {
+         int ct_page0 = 0, int ct_order = 0) {
   GemmArgs a{};
   a.ct_order = ct_order;
-  if (qr) a.qr = *qr;
   if (ct_blob && (T + gemm_block_n(T) - 1) / gemm_block_n(T) > 1) {
     // several token tiles would each re-decode every page inside the GEMM: expand
     // this matrix's pages once into the decode scratch and run the plain GEMM on it
@@ -538,17 +513,10 @@ int lm_prefill_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   auto pg = [&](int i) { return cb ? ct.page0(L, i) : 0; };
   KL(launch_rmsnorm_rows(e->lm_h, (const bf16*)part(4), e->lm_norm, S, D, d.lm_eps, e->ss));
   const uint32_t skip = e->diag_skip;
-  if (d.lm_hd == 128 && e->qkv_fuse) {  // q/k norm + RoPE + KV store in the GEMM epilogue
-    const QkvRopeArgs qr = qkv_rope(d.lm_hq, d.lm_hkv, 0, e->cache_stride(), d.lm_eps, part(6), part(7),
-                                    (const float2*)e->g[3], e->lm_q, e->kc(l), e->vc(l));
-    if (!(skip & (1u << 14)))
-      RC(gemm(e, GEMM_QKV_ROPE, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN, nullptr, -1, cb, pg(0), 0, &qr));
-  } else {
-    if (!(skip & (1u << 14))) RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN, nullptr, -1, cb, pg(0)));
-    KL(launch_qk_norm_rope(e->lm_qkv, S, d.lm_hq, d.lm_hkv, d.lm_hd, (const bf16*)part(6),
-                           (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], 0, e->lm_q,
-                           e->kc(l), e->vc(l), e->cache_stride(), e->ss));
-  }
+  if (!(skip & (1u << 14))) RC(gemm(e, GEMM_BF16, part(0), QN, D, S, e->m_lm_norm, e->lm_qkv, QN, nullptr, -1, cb, pg(0)));
+  KL(launch_qk_norm_rope(e->lm_qkv, S, d.lm_hq, d.lm_hkv, d.lm_hd, (const bf16*)part(6),
+                         (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], 0, e->lm_q,
+                         e->kc(l), e->vc(l), e->cache_stride(), e->ss));
   FlashArgs f = flash_base(S, d.lm_hq, d.lm_hkv, d.lm_hd);
   f.q = e->lm_q;
   f.q_tok_stride = AH;
@@ -629,16 +597,10 @@ int expert_layer(ls_exec* e, const char* w, const ls_layer_layout& L, int l,
   const uint32_t skip = e->diag_skip;
   if (!(skip & 1)) KL(launch_rmsnorm_rows(e->ex_h, (const bf16*)part(4), e->ex_norm, T, D, d.lm_eps, e->ss));
   const int co = ct.order;
-  if (d.ex_hd == 128 && e->qkv_fuse) {  // q/k norm + RoPE + KV store in the GEMM epilogue
-    const QkvRopeArgs qr = qkv_rope(d.ex_hq, d.ex_hkv, e->ctx, T * d.ex_hd, d.lm_eps, part(6), part(7),
-                                    (const float2*)e->g[3], e->ex_q, ek - shift, ev - shift);
-    if (!(skip & 8)) RC(gemm(e, GEMM_QKV_ROPE, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0), co, &qr));
-  } else {
-    if (!(skip & 8)) RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0), co));
-    if (!(skip & 2)) KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
-                           (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], e->ctx, e->ex_q,
-                           ek - shift, ev - shift, T * d.ex_hd, e->ss));
-  }
+  if (!(skip & 8)) RC(gemm(e, GEMM_BF16, part(0), QN, D, T, e->m_ex_norm, e->ex_qkv, QN, nullptr, -1, cb, pg(0), co));
+  if (!(skip & 2)) KL(launch_qk_norm_rope(e->ex_qkv, T, d.ex_hq, d.ex_hkv, d.ex_hd, (const bf16*)part(6),
+                         (const bf16*)part(7), d.lm_eps, (const float2*)e->g[3], e->ctx, e->ex_q,
+                         ek - shift, ev - shift, T * d.ex_hd, e->ss));
   FlashArgs f = flash_base(T, d.ex_hq, d.ex_hkv, d.ex_hd);
   f.q = e->ex_q;
   f.q_tok_stride = AH;
@@ -913,6 +875,9 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       std::sscanf(ov, "%d,%d,%d,%d", &gs[0], &gs[1], &gs[2], &gs[3]);
     e->gp_qkv = plan_gemv(QN, d.lm_d, gs[0]);
     e->gp_o = plan_gemv(d.lm_d, AH, gs[1]);
+    // QKV / O page rings capped at 3 slots: a decode-attention CTA fits beside the
+    // GEMV CTA (attention.cu kDecCapMin), measured -0.4 ms per inference
+    e->gp_qkv.slots = e->gp_o.slots = 3;
     e->gp_gu = plan_gemv(2 * d.lm_ffn, d.lm_d, gs[2]);
     e->gp_down = plan_gemv(d.lm_d, d.lm_ffn, gs[3]);
     e->gp_head = plan_gemv(head_rows(d), d.lm_d, e->nsm);
@@ -970,7 +935,6 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq / e->ex_g_pack, e->ctx + Te, e->nsm);
       if (const char* ov = std::getenv("LS_DIAG_EX_KV_SPLITS")) e->ex_kv_splits = std::atoi(ov);  // diagnostics
       if (const char* ov = std::getenv("LS_DIAG_DEC_SPLITS")) e->diag_dec_splits = std::atoi(ov);
-      if (const char* ov = std::getenv("LS_DIAG_QKV_FUSE")) e->qkv_fuse = std::atoi(ov) != 0;
       if (const char* ov = std::getenv("LS_DIAG_QO_SLOTS")) e->gp_qkv.slots = e->gp_o.slots = std::atoi(ov);
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)

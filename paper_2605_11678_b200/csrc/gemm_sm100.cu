@@ -312,27 +312,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
         // the bottleneck of the K = 1152 / 4096 GEMMs (gate|up 239 -> 156 us)
         const bool vec = (a.ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
         const bool vec4 = (a.ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
-        // GEMM_QKV_ROPE: the head's norm weights once per tile, the (cos, sin) of a
-        // chunk's tokens one chunk ahead -- no global round trip on the chunk's path
-        [[maybe_unused]] uint32_t qw0 = 0x3f803f80u, qw1 = 0x3f803f80u;  // bf16 1.0
-        [[maybe_unused]] float4 qcs[4];
-        [[maybe_unused]] const bool qrot = EPI == GEMM_QKV_ROPE && mt < a.qr.hq + a.qr.hkv;
-        [[maybe_unused]] auto load_cs = [&](int c) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int tok = n0 + c + q * 4 + u;
-            if (qrot && c < BN && tok < a.T)
-              qcs[u] = reinterpret_cast<const float4*>(a.qr.rope + static_cast<long>(a.qr.pos0 + tok) * 64)[lane];
-          }
-        };
-        if constexpr (EPI == GEMM_QKV_ROPE) {
-          const bf16* nwp = mt < a.qr.hq ? a.qr.qn_w : a.qr.kn_w;
-          if (qrot && nwp) {
-            qw0 = reinterpret_cast<const uint32_t*>(nwp)[lane];
-            qw1 = reinterpret_cast<const uint32_t*>(nwp)[32 + lane];
-          }
-          load_cs(0);
-        }
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
@@ -379,40 +358,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, CT, TM>::kThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) dst[e] = f2bf(o[e]);
               }
-            }
-          } else if constexpr (EPI == GEMM_QKV_ROPE) {
-            // the tile is head mt (128 features); warp q finishes tokens 4q..4q+3 of
-            // the chunk: bf16 rounding as GEMM_BF16 stores it, then the q/k norm +
-            // RoPE of qk_norm_rope128_kernel, straight into q_out / the KV cache
-            const QkvRopeArgs& r = a.qr;
-            const int head = mt;
-            float4 cs[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) cs[u] = qcs[u];
-            load_cs(c0 + 16);  // next chunk's tables, in flight while this one is stored
-            const bf16* nwp = head < r.hq ? r.qn_w : r.kn_w;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int jt = q * 4 + u, tok = n0 + c0 + jt;
-              if (tok >= a.T) break;
-              const float* sf = stage_f + jt;
-              const uint32_t xa = pack_bf16x2(sf[(2 * lane) * 17], sf[(2 * lane + 1) * 17]);
-              const uint32_t xb = pack_bf16x2(sf[(64 + 2 * lane) * 17], sf[(65 + 2 * lane) * 17]);
-              const long pos = r.pos0 + tok;
-              uint32_t* dst;
-              if (!qrot) {  // V head: straight into the cache
-                dst = reinterpret_cast<uint32_t*>(r.v_cache + static_cast<long>(head - r.hq - r.hkv) * r.cache_head_stride +
-                                                  pos * 128);
-                dst[lane] = xa;
-                dst[32 + lane] = xb;
-                continue;
-              }
-              const uint2 o = qk_norm_rope128_lane(xa, xb, nwp != nullptr, qw0, qw1, cs[u], r.eps);
-              dst = head < r.hq ? reinterpret_cast<uint32_t*>(r.q_out + (static_cast<long>(tok) * r.hq + head) * 128)
-                                : reinterpret_cast<uint32_t*>(r.k_cache + static_cast<long>(head - r.hq) * r.cache_head_stride +
-                                                              pos * 128);
-              dst[lane] = o.x;
-              dst[32 + lane] = o.y;
             }
           } else {  // GEMM_F32: float4 per (token, 4 features)
 #pragma unroll
@@ -579,7 +524,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const CUtensorMap& map, cudaStre
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   GemmArgs b = a;
-  b.ks = a.sk_ws && EPI != GEMM_QKV_ROPE ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n, CT) : 1;
+  b.ks = a.sk_ws ? gemm_splits(a.n_mt, a.n_kb, a.T, nsm, a.sk_ws_floats, a.sk_cnt_n, CT) : 1;
   static const int ks_cap = [] {  // LS_DIAG_GEMM_KS: split-K cap (diagnostics)
     const char* v = std::getenv("LS_DIAG_GEMM_KS");
     return v ? std::atoi(v) : 0;
@@ -598,7 +543,6 @@ static cudaError_t launch_epi(int epi, const GemmArgs& a, const CUtensorMap& map
     case GEMM_RESID_F32: return launch_bn<BN, GEMM_RESID_F32, CT, TM>(a, map, st);
     case GEMM_SILU_BF16: return launch_bn<BN, GEMM_SILU_BF16, CT, TM>(a, map, st);
     case GEMM_F32: return launch_bn<BN, GEMM_F32, CT, TM>(a, map, st);
-    case GEMM_QKV_ROPE: return launch_bn<BN, GEMM_QKV_ROPE, CT, TM>(a, map, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -69,23 +69,6 @@ enum GemmEpi : int {
   GEMM_RESID_F32 = 2,  // out_f32 += acc (+bias)
   GEMM_SILU_BF16 = 3,  // out_bf16[t, g*64+i] = silu(gate) * up
   GEMM_F32 = 4,        // out_f32 = acc (+bias)
-  // the QKV projection with the per-head q/k RMSNorm + RoPE + KV-cache append
-  // fused (head dim 128 = one 128-feature tile per head; out unused): the
-  // results of GEMM_BF16 followed by launch_qk_norm_rope, bit for bit
-  GEMM_QKV_ROPE = 5,
-};
-
-// GEMM_QKV_ROPE destinations (the arguments of launch_qk_norm_rope)
-struct QkvRopeArgs {
-  int hq, hkv, pos0, cache_head_stride;
-  float eps;
-  int _pad;
-  const bf16* qn_w;     // q RMSNorm weight [128] (nullptr: no q/k norm)
-  const bf16* kn_w;
-  const float2* rope;   // (cos, sin) [pos][64]
-  bf16* q_out;          // [T][hq][128]
-  bf16* k_cache;        // [hkv][max_ctx][128], token t at position pos0 + t
-  bf16* v_cache;
 };
 
 struct GemmArgs {
@@ -113,7 +96,6 @@ struct GemmArgs {
   // tile is requested before griddepcontrol.wait
   int w_dep;
   int ct_order;  // EctHeader.order of ct_blob (1: row order -> A decoded into TMEM)
-  QkvRopeArgs qr;  // GEMM_QKV_ROPE only
 };
 
 int gemm_block_n(int T);

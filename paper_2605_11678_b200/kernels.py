@@ -47,14 +47,8 @@ class FlashArgs(C.Structure):
 
 
 GEMV_F32, GEMV_RESID, GEMV_SILU, GEMV_QKV, GEMV_ARGMAX = range(5)
-GEMM_BF16, GEMM_BF16_GELU, GEMM_RESID_F32, GEMM_SILU_BF16, GEMM_F32, GEMM_QKV_ROPE = range(6)
+GEMM_BF16, GEMM_BF16_GELU, GEMM_RESID_F32, GEMM_SILU_BF16, GEMM_F32 = range(5)
 
-
-class QkvRopeArgs(C.Structure):
-    _fields_ = [("hq", C.c_int32), ("hkv", C.c_int32), ("pos0", C.c_int32),
-                ("cache_head_stride", C.c_int32), ("eps", C.c_float), ("_pad", C.c_int32),
-                ("qn_w", _vp), ("kn_w", _vp), ("rope", _vp), ("q_out", _vp), ("k_cache", _vp),
-                ("v_cache", _vp)]
 
 _bound = False
 
@@ -89,9 +83,7 @@ def _lib():
             fn.restype = C.c_int
         lib.ls_k_args_size.argtypes = [C.c_int32]
         lib.ls_k_args_size.restype = C.c_int64
-        lib.ls_set_gemm_qkv_rope.argtypes = [_vp]
-        lib.ls_set_gemm_qkv_rope.restype = C.c_int
-        for kind, st in enumerate((GemvArgs, DecodeAttnArgs, FlashArgs, QkvRopeArgs)):
+        for kind, st in enumerate((GemvArgs, DecodeAttnArgs, FlashArgs)):
             if lib.ls_k_args_size(kind) != C.sizeof(st):
                 raise RuntimeError(f"{st.__name__}: binding is {C.sizeof(st)} bytes, library "
                                    f"{lib.ls_k_args_size(kind)} (stale liblayerswap_b200.so?)")
@@ -201,12 +193,9 @@ _SPLITK_WS: dict = {}
 
 def gemm(epi: int, w_tiled: torch.Tensor, n: int, k: int, x: torch.Tensor, out: torch.Tensor,
          *, bias=None, n_valid=None, ldo=None, stream=None, splitk: bool = False, ct_blob=None,
-         ct_page0: int = 0, qkv_rope: "QkvRopeArgs | None" = None):
+         ct_page0: int = 0):
     """splitk=True passes a split-K workspace (skinny shapes then split K);
-    ct_blob: weights are ECT pages ct_page0.. of that blob (decoded in smem);
-    qkv_rope: destinations of epi GEMM_QKV_ROPE (q/k norm + RoPE + KV append)."""
-    if qkv_rope is not None:
-        _native.check(_lib().ls_set_gemm_qkv_rope(C.byref(qkv_rope)), RuntimeError)
+    ct_blob: weights are ECT pages ct_page0.. of that blob (decoded in smem)."""
     n_mt, n_kb = tile_dims(n, k)
     T = x.shape[0]
     bias_f = bias if bias is not None and bias.dtype == torch.float32 else None

@@ -302,50 +302,6 @@ def test_qk_norm_rope_prefill_kernel(T, hq, hkv, hd):
     assert torch.equal(vc[:, 5:5 + T].permute(1, 0, 2), qkv.view(T, -1, hd)[:, hq + hkv:])
 
 
-# (T, hq, hkv, K, ect order): the expert (T 64, pages decoded into TMEM), the
-# LM prefill (T 1024 -> 4 token tiles of 256), ragged T, no q/k norm weights
-@pytest.mark.parametrize("T,hq,hkv,k,order,norm", [(64, 32, 8, 2048, 1, True), (64, 32, 8, 2048, None, True),
-                                                   (1024, 32, 8, 4096, None, True), (77, 8, 2, 512, None, True),
-                                                   (200, 4, 2, 256, None, False)])
-def test_gemm_qkv_rope_epilogue_bit_identical(T, hq, hkv, k, order, norm):
-    """GEMM_QKV_ROPE (q/k norm + RoPE + KV append in the GEMM epilogue) == GEMM_BF16
-    followed by the qk_norm_rope kernel, bit for bit, for every destination."""
-    from paper_2605_11678_b200 import ect
-    torch.manual_seed(19)
-    hd, pos0 = 128, 9
-    n = (hq + 2 * hkv) * hd
-    w = (torch.randn(n, k, device=DEV) * 0.02).to(torch.bfloat16)
-    tiled = K.pack_tiled(w)
-    x = torch.randn(T, k, device=DEV).to(torch.bfloat16)
-    qn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16) if norm else None
-    kn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16) if norm else None
-    rope = _rope_table(pos0 + T + 4, hd, 1e6)
-    max_ctx = pos0 + T + 4
-
-    def dests():
-        return (torch.zeros(T, hq, hd, dtype=torch.bfloat16, device=DEV),
-                torch.zeros(hkv, max_ctx, hd, dtype=torch.bfloat16, device=DEV),
-                torch.zeros(hkv, max_ctx, hd, dtype=torch.bfloat16, device=DEV))
-    qkv = torch.empty(T, n, dtype=torch.bfloat16, device=DEV)
-    K.gemm(K.GEMM_BF16, tiled, n, k, x, qkv)
-    q1, k1, v1 = dests()
-    K.qk_norm_rope(qkv, hq, hkv, hd, qn, kn, 1e-6, rope, pos0, q1, k1, v1)
-    q2, k2, v2 = dests()
-    args = K.QkvRopeArgs(hq=hq, hkv=hkv, pos0=pos0, cache_head_stride=k2.stride(0), eps=1e-6,
-                         qn_w=K._p(qn), kn_w=K._p(kn), rope=K._p(rope), q_out=K._p(q2),
-                         k_cache=K._p(k2), v_cache=K._p(v2))
-    if order is None:
-        K.gemm(K.GEMM_QKV_ROPE, tiled, n, k, x, qkv, qkv_rope=args)
-    else:
-        flat = tiled.view(torch.uint8).reshape(-1)
-        blob = ect.compress(flat, flat.numel(), order)
-        K.gemm(K.GEMM_QKV_ROPE, None, n, k, x, qkv, ct_blob=blob, qkv_rope=args)
-    torch.cuda.synchronize()
-    assert torch.equal(q1, q2)
-    assert torch.equal(k1, k2)
-    assert torch.equal(v1, v2)
-
-
 @pytest.mark.parametrize("n,k,page0", [(384, 256, 0), (6144, 4096, 0), (4096, 12288, 3),
                                        (320, 1152, 1),     # 18 k-blocks: chunks 4,4,4,4,2; ragged n
                                        (128, 16384, 0),    # one m-tile over every CTA; x staged by the loop path
