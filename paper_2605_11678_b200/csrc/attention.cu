@@ -33,10 +33,8 @@ constexpr int kDecChunk = 128;
 constexpr int kDecThreads = 256;  // 2 scores / 1 output pair per thread per head group
 constexpr int kDecMaxSplits = 16;
 
-constexpr int kDecCapMin = 112;
-
 // rows of the K / V / score buffers a CTA lays out: its share of the positions
-// rounded up to 8 (the launch reserves at least kDecCapMin rows)
+// rounded up to 8 (the launch reserves kDecChunk)
 __host__ __device__ inline int dec_cap(int n_ctx, int n_split) {
   return ((n_ctx + n_split - 1) / n_split + 7) & ~7;
 }
@@ -213,16 +211,11 @@ static cudaError_t decode_launch(const DecodeAttnArgs& a, cudaStream_t st) {
   const auto bytes = [](int cap) {
     return 2ull * cap * HD * 2 + 4ull * (G * (HD + cap) + G * HD + kDecMaxSplits + kDecMaxSplits * 2 * G);
   };
-  // Shared memory for max(positions, kDecCapMin) rows: 63.8 KiB fits beside a QKV /
-  // O GEMV CTA whose page ring is capped at 3 slots (162 KiB), so the attention
-  // CTAs start, and fetch their cached K/V, while the QKV GEMV still runs; never
-  // below that -- smaller CTAs pack more of a cluster onto one SM (sized to the
-  // ~67 positions: 42 KiB, +2.7 ms per inference)
-  static const int cap_min = [] {  // LS_DIAG_DEC_CAP_MIN (diagnostics)
-    const char* v = std::getenv("LS_DIAG_DEC_CAP_MIN");
-    return v ? std::atoi(v) : kDecCapMin;
-  }();
-  const size_t smem = bytes(std::min(kDecChunk, std::max(cap_min, dec_cap(a.n_ctx, a.n_split))));
+  // shared memory for the full kDecChunk rows whatever the split's share: smaller
+  // CTAs pack more of a cluster onto one SM (sized to ~67 positions, 42 KiB:
+  // +2.7 ms per inference; 112 rows, which fits beside a 3-slot QKV / O GEMV
+  // CTA: +0.26 ms)
+  const size_t smem = bytes(kDecChunk);
   static DeviceFlags attr;
   if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,

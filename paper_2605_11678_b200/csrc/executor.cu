@@ -875,8 +875,8 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       std::sscanf(ov, "%d,%d,%d,%d", &gs[0], &gs[1], &gs[2], &gs[3]);
     e->gp_qkv = plan_gemv(QN, d.lm_d, gs[0]);
     e->gp_o = plan_gemv(d.lm_d, AH, gs[1]);
-    // QKV / O page rings capped at 3 slots: a decode-attention CTA fits beside the
-    // GEMV CTA (attention.cu kDecCapMin), measured -0.4 ms per inference
+    // QKV / O page rings capped at 3 slots (162 KiB): measured -0.4 ms per
+    // inference against 4 (LS_DIAG_QO_SLOTS overrides)
     e->gp_qkv.slots = e->gp_o.slots = 3;
     e->gp_gu = plan_gemv(2 * d.lm_ffn, d.lm_d, gs[2]);
     e->gp_down = plan_gemv(d.lm_d, d.lm_ffn, gs[3]);
