@@ -30,7 +30,7 @@ if [ -f "$PROF" ] && [ -z "$SKIP_NCU" ]; then
   python tools/ncu_kv.py $OUT/gemm_gu_prefill.ncu-rep > $OUT/gemm_gu_prefill_summary.txt 2>&1
   # the ViT flash attention (hd 72, per-image blocks) as launched in the step
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-      -k 'regex:flash_kernel<72' -s 2 -c 1 -o $OUT/flash_vit python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_flash_vit.log 2>&1
+      -k 'regex:flash_kernel<.int.72' -s 2 -c 1 -o $OUT/flash_vit python tools/profile_step.py --profile $PROF --runs 1 > $OUT/full_flash_vit.log 2>&1
   python tools/ncu_kv.py $OUT/flash_vit.ncu-rep > $OUT/flash_vit_summary.txt 2>&1
   ncu -i $OUT/flash_vit.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active,smsp__warp_issue_stalled_barrier_per_warp_active.pct,smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct >> $OUT/flash_vit_summary.txt 2>&1; head -20 $OUT/flash_vit_summary.txt
 fi
