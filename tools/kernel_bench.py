@@ -283,6 +283,13 @@ def main():
         res.append(bench_gemm(3072, 3456, 1152))
         res.append(bench_gemm(3072, 4352, 1152, K.GEMM_BF16_GELU))
         res.append(bench_gemm(3072, 1152, 4352, K.GEMM_RESID_F32))
+    if args.only == "prefill_ct":  # LM prefill / ViT shapes: plain tiles vs ECT pages decoded in the GEMM
+        for T, n, k, epi in ((1024, 6144, 4096, K.GEMM_BF16), (1024, 4096, 4096, K.GEMM_RESID_F32),
+                             (1024, 24576, 4096, K.GEMM_SILU_BF16), (1024, 4096, 12288, K.GEMM_RESID_F32),
+                             (3072, 3456, 1152, K.GEMM_BF16), (3072, 1152, 4352, K.GEMM_RESID_F32)):
+            res.append(bench_gemm(T, n, k, epi))
+            res.append(bench_gemm(T, n, k, epi, ct=True))
+        res.append(bench_ect_decode())
     if args.only == "prefill_gemm":
         res.append(bench_gemm(1024, 24576, 4096, K.GEMM_SILU_BF16))
         res.append(bench_gemm(1024, 4096, 12288, K.GEMM_RESID_F32))
