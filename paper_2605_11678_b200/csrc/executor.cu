@@ -935,6 +935,8 @@ int ls_exec_create(const ls_dims* dims, int32_t device, uint64_t cap_bytes, int3
       e->ex_kv_splits = flash_kv_splits(Te, d.ex_hq / e->ex_g_pack, e->ctx + Te, e->nsm);
       if (const char* ov = std::getenv("LS_DIAG_EX_KV_SPLITS")) e->ex_kv_splits = std::atoi(ov);  // diagnostics
       if (const char* ov = std::getenv("LS_DIAG_DEC_SPLITS")) e->diag_dec_splits = std::atoi(ov);
+      if (const char* ov = std::getenv("LS_DIAG_GU_SLOTS")) e->gp_gu.slots = std::atoi(ov);
+      if (const char* ov = std::getenv("LS_DIAG_DOWN_SLOTS")) e->gp_down.slots = std::atoi(ov);
       if (const char* ov = std::getenv("LS_DIAG_QO_SLOTS")) e->gp_qkv.slots = e->gp_o.slots = std::atoi(ov);
     }
     // ViT aliases start at vit_qkv (entry 2 of set 0)
