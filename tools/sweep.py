@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--out", default="profiles/r2_sweep.json")
     ap.add_argument("--no-prefetch", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=5)
+    ap.add_argument("--ks", default=None, help="comma-separated subset of k (must include 0)")
     args = ap.parse_args()
     import paper_2605_11678_b200 as ls
     from bench import max_resident_run
@@ -58,7 +59,9 @@ def main():
     placements = {"interleaved": lambda k: ls.interleaved_indices(k, L) if k < L else range(L),
                   "contiguous": lambda k: range(k)}
     import random
-    points = [(name, k) for name in placements for k in range(0, L + 1)]
+    ks_all = sorted({int(v) for v in args.ks.split(",")}) if args.ks else list(range(0, L + 1))
+    assert ks_all[0] == 0, "the sweep needs k = 0 (Eq. 10 intercept)"
+    points = [(name, k) for name in placements for k in ks_all]
     trials = {p: [] for p in points}
     rng = random.Random(0)
     for p in points:  # warm-up (graph capture) run of every point
@@ -74,7 +77,7 @@ def main():
             trials[p].append(eng.execute(pl, sim_cfg, inputs=inputs, record_timeline=False).total_ms)
     rows = []
     for name, fn in placements.items():
-        for k in range(0, L + 1):
+        for k in ks_all:
             pl = ls.Placement.of({"vlm": fn(k)}) if k else ls.Placement.empty()
             ms = trials[(name, k)]
             sim = ls.simulated_total(prof, pl, sim_cfg)
