@@ -574,7 +574,10 @@ def main():
     pred = None
     if not args.no_sweep and not tp:
         vlm = prof.module("vlm")
-        ks = [0, 8, 17, 26, 31, 35]
+        # vlm-only placements that fit the cap (at 8000 MiB the LM holds ~19 layers)
+        from paper_2605_11678_b200.planner import fixed_costs_mb
+        k_fit = int((prof.hardware.vram_mb - fixed_costs_mb(prof, sim_cfg)) // vlm.layer_mem_mb) - 1
+        ks = sorted({min(k, k_fit, vlm.layers - 1) for k in (0, 8, 17, 26, 31, 35)})
         measured = [(0, prof.calibration_total_s)]
         for k in ks[1:]:
             pl = ls.Placement({"vlm": ls.interleaved_indices(k, vlm.layers)})
